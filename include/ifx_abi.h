@@ -1,0 +1,163 @@
+/*
+ * ifx_abi.h — C-ABI of libinferix_b200.so, the B200-native (sm_100a) block-diffusion
+ * decode hot path. Plain pointers, sizes and opaque handles only: no torch types.
+ *
+ * The reference (/root/reference/pkg/src/inferix) is pure Python, so it has no FFI of its
+ * own; each entry point below names the Python interface it replaces (file:line). The
+ * Python façade in paper_2511_20714_b200/ binds these with ctypes.
+ *
+ * Conventions
+ *   - Every function returns int status: IFX_OK (0) or one of IFX_E* below. The message of
+ *     the last failure on the calling thread is available from ifx_last_error().
+ *   - Status codes map 1:1 onto the reference exception classes (errors.py:4-33).
+ *   - `stream` is a cudaStream_t passed as void*; kernels are enqueued on it, never synced.
+ *   - Device pointers are borrowed for the duration of the enqueued work.
+ *   - Token/row counts are int64.
+ */
+#ifndef IFX_ABI_H
+#define IFX_ABI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:4-33) -------------------------------------------------- */
+#define IFX_OK 0
+#define IFX_EDIM 1      /* DimensionError  (errors.py:8)  */
+#define IFX_EMASK 2     /* MaskError       (errors.py:12) */
+#define IFX_ECAPACITY 3 /* CapacityError   (errors.py:16) */
+#define IFX_ERANGE 4    /* OutOfRangeError (errors.py:20) */
+#define IFX_ECONFIG 5   /* ConfigError     (errors.py:24) */
+#define IFX_ECUDA 16    /* CUDA runtime/driver failure (no reference equivalent) */
+#define IFX_EUNSUPPORTED 17
+
+/* stream kinds (kvcache.py:75-76) */
+#define IFX_SELF_ATTN 0
+#define IFX_CROSS_ATTN 1
+
+/* element types of device buffers */
+#define IFX_F32 0
+#define IFX_BF16 1
+
+const char* ifx_last_error(void);
+int ifx_version(void);
+
+/* =====================================================================================
+ * Page table: bit-exact bookkeeping of KvCache (kvcache.py:105-404), host C++.
+ * Data lives in caller-owned device slabs addressed by stream position;
+ * the page table decides ids, tiers, LRU, eviction and block entries exactly as the
+ * reference does.
+ * ===================================================================================*/
+typedef struct ifx_pagetable ifx_pagetable;
+
+/* KvCache.__init__ / KvConfig.validate (kvcache.py:33-58,108-122) */
+int ifx_pt_create(int64_t num_layers, int64_t head_dim, int64_t page_len,
+                  int64_t capacity_pages_device, int64_t capacity_pages_host,
+                  ifx_pagetable** out);
+void ifx_pt_destroy(ifx_pagetable* pt);
+
+/* KvCache.append_block bookkeeping (kvcache.py:205-234).
+ * On success *out_written == t and the block entry is returned through the out params
+ * (page ids into out_pages[0..*out_npages), capacity page_cap). On IFX_ECAPACITY the
+ * reference has already packed *out_written tokens into pages (kvcache.py:210-223); the
+ * caller must still copy those rows. */
+int ifx_pt_append(ifx_pagetable* pt, int64_t layer, int kind, int64_t t, int64_t chunk_index,
+                  int64_t* out_block_id, int64_t* out_start, int64_t* out_written,
+                  int64_t* out_pages, int64_t page_cap, int64_t* out_npages);
+/* KvCache.offload_blocks (kvcache.py:236-256) */
+int ifx_pt_offload(ifx_pagetable* pt, const int64_t* block_ids, int64_t n, int64_t* out_moved);
+/* KvCache.evict_window (kvcache.py:258-285) */
+int ifx_pt_evict_window(ifx_pagetable* pt, int64_t keep_last_n_tokens, int64_t* out_freed);
+/* KvCache.clear_cross_attention (kvcache.py:287-299) */
+int ifx_pt_clear_cross(ifx_pagetable* pt, int64_t* out_cleared);
+/* fetch_range bookkeeping: restore-on-read + per-token access clock (kvcache.py:303-339) */
+int ifx_pt_touch_range(ifx_pagetable* pt, int64_t layer, int kind, int64_t start, int64_t end);
+/* fetch_indices bookkeeping (kvcache.py:341-353) */
+int ifx_pt_touch_indices(ifx_pagetable* pt, int64_t layer, int kind, const int64_t* idx,
+                         int64_t n);
+/* KvCache.addressable_range (kvcache.py:355-357) */
+int ifx_pt_range(const ifx_pagetable* pt, int64_t layer, int kind, int64_t* base,
+                 int64_t* total);
+/* KvCache.memory_stats counters (kvcache.py:359-372): out[0]=device pages, out[1]=host
+ * pages, out[2]=addressable tokens, out[3+l]=block entries of layer l */
+int ifx_pt_stats(const ifx_pagetable* pt, int64_t* out, int64_t out_cap);
+/* Full canonical state as a flat int64 record (layout in pagetable.cpp header comment);
+ * *out_len receives the needed length; call with out=NULL to size. */
+int ifx_pt_snapshot(const ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* out_len);
+
+/* =====================================================================================
+ * KV data kernels (HBM-bound)
+ * ===================================================================================*/
+/* K2 — page write for KvCache.append_block (kvcache.py:215-218): copy t rows of K and V
+ * (src row stride in elements) into slab rows [dst_row, dst_row + t). 128-bit vectorised.
+ * src/dst types: F32->F32, F32->BF16, BF16->BF16. */
+int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_type,
+                  void* k_slab, void* v_slab, int64_t slab_ld, int slab_type, int64_t dst_row,
+                  int64_t t, int64_t width, void* stream);
+/* K7 — gather for fetch_range / fetch_indices (kvcache.py:303-353): out[i] =
+ * slab[rows[i]] (rows==NULL: rows are first_row + i). Same dtype in and out. */
+int ifx_kv_gather(const void* k_slab, const void* v_slab, int64_t slab_ld, int type,
+                  const int64_t* rows, int64_t first_row, int64_t n, int64_t width,
+                  void* k_out, void* v_out, void* stream);
+
+/* =====================================================================================
+ * K1 — fused attention of a block's queries over [cached context ∥ the block's own K/V]
+ * (engine.py:176-182,206-210 + attention.py:74-94), tcgen05/TMEM/TMA, bf16 in, fp32
+ * accumulate. All heads of one [n_q, H*dh] Q matrix in one launch.
+ * ===================================================================================*/
+typedef struct ifx_attn_params {
+  /* Q: [n_q, heads*head_dim] bf16, row stride q_ld elements */
+  const void* q;
+  int64_t q_ld;
+  int64_t n_q;
+  /* segment 0 (cached context): rows [ctx_row0, ctx_row0 + n_ctx) of K/V slabs */
+  const void* k_ctx;
+  const void* v_ctx;
+  int64_t ctx_ld;    /* row stride (elements) of the context slabs */
+  int64_t ctx_rows;  /* physical rows of the context slabs (TMA extent) */
+  int64_t ctx_row0;
+  int64_t n_ctx;
+  /* segment 1 (the block's own K/V): rows [0, n_cur) */
+  const void* k_cur;
+  const void* v_cur;
+  int64_t cur_ld;
+  int64_t n_cur;
+  /* output [n_q, heads*head_dim] bf16, row stride o_ld */
+  void* o;
+  int64_t o_ld;
+  int64_t heads;
+  int64_t head_dim;  /* 64 or 128 */
+  float scale;       /* usually 1/sqrt(head_dim) (attention.py:87) */
+  /* optional dense visibility mask, uint8 [n_q, n_ctx + n_cur] row stride mask_ld
+   * (attention.py:89); NULL = every key visible (engine.py:209) */
+  const uint8_t* mask;
+  int64_t mask_ld;
+  /* optional split-KV partials for merge (attention.py:127-173): when lse != NULL the
+   * kernel also writes per (head,row) running max (log2 domain) and denominator. */
+  float* row_max;
+  float* row_sum;
+} ifx_attn_params;
+
+int ifx_attn_fwd(const ifx_attn_params* p, void* stream);
+/* test hook: variant 0 = P staged in smem (SS MMA, the default), 1 = P kept in TMEM (TS) */
+int ifx_attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream);
+
+/* Fused RMS-norm (engine.py:171-173) + optional time conditioning, fp32 in, bf16 out:
+ * y = bf16( (x + t*tvec) / sqrt(mean((x + t*tvec)^2) + eps) ). If x_out != NULL the
+ * conditioned fp32 row is also written there. tvec may be NULL. */
+int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
+                 float* x_out, void* y, void* stream);
+
+/* Ulysses re-shard pack/unpack (parallel.py:150-169): seq-sharded [n, H*dh] <-> per-peer
+ * contiguous [W][n, (H/W)*dh] chunks for a single all-to-all. */
+int ifx_ulysses_pack(const void* src, int64_t n, int64_t width, int64_t src_ld, int64_t world,
+                     int type, void* dst, void* stream);
+int ifx_ulysses_unpack(const void* src, int64_t n, int64_t width, int64_t world, int type,
+                       void* dst, int64_t dst_ld, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IFX_ABI_H */

@@ -1,0 +1,111 @@
+"""ctypes binding of libinferix_b200.so (include/ifx_abi.h).
+
+The library is built in-tree by `paper_2511_20714_b200._build` (or
+`__graft_entry__.build()`); there is no fallback: if it is missing, importing the
+hot-path modules raises. Status codes are mapped onto the reference exception
+classes (errors.py:4-33).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import (
+    CapacityError,
+    ConfigError,
+    CudaError,
+    DimensionError,
+    InferixError,
+    MaskError,
+    OutOfRangeError,
+)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libinferix_b200.so")
+
+OK, EDIM, EMASK, ECAPACITY, ERANGE, ECONFIG, ECUDA, EUNSUPPORTED = 0, 1, 2, 3, 4, 5, 16, 17
+SELF_ATTN, CROSS_ATTN = 0, 1
+F32, BF16 = 0, 1
+
+_ERRORS = {EDIM: DimensionError, EMASK: MaskError, ECAPACITY: CapacityError,
+           ERANGE: OutOfRangeError, ECONFIG: ConfigError, ECUDA: CudaError,
+           EUNSUPPORTED: DimensionError}
+
+# every symbol include/ifx_abi.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "ifx_last_error", "ifx_version",
+    "ifx_pt_create", "ifx_pt_destroy", "ifx_pt_append", "ifx_pt_offload", "ifx_pt_evict_window",
+    "ifx_pt_clear_cross", "ifx_pt_touch_range", "ifx_pt_touch_indices", "ifx_pt_range",
+    "ifx_pt_stats", "ifx_pt_snapshot",
+    "ifx_kv_append", "ifx_kv_gather",
+    "ifx_attn_fwd", "ifx_attn_fwd_variant",
+    "ifx_rms_bf16", "ifx_ulysses_pack", "ifx_ulysses_unpack",
+)
+
+
+class AttnParams(ctypes.Structure):
+    """Mirror of `ifx_attn_params` (include/ifx_abi.h)."""
+
+    _fields_ = [
+        ("q", ctypes.c_void_p), ("q_ld", ctypes.c_int64), ("n_q", ctypes.c_int64),
+        ("k_ctx", ctypes.c_void_p), ("v_ctx", ctypes.c_void_p), ("ctx_ld", ctypes.c_int64),
+        ("ctx_rows", ctypes.c_int64), ("ctx_row0", ctypes.c_int64), ("n_ctx", ctypes.c_int64),
+        ("k_cur", ctypes.c_void_p), ("v_cur", ctypes.c_void_p), ("cur_ld", ctypes.c_int64),
+        ("n_cur", ctypes.c_int64),
+        ("o", ctypes.c_void_p), ("o_ld", ctypes.c_int64),
+        ("heads", ctypes.c_int64), ("head_dim", ctypes.c_int64), ("scale", ctypes.c_float),
+        ("mask", ctypes.c_void_p), ("mask_ld", ctypes.c_int64),
+        ("row_max", ctypes.c_void_p), ("row_sum", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+I64 = ctypes.c_int64
+P = ctypes.c_void_p
+PI64 = ctypes.POINTER(ctypes.c_int64)
+
+
+def lib() -> ctypes.CDLL:
+    """Load the native library once; raise loudly if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                    f"g.build()'` (there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            L.ifx_last_error.restype = ctypes.c_char_p
+            L.ifx_pt_create.argtypes = [I64, I64, I64, I64, I64, ctypes.POINTER(P)]
+            L.ifx_pt_destroy.argtypes = [P]
+            L.ifx_pt_destroy.restype = None
+            L.ifx_pt_append.argtypes = [P, I64, ctypes.c_int, I64, I64, PI64, PI64, PI64, PI64, I64, PI64]
+            L.ifx_pt_offload.argtypes = [P, PI64, I64, PI64]
+            L.ifx_pt_evict_window.argtypes = [P, I64, PI64]
+            L.ifx_pt_clear_cross.argtypes = [P, PI64]
+            L.ifx_pt_touch_range.argtypes = [P, I64, ctypes.c_int, I64, I64]
+            L.ifx_pt_touch_indices.argtypes = [P, I64, ctypes.c_int, PI64, I64]
+            L.ifx_pt_range.argtypes = [P, I64, ctypes.c_int, PI64, PI64]
+            L.ifx_pt_stats.argtypes = [P, PI64, I64]
+            L.ifx_pt_snapshot.argtypes = [P, PI64, I64, PI64]
+            L.ifx_kv_append.argtypes = [P, P, I64, ctypes.c_int, P, P, I64, ctypes.c_int, I64, I64, I64, P]
+            L.ifx_kv_gather.argtypes = [P, P, I64, ctypes.c_int, P, I64, I64, I64, P, P, P]
+            L.ifx_attn_fwd.argtypes = [ctypes.POINTER(AttnParams), P]
+            L.ifx_attn_fwd_variant.argtypes = [ctypes.POINTER(AttnParams), ctypes.c_int, P]
+            L.ifx_rms_bf16.argtypes = [P, I64, I64, P, ctypes.c_float, P, P, P]
+            L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, ctypes.c_int, P, P]
+            L.ifx_ulysses_unpack.argtypes = [P, I64, I64, I64, ctypes.c_int, P, I64, P]
+            _lib = L
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == OK:
+        return
+    msg = lib().ifx_last_error().decode(errors="replace")
+    cls = _ERRORS.get(rc, InferixError)
+    raise cls(f"{what}: {msg}" if what else msg)

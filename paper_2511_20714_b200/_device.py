@@ -1,0 +1,102 @@
+"""Device-side helpers shared by the façades: stream handle, tensor coercion, launchers.
+
+PyTorch is plumbing here (device memory, streams, cuBLAS GEMMs); every hot-path
+kernel is ours and is reached through `_abi` (include/ifx_abi.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _abi
+from .errors import DimensionError
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2511_20714_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def to_device(x, dtype=torch.float32) -> torch.Tensor:
+    """numpy / list / tensor -> CUDA tensor of `dtype` (copy only if needed)."""
+    dev = require_cuda()
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=dtype)
+    a = np.asarray(x, dtype=np.float32)
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def row_ld(t: torch.Tensor) -> int:
+    """Row stride (elements) of a 2-D tensor whose rows are contiguous."""
+    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+        raise DimensionError("expected a 2-D tensor with contiguous rows")
+    return t.stride(0)
+
+
+def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
+             ctx_k: torch.Tensor | None = None, ctx_v: torch.Tensor | None = None,
+             ctx_row0: int = 0, n_ctx: int = 0,
+             cur_k: torch.Tensor | None = None, cur_v: torch.Tensor | None = None,
+             scale: float | None = None, mask: torch.Tensor | None = None,
+             row_max: torch.Tensor | None = None, row_sum: torch.Tensor | None = None,
+             variant: int = 0, stream=None) -> torch.Tensor:
+    """Enqueue K1 (attn_fwd_sm100.cu): out = softmax(q [ctx∥cur]^T * scale) [ctx∥cur].
+
+    q/out: [n_q, heads*head_dim] bf16 (row-strided views allowed). ctx_*: slabs whose rows
+    [ctx_row0, ctx_row0+n_ctx) are the cached keys. cur_*: [n_cur, heads*head_dim] views.
+    """
+    p = _abi.AttnParams()
+    p.q, p.q_ld, p.n_q = q.data_ptr(), row_ld(q), q.shape[0]
+    if n_ctx > 0:
+        p.k_ctx, p.v_ctx = ctx_k.data_ptr(), ctx_v.data_ptr()
+        p.ctx_ld, p.ctx_rows = row_ld(ctx_k), ctx_k.shape[0]
+        p.ctx_row0, p.n_ctx = ctx_row0, n_ctx
+    if cur_k is not None and cur_k.shape[0] > 0:
+        p.k_cur, p.v_cur = cur_k.data_ptr(), cur_v.data_ptr()
+        p.cur_ld, p.n_cur = row_ld(cur_k), cur_k.shape[0]
+    p.o, p.o_ld = out.data_ptr(), row_ld(out)
+    p.heads, p.head_dim = heads, head_dim
+    p.scale = (1.0 / math.sqrt(head_dim)) if scale is None else scale
+    if mask is not None:
+        p.mask, p.mask_ld = mask.data_ptr(), mask.stride(0)
+    if row_max is not None:
+        p.row_max, p.row_sum = row_max.data_ptr(), row_sum.data_ptr()
+    L = _abi.lib()
+    if variant == 0:
+        rc = L.ifx_attn_fwd(ctypes.byref(p), stream_ptr(stream))
+    else:
+        rc = L.ifx_attn_fwd_variant(ctypes.byref(p), variant, stream_ptr(stream))
+    _abi.check(rc, "attn_fwd")
+    return out
+
+
+def rms_bf16(x: torch.Tensor, out: torch.Tensor, tvec: torch.Tensor | None = None,
+             t: float = 0.0, x_out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Enqueue the fused RMS-norm (engine.py:171-173): out = bf16(rms(x + t*tvec))."""
+    rows, width = x.shape
+    _abi.check(_abi.lib().ifx_rms_bf16(x.data_ptr(), rows, width, ptr(tvec), float(t),
+                                       ptr(x_out), out.data_ptr(), stream_ptr(stream)), "rms")
+    return out
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return _abi.F32
+    if dt == torch.bfloat16:
+        return _abi.BF16
+    raise DimensionError(f"unsupported dtype {dt}")

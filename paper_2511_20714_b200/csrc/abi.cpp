@@ -1,0 +1,186 @@
+// abi.cpp — extern "C" entry points of libinferix_b200.so (declared in include/ifx_abi.h):
+// argument validation, TMA tensor-map encoding, status-code / last-error plumbing.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/ifx_abi.h"
+#include "attn_kernel.h"
+#include "common_host.h"
+#include "kv_kernels.h"
+
+namespace ifx {
+
+static thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static int cuda_fail(int err, const char* what) {
+  if (err == 0) return IFX_OK;
+  return fail(IFX_ECUDA, std::string(what) + ": " + cudaGetErrorString((cudaError_t)err));
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// bf16 matrix [rows, cols] with row stride ld (elements); box = 64 cols x 128 rows, SW128.
+static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+  std::memset(m, 0, sizeof(*m));
+  if (base == nullptr || rows <= 0) return IFX_OK;  // unused segment
+  auto fn = encode_fn();
+  if (!fn) return fail(IFX_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 2) & 15))
+    return fail(IFX_EDIM, "TMA operands need 16-byte aligned base and row stride");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(IFX_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return IFX_OK;
+}
+
+int attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream) {
+  if (p->head_dim != 64 && p->head_dim != 128)
+    return fail(IFX_EUNSUPPORTED, "head_dim must be 64 or 128");
+  if (p->heads < 1 || p->n_q < 0 || p->n_ctx < 0 || p->n_cur < 0)
+    return fail(IFX_EDIM, "bad attention sizes");
+  if (p->n_ctx + p->n_cur == 0 && p->n_q > 0) return fail(IFX_EMASK, "query row with no allowed key");
+  if (p->n_q == 0) return IFX_OK;
+  if (p->n_ctx > 0 && p->ctx_row0 + p->n_ctx > p->ctx_rows)
+    return fail(IFX_ERANGE, "context rows outside the slab");
+  const int64_t width = p->heads * p->head_dim;
+  if (p->n_q > INT32_MAX || p->ctx_rows > INT32_MAX || p->n_cur > INT32_MAX)
+    return fail(IFX_EDIM, "attention extents must fit int32");
+  AttnKernelArgs a;
+  std::memset(&a, 0, sizeof(a));
+  int rc;
+  if ((rc = make_map(&a.tm_q, p->q, p->n_q, width, p->q_ld))) return rc;
+  if (p->n_ctx > 0) {
+    if ((rc = make_map(&a.tm_kc, p->k_ctx, p->ctx_rows, width, p->ctx_ld))) return rc;
+    if ((rc = make_map(&a.tm_vc, p->v_ctx, p->ctx_rows, width, p->ctx_ld))) return rc;
+  }
+  if (p->n_cur > 0) {
+    if ((rc = make_map(&a.tm_kn, p->k_cur, p->n_cur, width, p->cur_ld))) return rc;
+    if ((rc = make_map(&a.tm_vn, p->v_cur, p->n_cur, width, p->cur_ld))) return rc;
+  }
+  a.n_q = (int)p->n_q;
+  a.n_ctx = (int)p->n_ctx;
+  a.n_cur = (int)p->n_cur;
+  a.ctx_row0 = (int)p->ctx_row0;
+  a.scale_log2 = p->scale * 1.4426950408889634f;
+  a.o = static_cast<__nv_bfloat16*>(p->o);
+  a.o_ld = p->o_ld;
+  a.mask = p->mask;
+  a.mask_ld = p->mask_ld;
+  a.row_max = p->row_max;
+  a.row_sum = p->row_sum;
+  int e = attn_fwd_launch(a, (int)p->head_dim, variant, (int)p->n_q, (int)p->heads,
+                          static_cast<cudaStream_t>(stream));
+  return cuda_fail(e, "attn_fwd launch");
+}
+
+}  // namespace ifx
+
+extern "C" {
+
+const char* ifx_last_error(void) { return ifx::g_last_error.c_str(); }
+int ifx_version(void) { return 1; }
+
+int ifx_attn_fwd(const ifx_attn_params* p, void* stream) {
+  return ifx::attn_fwd_variant(p, 0, stream);
+}
+
+// test hook: select the P-in-TMEM (TS MMA) variant of K1
+int ifx_attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream) {
+  return ifx::attn_fwd_variant(p, variant, stream);
+}
+
+int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_type, void* k_slab,
+                  void* v_slab, int64_t slab_ld, int slab_type, int64_t dst_row, int64_t t,
+                  int64_t width, void* stream) {
+  if (t < 0 || width <= 0) return ifx::fail(IFX_EDIM, "bad append sizes");
+  if (t == 0) return IFX_OK;
+  if (src_type == IFX_BF16 && slab_type == IFX_F32)
+    return ifx::fail(IFX_EUNSUPPORTED, "bf16 -> fp32 append not supported");
+  const int esz = slab_type == IFX_BF16 ? 2 : 4;
+  if ((width * esz) % 16 || (src_type == IFX_F32 && slab_type == IFX_BF16 && width % 8))
+    return ifx::fail(IFX_EDIM, "row width must be a multiple of 16 bytes");
+  const int ssz = src_type == IFX_BF16 ? 2 : 4;
+  if ((reinterpret_cast<uintptr_t>(k_src) | reinterpret_cast<uintptr_t>(v_src) |
+       reinterpret_cast<uintptr_t>(k_slab) | reinterpret_cast<uintptr_t>(v_slab)) & 15 ||
+      (src_ld * ssz) % 16 || (slab_ld * esz) % 16)
+    return ifx::fail(IFX_EDIM, "append operands must be 16-byte aligned");
+  int e = ifx::kv_append_launch(k_src, v_src, src_ld, src_type == IFX_BF16, k_slab, v_slab,
+                                slab_ld, slab_type == IFX_BF16, dst_row, t, width,
+                                static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "kv_append launch");
+}
+
+int ifx_kv_gather(const void* k_slab, const void* v_slab, int64_t slab_ld, int type,
+                  const int64_t* rows, int64_t first_row, int64_t n, int64_t width, void* k_out,
+                  void* v_out, void* stream) {
+  if (n < 0 || width <= 0) return ifx::fail(IFX_EDIM, "bad gather sizes");
+  if (n == 0) return IFX_OK;
+  const int esz = type == IFX_BF16 ? 2 : 4;
+  if ((width * esz) % 16 || (slab_ld * esz) % 16)
+    return ifx::fail(IFX_EDIM, "row width must be a multiple of 16 bytes");
+  int e = ifx::kv_gather_launch(k_slab, v_slab, slab_ld, esz, rows, first_row, n, width, k_out,
+                                v_out, static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "kv_gather launch");
+}
+
+int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
+                 float* x_out, void* y, void* stream) {
+  if (rows < 0 || width <= 0 || width % 4) return ifx::fail(IFX_EDIM, "rms width must be a multiple of 4");
+  if (rows == 0) return IFX_OK;
+  int e = ifx::rms_launch(x, rows, width, tvec, t, x_out, y, static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "rms launch");
+}
+
+int ifx_ulysses_pack(const void* src, int64_t n, int64_t width, int64_t src_ld, int64_t world,
+                     int type, void* dst, void* stream) {
+  const int esz = type == IFX_BF16 ? 2 : 4;
+  if (world < 1 || width % world) return ifx::fail(IFX_EDIM, "width not divisible by world");
+  const int64_t chunk_b = width / world * esz;
+  if (chunk_b % 16 || (src_ld * esz) % 16) return ifx::fail(IFX_EDIM, "chunks must be 16-byte multiples");
+  if (n == 0) return IFX_OK;
+  int e = ifx::ulysses_launch(src, dst, n, world, chunk_b, src_ld * esz, true,
+                              static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "ulysses pack");
+}
+
+int ifx_ulysses_unpack(const void* src, int64_t n, int64_t width, int64_t world, int type,
+                       void* dst, int64_t dst_ld, void* stream) {
+  const int esz = type == IFX_BF16 ? 2 : 4;
+  if (world < 1 || width % world) return ifx::fail(IFX_EDIM, "width not divisible by world");
+  const int64_t chunk_b = width / world * esz;
+  if (chunk_b % 16 || (dst_ld * esz) % 16) return ifx::fail(IFX_EDIM, "chunks must be 16-byte multiples");
+  if (n == 0) return IFX_OK;
+  int e = ifx::ulysses_launch(src, dst, n, world, chunk_b, dst_ld * esz, false,
+                              static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "ulysses unpack");
+}
+
+}  // extern "C"

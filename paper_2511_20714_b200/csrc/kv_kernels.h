@@ -1,0 +1,18 @@
+// kv_kernels.h — launchers of the HBM-bound kernels in kv_ops.cu (return cudaError_t).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ifx {
+int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf16, void* kd,
+                     void* vd, int64_t dst_ld, int dst_bf16, int64_t dst_row, int64_t t,
+                     int64_t width, cudaStream_t st);
+int kv_gather_launch(const void* ks, const void* vs, int64_t ld, int esz, const int64_t* rows,
+                     int64_t first_row, int64_t n, int64_t width, void* ko, void* vo,
+                     cudaStream_t st);
+int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
+               float* x_out, void* y, cudaStream_t st);
+int ulysses_launch(const void* src, void* dst, int64_t n, int64_t world, int64_t chunk_bytes,
+                   int64_t ld_bytes, bool pack, cudaStream_t st);
+}  // namespace ifx

@@ -1,0 +1,205 @@
+// kv_ops.cu — HBM-bound kernels around the attention: K2 page write (append), K7 gather,
+// fused RMS-norm -> bf16, Ulysses pack/unpack. All use 16-byte vector accesses and grids
+// sized in multiples of the SM count (grid-stride loops), per the B200 rules in DESIGN.md.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kv_kernels.h"
+
+namespace ifx {
+namespace {
+
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ uint4 ld_nc(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_na(void* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w));
+}
+__device__ __forceinline__ uint32_t f2_to_bf2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+
+// ---- K2: page write. One 16-byte destination vector per thread-iteration. -------------
+// same-type copy: vec = 16 bytes of src == 16 bytes of dst
+__global__ void append_same(const uint8_t* __restrict__ ks, const uint8_t* __restrict__ vs,
+                            int64_t src_ld_b, uint8_t* __restrict__ kd, uint8_t* __restrict__ vd,
+                            int64_t dst_ld_b, int64_t t, int64_t row_vecs) {
+  const int64_t total = t * row_vecs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool is_v = i >= total;
+    const int64_t e = is_v ? i - total : i;
+    const int64_t r = e / row_vecs, c = e - r * row_vecs;
+    const uint8_t* s = (is_v ? vs : ks) + r * src_ld_b + c * 16;
+    uint8_t* d = (is_v ? vd : kd) + r * dst_ld_b + c * 16;
+    st_na(d, ld_nc(s));
+  }
+}
+// fp32 -> bf16: each thread reads 32 B (8 floats) and writes 16 B
+__global__ void append_f32_bf16(const float* __restrict__ ks, const float* __restrict__ vs,
+                                int64_t src_ld, __nv_bfloat16* __restrict__ kd,
+                                __nv_bfloat16* __restrict__ vd, int64_t dst_ld, int64_t t,
+                                int64_t row_vecs) {
+  const int64_t total = t * row_vecs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool is_v = i >= total;
+    const int64_t e = is_v ? i - total : i;
+    const int64_t r = e / row_vecs, c = e - r * row_vecs;
+    const float* s = (is_v ? vs : ks) + r * src_ld + c * 8;
+    const uint4 a = ld_nc(s), b = ld_nc(s + 4);
+    uint4 o;
+    o.x = f2_to_bf2(__uint_as_float(a.x), __uint_as_float(a.y));
+    o.y = f2_to_bf2(__uint_as_float(a.z), __uint_as_float(a.w));
+    o.z = f2_to_bf2(__uint_as_float(b.x), __uint_as_float(b.y));
+    o.w = f2_to_bf2(__uint_as_float(b.z), __uint_as_float(b.w));
+    st_na((is_v ? vd : kd) + r * dst_ld + c * 8, o);
+  }
+}
+
+// ---- K7: gather rows (explicit list or contiguous) ------------------------------------
+__global__ void gather_rows(const uint8_t* __restrict__ ks, const uint8_t* __restrict__ vs,
+                            int64_t ld_b, const int64_t* __restrict__ rows, int64_t first_row,
+                            int64_t n, int64_t row_vecs, uint8_t* __restrict__ ko,
+                            uint8_t* __restrict__ vo, int64_t row_b) {
+  const int64_t total = n * row_vecs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool is_v = i >= total;
+    const int64_t e = is_v ? i - total : i;
+    const int64_t r = e / row_vecs, c = e - r * row_vecs;
+    const int64_t src_r = rows ? rows[r] : first_row + r;
+    const uint4 v = ld_nc((is_v ? vs : ks) + src_r * ld_b + c * 16);
+    *reinterpret_cast<uint4*>((is_v ? vo : ko) + r * row_b + c * 16) = v;
+  }
+}
+
+// ---- fused RMS norm (engine.py:171-173), one warp per row ------------------------------
+__global__ void rms_bf16_kernel(const float* __restrict__ x, int64_t rows, int64_t width,
+                                const float* __restrict__ tvec, float t, float* __restrict__ x_out,
+                                __nv_bfloat16* __restrict__ y) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += warps) {
+    const float* xr = x + r * width;
+    float ss = 0.f;
+    for (int64_t c = lane * 4; c < width; c += 128) {
+      float4 v = *reinterpret_cast<const float4*>(xr + c);
+      if (tvec) {
+        const float4 tv = *reinterpret_cast<const float4*>(tvec + c);
+        v.x += t * tv.x; v.y += t * tv.y; v.z += t * tv.z; v.w += t * tv.w;
+      }
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float inv = rsqrtf(ss / (float)width + 1e-6f);
+    for (int64_t c = lane * 4; c < width; c += 128) {
+      float4 v = *reinterpret_cast<const float4*>(xr + c);
+      if (tvec) {
+        const float4 tv = *reinterpret_cast<const float4*>(tvec + c);
+        v.x += t * tv.x; v.y += t * tv.y; v.z += t * tv.z; v.w += t * tv.w;
+        if (x_out) *reinterpret_cast<float4*>(x_out + r * width + c) = v;
+      }
+      uint2 o;
+      o.x = f2_to_bf2(v.x * inv, v.y * inv);
+      o.y = f2_to_bf2(v.z * inv, v.w * inv);
+      *reinterpret_cast<uint2*>(y + r * width + c) = o;
+    }
+  }
+}
+
+// ---- Ulysses: [n, W*w] <-> [W][n, w] (16-byte vectors) ---------------------------------
+__global__ void ulysses_transpose(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                  int64_t n, int64_t world, int64_t chunk_vecs, int64_t ld_b,
+                                  bool pack) {
+  const int64_t total = n * world * chunk_vecs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % chunk_vecs;
+    const int64_t rr = i / chunk_vecs;
+    const int64_t r = rr % n, p = rr / n;  // p = peer
+    const int64_t packed = ((p * n + r) * chunk_vecs + c) * 16;
+    const int64_t rowmaj = r * ld_b + (p * chunk_vecs + c) * 16;
+    if (pack)
+      *reinterpret_cast<uint4*>(dst + packed) = ld_nc(src + rowmaj);
+    else
+      *reinterpret_cast<uint4*>(dst + rowmaj) = ld_nc(src + packed);
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  int64_t blocks = (work + threads - 1) / threads;
+  const int64_t cap = (int64_t)kSMs * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+}  // namespace
+
+int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf16, void* kd,
+                     void* vd, int64_t dst_ld, int dst_bf16, int64_t dst_row, int64_t t,
+                     int64_t width, cudaStream_t st) {
+  const int threads = 256;
+  if (!src_bf16 && dst_bf16) {
+    const int64_t rv = width / 8;
+    auto* k = static_cast<__nv_bfloat16*>(kd) + dst_row * dst_ld;
+    auto* v = static_cast<__nv_bfloat16*>(vd) + dst_row * dst_ld;
+    append_f32_bf16<<<grid_for(2 * t * rv, threads), threads, 0, st>>>(
+        static_cast<const float*>(ks), static_cast<const float*>(vs), src_ld, k, v, dst_ld, t, rv);
+  } else {
+    const int esz = dst_bf16 ? 2 : 4;
+    const int64_t rv = width * esz / 16;
+    auto* k = static_cast<uint8_t*>(kd) + dst_row * dst_ld * esz;
+    auto* v = static_cast<uint8_t*>(vd) + dst_row * dst_ld * esz;
+    append_same<<<grid_for(2 * t * rv, threads), threads, 0, st>>>(
+        static_cast<const uint8_t*>(ks), static_cast<const uint8_t*>(vs), src_ld * esz, k, v,
+        dst_ld * esz, t, rv);
+  }
+  return (int)cudaGetLastError();
+}
+
+int kv_gather_launch(const void* ks, const void* vs, int64_t ld, int esz, const int64_t* rows,
+                     int64_t first_row, int64_t n, int64_t width, void* ko, void* vo,
+                     cudaStream_t st) {
+  const int threads = 256;
+  const int64_t rv = width * esz / 16;
+  gather_rows<<<grid_for(2 * n * rv, threads), threads, 0, st>>>(
+      static_cast<const uint8_t*>(ks), static_cast<const uint8_t*>(vs), ld * esz, rows, first_row,
+      n, rv, static_cast<uint8_t*>(ko), static_cast<uint8_t*>(vo), width * esz);
+  return (int)cudaGetLastError();
+}
+
+int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
+               float* x_out, void* y, cudaStream_t st) {
+  const int threads = 256;
+  const int64_t blocks = (rows + 7) / 8;
+  const int g = (int)(blocks < (int64_t)kSMs * 16 ? blocks : (int64_t)kSMs * 16);
+  rms_bf16_kernel<<<g, threads, 0, st>>>(x, rows, width, tvec, t, x_out,
+                                         static_cast<__nv_bfloat16*>(y));
+  return (int)cudaGetLastError();
+}
+
+int ulysses_launch(const void* src, void* dst, int64_t n, int64_t world, int64_t chunk_bytes,
+                   int64_t ld_bytes, bool pack, cudaStream_t st) {
+  const int threads = 256;
+  const int64_t cv = chunk_bytes / 16;
+  ulysses_transpose<<<grid_for(n * world * cv, threads), threads, 0, st>>>(
+      static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), n, world, cv, ld_bytes, pack);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace ifx

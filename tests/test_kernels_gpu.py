@@ -1,0 +1,164 @@
+"""GPU numerics of the individual kernels vs plain PyTorch fp32 references.
+
+K1 attention (both P paths), K2 append, K7 gather, fused RMS, Ulysses pack/unpack.
+"""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref_attn(q, k, v, heads, scale=None, mask=None):
+    n, d = q.shape
+    dh = d // heads
+    scale = scale or 1.0 / math.sqrt(dh)
+    qf, kf, vf = q.float(), k.float(), v.float()
+    outs = []
+    for h in range(heads):
+        sl = slice(h * dh, (h + 1) * dh)
+        s = (qf[:, sl] @ kf[:, sl].T) * scale
+        if mask is not None:
+            s = s.masked_fill(~mask, float("-inf"))
+        outs.append(torch.softmax(s, dim=1) @ vf[:, sl])
+    return torch.cat(outs, dim=1)
+
+
+CASES = [
+    # heads, head_dim, n_q, n_ctx, ctx_row0, n_cur
+    (2, 64, 128, 0, 0, 128),
+    (1, 128, 128, 0, 0, 128),
+    (4, 64, 768, 768, 0, 768),
+    (3, 128, 200, 300, 5, 77),
+    (2, 128, 130, 1000, 17, 0),
+    (12, 128, 520, 384, 0, 520),
+    (1, 128, 64, 3, 0, 0),
+    (2, 64, 33, 0, 0, 2),
+]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("case", CASES)
+def test_attention_matches_torch(case, variant):
+    from paper_2511_20714_b200._device import attn_fwd
+
+    heads, hd, n_q, n_ctx, row0, n_cur = case
+    d = heads * hd
+    g = torch.Generator(device="cuda").manual_seed(hash(case) % 2**31)
+    dev = "cuda"
+    q = torch.randn(n_q, d, device=dev, generator=g).bfloat16()
+    slab_rows = row0 + n_ctx + 40
+    ks = torch.randn(slab_rows, d, device=dev, generator=g).bfloat16()
+    vs = torch.randn(slab_rows, d, device=dev, generator=g).bfloat16()
+    qkv = torch.randn(max(n_cur, 1), 3 * d, device=dev, generator=g).bfloat16()[:n_cur]
+    kc, vc = qkv[:, d:2 * d], qkv[:, 2 * d:]
+    out = torch.empty(n_q, d, device=dev, dtype=torch.bfloat16)
+    attn_fwd(q, heads, hd, out, ks, vs, row0, n_ctx, kc if n_cur else None, vc if n_cur else None,
+             variant=variant)
+    torch.cuda.synchronize()
+    k = torch.cat([ks[row0:row0 + n_ctx], kc])
+    v = torch.cat([vs[row0:row0 + n_ctx], vc])
+    ref = _ref_attn(q, k, v, heads)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_attention_large_scores_and_masks(variant):
+    """Large logits exercise the lazy-rescale path; a dense mask exercises masking."""
+    from paper_2511_20714_b200._device import attn_fwd
+
+    heads, hd, n_q, n = 2, 128, 256, 700
+    d = heads * hd
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q = (torch.randn(n_q, d, device="cuda", generator=g) * 3).bfloat16()
+    k = (torch.randn(n, d, device="cuda", generator=g) * 3).bfloat16()
+    # increasing key scale so the running max keeps growing across tiles
+    k = (k.float() * torch.linspace(0.2, 2.0, n, device="cuda")[:, None]).bfloat16()
+    v = torch.randn(n, d, device="cuda", generator=g).bfloat16()
+    mask = torch.rand(n_q, n, device="cuda", generator=g) < 0.6
+    mask[:, 0] = True
+    out = torch.empty(n_q, d, device="cuda", dtype=torch.bfloat16)
+    attn_fwd(q, heads, hd, out, k, v, 0, n, variant=variant)
+    torch.cuda.synchronize()
+    ref = _ref_attn(q, k, v, heads)
+    assert (out.float() - ref).abs().max().item() < 3e-2
+    m8 = mask.to(torch.uint8).contiguous()
+    attn_fwd(q, heads, hd, out, k, v, 0, n, mask=m8, variant=variant)
+    torch.cuda.synchronize()
+    ref = _ref_attn(q, k, v, heads, mask=mask)
+    assert (out.float() - ref).abs().max().item() < 3e-2
+
+
+def test_kv_append_and_gather_bit_exact():
+    from paper_2511_20714_b200 import _abi
+    from paper_2511_20714_b200._device import stream_ptr
+
+    L = _abi.lib()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for src_dt, dst_dt in [(torch.float32, torch.float32), (torch.float32, torch.bfloat16),
+                           (torch.bfloat16, torch.bfloat16)]:
+        t, w = 37, 256
+        src = torch.randn(t, 3 * w, device="cuda", generator=g).to(src_dt)
+        ks, vs = src[:, w:2 * w], src[:, 2 * w:]
+        kd = torch.zeros(100, w, device="cuda", dtype=dst_dt)
+        vd = torch.zeros(100, w, device="cuda", dtype=dst_dt)
+        code = lambda dt: _abi.BF16 if dt == torch.bfloat16 else _abi.F32
+        _abi.check(L.ifx_kv_append(ks.data_ptr(), vs.data_ptr(), 3 * w, code(src_dt), kd.data_ptr(),
+                                   vd.data_ptr(), w, code(dst_dt), 11, t, w, stream_ptr()))
+        torch.cuda.synchronize()
+        assert torch.equal(kd[11:11 + t], ks.to(dst_dt))
+        assert torch.equal(vd[11:11 + t], vs.to(dst_dt))
+        assert kd[:11].abs().sum() == 0 and kd[11 + t:].abs().sum() == 0
+        rows = torch.tensor([12, 11, 40, 12], device="cuda", dtype=torch.int64)
+        ko = torch.empty(4, w, device="cuda", dtype=dst_dt)
+        vo = torch.empty_like(ko)
+        _abi.check(L.ifx_kv_gather(kd.data_ptr(), vd.data_ptr(), w, code(dst_dt), rows.data_ptr(),
+                                   0, 4, w, ko.data_ptr(), vo.data_ptr(), stream_ptr()))
+        torch.cuda.synchronize()
+        assert torch.equal(ko, kd[rows]) and torch.equal(vo, vd[rows])
+
+
+def test_rms_matches_torch():
+    from paper_2511_20714_b200._device import rms_bf16
+
+    x = torch.randn(777, 1536, device="cuda")
+    tv = torch.randn(1536, device="cuda")
+    y = torch.empty(777, 1536, device="cuda", dtype=torch.bfloat16)
+    xo = torch.empty_like(x)
+    rms_bf16(x, y, tv, 0.75, xo)
+    torch.cuda.synchronize()
+    xc = x + 0.75 * tv
+    ref = xc / torch.sqrt((xc * xc).mean(-1, keepdim=True) + 1e-6)
+    assert torch.allclose(xo, xc, atol=1e-5)
+    assert (y.float() - ref).abs().max().item() < 2e-2
+
+
+def test_ulysses_pack_unpack_roundtrip():
+    from paper_2511_20714_b200 import _abi
+    from paper_2511_20714_b200._device import stream_ptr
+
+    L = _abi.lib()
+    n, width, world = 93, 1536, 4
+    x = torch.randn(n, width, device="cuda").bfloat16()
+    packed = torch.empty(world, n, width // world, device="cuda", dtype=torch.bfloat16)
+    _abi.check(L.ifx_ulysses_pack(x.data_ptr(), n, width, width, world, _abi.BF16,
+                                  packed.data_ptr(), stream_ptr()))
+    back = torch.empty_like(x)
+    _abi.check(L.ifx_ulysses_unpack(packed.data_ptr(), n, width, world, _abi.BF16,
+                                    back.data_ptr(), width, stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(packed, x.view(n, world, width // world).permute(1, 0, 2))
+    assert torch.equal(back, x)
+
+
+def test_addmm_out_dtype_fp32_residual():
+    """The engine keeps the residual stream fp32 with bf16 GEMM inputs."""
+    a = torch.randn(64, 128, device="cuda").bfloat16()
+    b = torch.randn(128, 32, device="cuda").bfloat16()
+    x = torch.randn(64, 32, device="cuda")
+    y = torch.mm(a, b, out_dtype=torch.float32)
+    assert y.dtype == torch.float32
+    assert torch.allclose(y, a.float() @ b.float(), atol=1e-3)

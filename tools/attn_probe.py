@@ -1,0 +1,48 @@
+"""Quick K1 timing at the Wan-1.3B shape (T=4680, H=12, dh=128) for b cached blocks.
+
+    python tools/attn_probe.py [--variant 0|1]
+
+Prints algorithmic TFLOP/s = 4*T*(C+T)*D / kernel time (CUDA events, warm, inputs > L2).
+"""
+
+import argparse
+import json
+
+import torch
+
+from paper_2511_20714_b200._device import attn_fwd
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--iters", type=int, default=10)
+    args = ap.parse_args()
+    T, H, dh = 4680, 12, 128
+    D = H * dh
+    res = []
+    for b in (0, 1, 3, 6, 20):
+        C = b * T
+        qkv = torch.randn(T, 3 * D, device="cuda").bfloat16()
+        ks = torch.randn(max(C, 1), D, device="cuda").bfloat16()
+        vs = torch.randn(max(C, 1), D, device="cuda").bfloat16()
+        out = torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
+        f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:],
+                             variant=args.variant)
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.iters):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.iters
+        flops = 4.0 * T * (C + T) * D
+        res.append({"b": b, "ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1)})
+        print(json.dumps(res[-1]), flush=True)
+
+
+if __name__ == "__main__":
+    main()
