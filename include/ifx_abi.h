@@ -141,7 +141,7 @@ typedef struct ifx_attn_params {
 } ifx_attn_params;
 
 int ifx_attn_fwd(const ifx_attn_params* p, void* stream);
-/* test hook: variant 0 = P staged in smem (SS MMA, the default), 1 = P kept in TMEM (TS) */
+/* test hook: variant 0 = P staged in smem (SS MMA), 1 = P kept in TMEM (TS MMA, the default) */
 int ifx_attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream);
 
 /* Fused RMS-norm (engine.py:171-173) + optional time conditioning, fp32 in, bf16 out:

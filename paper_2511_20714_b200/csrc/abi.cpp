@@ -108,11 +108,12 @@ extern "C" {
 const char* ifx_last_error(void) { return ifx::g_last_error.c_str(); }
 int ifx_version(void) { return 1; }
 
+// default: P kept in TMEM (TS MMA) — measured faster than staging P in smem
 int ifx_attn_fwd(const ifx_attn_params* p, void* stream) {
-  return ifx::attn_fwd_variant(p, 0, stream);
+  return ifx::attn_fwd_variant(p, 1, stream);
 }
 
-// test hook: select the P-in-TMEM (TS MMA) variant of K1
+// test hook: 0 = P staged in smem (SS MMA), 1 = P in TMEM (TS MMA)
 int ifx_attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream) {
   return ifx::attn_fwd_variant(p, variant, stream);
 }

@@ -1,0 +1,573 @@
+"""Generate-and-cache block-diffusion loop on B200 — drop-in for `inferix.engine`.
+
+Reference: /root/reference/pkg/src/inferix/engine.py. Same public surface (ModelConfig,
+DenoiseSchedule, GenerationRequest, GeneratedBlock, ToyModel/build_model, embed_prompt,
+denoise_step, decode_frames, generate_block, default_kv_config, Engine,
+generate_sequence, Pipeline registry) and the same semantics:
+  * weights drawn from one PCG64 stream in the reference's order (engine.py:120-144),
+    noise from default_rng([seed, chunk]) (engine.py:280-282) — bit-identical inputs;
+  * S Euler steps then a clean t=0 pass whose K/V are appended to the cache
+    (engine.py:285-312); prompt switches clear the cross streams (engine.py:382-391);
+    window eviction after each block (engine.py:403-404);
+  * KV-cache bookkeeping calls in the reference's order (context fetch once per block,
+    engine.py:228-250) so page ids / tiers / access clock match bit-for-bit.
+
+What changes is where it runs: one CUDA stream; per layer a fused RMS-norm kernel, one
+bf16 QKV GEMM (cuBLAS), K1 attention reading the cached context IN PLACE from the HBM
+slab plus the block's own K/V straight out of the QKV buffer (no concat, no gather),
+K2 page write on the clean pass, fp32 residual stream (GEMMs with fp32 output).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+import threading
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from ._device import attn_fwd, require_cuda, rms_bf16
+from .errors import ConfigError, DimensionError
+from .kvcache import CROSS_ATTN, SELF_ATTN, KvCache, KvConfig
+
+LAYER_FIELDS = ("wq", "wk", "wv", "wo", "cq", "ck", "cv", "co", "w1", "w2")  # engine.py:131-138
+
+
+@dataclass
+class ModelConfig:
+    """engine.py:29-48."""
+    layers: int = 2
+    heads: int = 2
+    head_dim: int = 8
+    block_len: int = 16
+    frame_shape: tuple = (16, 16)
+    prompt_dim: int = 16
+    weight_seed: int = 0
+
+    def validate(self):
+        for name in ("layers", "heads", "head_dim", "block_len", "prompt_dim"):
+            if getattr(self, name) < 1:
+                raise ConfigError(f"{name} must be >= 1")
+        if self.frame_shape[0] < 1 or self.frame_shape[1] < 1:
+            raise ConfigError("frame_shape must be positive")
+
+    @property
+    def model_dim(self) -> int:
+        return self.heads * self.head_dim
+
+
+@dataclass
+class DenoiseSchedule:
+    """engine.py:51-62."""
+    steps: list
+    step_scale: float = 0.5
+
+    def validate(self):
+        if not self.steps:
+            raise ConfigError("schedule needs at least one step")
+        if any(t <= 0 for t in self.steps):
+            raise ConfigError("noise levels must be > 0")
+        if any(a <= b for a, b in zip(self.steps, self.steps[1:])):
+            raise ConfigError("noise levels must be strictly decreasing")
+
+
+@dataclass
+class GenerationRequest:
+    """engine.py:65-87."""
+    num_blocks: int
+    schedule: DenoiseSchedule
+    seed: int = 0
+    prompt_schedule: list = field(default_factory=lambda: [(0, "a quiet scene")])
+    kv_window: int | None = None
+
+    def validate(self):
+        if self.num_blocks < 1:
+            raise ConfigError("num_blocks must be >= 1")
+        self.schedule.validate()
+        if not self.prompt_schedule or self.prompt_schedule[0][0] != 0:
+            raise ConfigError("prompt_schedule must start at chunk 0")
+        chunks = [c for c, _ in self.prompt_schedule]
+        if any(a >= b for a, b in zip(chunks, chunks[1:])):
+            raise ConfigError("prompt_schedule chunks must be strictly increasing")
+        if any(not text for _, text in self.prompt_schedule):
+            raise ConfigError("prompts must be nonempty")
+        if self.kv_window is not None and self.kv_window < 0:
+            raise ConfigError("kv_window must be >= 0")
+
+
+@dataclass
+class GeneratedBlock:
+    """engine.py:90-95 (latent as host numpy fp32, frames as uint8 [h, w] per token)."""
+    chunk_index: int
+    latent: np.ndarray
+    frames: list
+    prompt_in_effect: str
+
+
+def padded_head_dim(head_dim: int) -> int:
+    """K1 runs 64- or 128-wide heads; narrower heads are zero-padded (exact: zero q/k
+    columns do not change q.k, zero V columns give zero outputs that meet zero rows of
+    wo/co). The softmax scale stays 1/sqrt(head_dim)."""
+    if head_dim <= 64:
+        return 64
+    if head_dim <= 128:
+        return 128
+    raise ConfigError("head_dim > 128 is not supported by the B200 attention kernel")
+
+
+def _pad_cols(w: torch.Tensor, heads: int, dh: int, dhp: int) -> torch.Tensor:
+    if dh == dhp:
+        return w
+    out = w.new_zeros(w.shape[0], heads, dhp)
+    out[:, :, :dh] = w.view(w.shape[0], heads, dh)
+    return out.view(w.shape[0], heads * dhp)
+
+
+def _pad_rows(w: torch.Tensor, heads: int, dh: int, dhp: int) -> torch.Tensor:
+    if dh == dhp:
+        return w
+    out = w.new_zeros(heads, dhp, w.shape[1])
+    out[:, :dh] = w.view(heads, dh, w.shape[1])
+    return out.view(heads * dhp, w.shape[1])
+
+
+class _LayerWeights:
+    """Device weights of one layer: fused [D, 3Dp] QKV, bf16 GEMM operands (Dp = heads x
+    padded head width); the prompt projections ck/cv stay fp32 (they run once per prompt,
+    engine.py:224-225)."""
+
+    def __init__(self, w: dict, dev, heads: int, dh: int, dhp: int):
+        f32 = lambda a: torch.as_tensor(a).to(dev, torch.float32)  # noqa: E731
+        cols = lambda a: _pad_cols(f32(a), heads, dh, dhp)  # noqa: E731
+        rows = lambda a: _pad_rows(f32(a), heads, dh, dhp)  # noqa: E731
+        bf = torch.bfloat16
+        self.wqkv = torch.cat([cols(w["wq"]), cols(w["wk"]), cols(w["wv"])], dim=1).to(bf).contiguous()
+        self.wo, self.cq, self.co = rows(w["wo"]).to(bf), cols(w["cq"]).to(bf), rows(w["co"]).to(bf)
+        self.w1, self.w2 = f32(w["w1"]).to(bf), f32(w["w2"]).to(bf)
+        self.ck, self.cv = cols(w["ck"]).contiguous(), cols(w["cv"]).contiguous()
+
+
+class ToyModel:
+    """Seeded toy transformer denoiser (engine.py:112-150) with device-resident weights.
+
+    weights="reference": identical PCG64 draws to the reference (bit-identical fp32
+    source, then cast to bf16 for the GEMMs). weights="device": torch.randn on the GPU
+    (same shapes / scales; for the 14B-shaped configs where host generation of ~10^10
+    normals is impractical — not bit-comparable with the reference)."""
+
+    def __init__(self, config: ModelConfig, weights: str = "reference"):
+        config.validate()
+        self.config = config
+        dev = require_cuda()
+        d, p = config.model_dim, config.prompt_dim
+        h, wd = config.frame_shape
+        self.dh_pad = padded_head_dim(config.head_dim)
+        lw = lambda ws: _LayerWeights(ws, dev, config.heads, config.head_dim, self.dh_pad)  # noqa: E731
+        shapes = {"wq": (d, d), "wk": (d, d), "wv": (d, d), "wo": (d, d), "cq": (d, d),
+                  "ck": (p, d), "cv": (p, d), "co": (d, d), "w1": (d, 2 * d), "w2": (2 * d, d)}
+        if weights == "reference":
+            rng = np.random.default_rng(np.random.PCG64(config.weight_seed))
+
+            def draw(r, c):
+                return rng.standard_normal((r, c)).astype(np.float32) * np.float32(0.5 / np.sqrt(r))
+
+            self.layers = [lw({f: draw(*shapes[f]) for f in LAYER_FIELDS})
+                           for _ in range(config.layers)]
+            tv = draw(1, d)[0]
+            wout = draw(d, d)
+            wdec = rng.standard_normal((d, h * wd)).astype(np.float32) * np.float32(0.35)
+        elif weights == "device":
+            g = torch.Generator(device=dev).manual_seed(config.weight_seed)
+
+            def draw(r, c):
+                return torch.randn(r, c, device=dev, generator=g) * (0.5 / math.sqrt(r))
+
+            self.layers = [lw({f: draw(*shapes[f]) for f in LAYER_FIELDS})
+                           for _ in range(config.layers)]
+            tv, wout = draw(1, d)[0], draw(d, d)
+            wdec = torch.randn(d, h * wd, device=dev, generator=g) * 0.35
+        else:
+            raise ConfigError(f"unknown weights source {weights!r}")
+        self.time_vec = torch.as_tensor(tv).to(dev, torch.float32).contiguous()
+        self.w_out = torch.as_tensor(wout).to(dev, torch.bfloat16)
+        self.w_decode = torch.as_tensor(wdec).to(dev, torch.float32)
+
+    def num_parameters(self) -> int:
+        """engine.py:146-150: L*(10D^2 + 2PD) + D + D^2 + D*H*W."""
+        c = self.config
+        d, p = c.model_dim, c.prompt_dim
+        h, w = c.frame_shape
+        return c.layers * (10 * d * d + 2 * p * d) + d + d * d + d * h * w
+
+    @property
+    def attn_width(self) -> int:
+        """Row width of Q/K/V/O and of the KV slabs (heads x padded head width)."""
+        return self.config.heads * self.dh_pad
+
+
+def build_model(config: ModelConfig, **kw) -> ToyModel:
+    """engine.py:153-154."""
+    return ToyModel(config, **kw)
+
+
+def embed_prompt(model: ToyModel, prompt_text: str) -> np.ndarray:
+    """engine.py:157-168 — sha256 of each whitespace token seeds a unit vector (host)."""
+    if not prompt_text:
+        raise ConfigError("empty prompt")
+    dim = model.config.prompt_dim
+    rows = []
+    for tok in prompt_text.split():
+        seed = int.from_bytes(hashlib.sha256(tok.encode("utf-8")).digest()[:8], "little")
+        vec = np.random.default_rng(seed).standard_normal(dim).astype(np.float32)
+        rows.append(vec / np.float32(np.linalg.norm(vec)))
+    return np.stack(rows)
+
+
+def _init_noise(cfg: ModelConfig, seed: int, chunk_index: int) -> np.ndarray:
+    """engine.py:280-282 — bit-identical host noise."""
+    rng = np.random.default_rng([seed, chunk_index])
+    return rng.standard_normal((cfg.block_len, cfg.model_dim)).astype(np.float32)
+
+
+def _cross_kv(model: ToyModel, prompt_emb: np.ndarray):
+    """engine.py:224-225 on device (fp32)."""
+    e = torch.as_tensor(prompt_emb).cuda()
+    return [(e @ lw.ck, e @ lw.cv) for lw in model.layers]
+
+
+class _Workspace:
+    """Per-(T, D) device buffers reused across passes (no allocator traffic in the loop)."""
+
+    def __init__(self, T: int, D: int, Dp: int, dev):
+        self.x = torch.empty(T, D, device=dev, dtype=torch.float32)
+        self.h = torch.empty(T, D, device=dev, dtype=torch.bfloat16)
+        self.qkv = torch.empty(T, 3 * Dp, device=dev, dtype=torch.bfloat16)
+        self.q2 = torch.empty(T, Dp, device=dev, dtype=torch.bfloat16)
+        self.attn = torch.empty(T, Dp, device=dev, dtype=torch.bfloat16)
+        self.ffn = torch.empty(T, 2 * D, device=dev, dtype=torch.bfloat16)
+        self.tmp = torch.empty(T, D, device=dev, dtype=torch.float32)
+
+
+def _residual(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor, tmp: torch.Tensor):
+    """x += a @ w with bf16 operands and fp32 output/accumulation (cuBLAS)."""
+    torch.mm(a, w, out_dtype=torch.float32, out=tmp)
+    x.add_(tmp)
+
+
+class BlockRunner:
+    """Runs the denoise passes of one block on the device (engine.py:185-221,285-312).
+
+    `attn_events`: if a list, (start, end) CUDA events are recorded around every
+    self-attention K1 launch (bench roofline timing)."""
+
+    def __init__(self, model: ToyModel):
+        self.model = model
+        c = model.config
+        self.dev = require_cuda()
+        self.ws = _Workspace(c.block_len, c.model_dim, model.attn_width, self.dev)
+        self.attn_events = None
+        self.kernel_launches = 0
+
+    def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
+                collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None):
+        """One pass. ctx[l] = (slab, base, total) or None; cross[l] = (k, v, row0, n) or None."""
+        m, ws = self.model, self.ws
+        c = m.config
+        H, dhp, Dp = c.heads, m.dh_pad, m.attn_width
+        sc = 1.0 / math.sqrt(c.head_dim)
+        q, kc, vc = ws.qkv[:, :Dp], ws.qkv[:, Dp:2 * Dp], ws.qkv[:, 2 * Dp:]
+        for li, lw in enumerate(m.layers):
+            if li == 0:  # x = latent + t*time_vec fused into the first norm (engine.py:199)
+                rms_bf16(latent, ws.h, m.time_vec, t, x_out=ws.x)
+            else:
+                rms_bf16(ws.x, ws.h)
+            torch.mm(ws.h, lw.wqkv, out=ws.qkv)
+            ev = self.attn_events
+            if ev is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            slab_info = ctx[li] if ctx is not None else None
+            if slab_info is not None and slab_info[2] > slab_info[1]:
+                s, base, total = slab_info
+                attn_fwd(q, H, dhp, ws.attn, s.k, s.v, base - s.origin, total - base, kc, vc,
+                         scale=sc)
+            else:
+                attn_fwd(q, H, dhp, ws.attn, cur_k=kc, cur_v=vc, scale=sc)
+            if ev is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                ev.append((e0, e1))
+            _residual(ws.x, ws.attn, lw.wo, ws.tmp)
+            if cross is not None:
+                xk, xv, row0, n = cross[li]
+                rms_bf16(ws.x, ws.h)
+                torch.mm(ws.h, lw.cq, out=ws.q2)
+                attn_fwd(ws.q2, H, dhp, ws.attn, xk, xv, row0, n, scale=sc)
+                _residual(ws.x, ws.attn, lw.co, ws.tmp)
+                self.kernel_launches += 2
+            rms_bf16(ws.x, ws.h)
+            torch.mm(ws.h, lw.w1, out=ws.ffn)
+            ws.ffn.relu_()
+            _residual(ws.x, ws.ffn, lw.w2, ws.tmp)
+            self.kernel_launches += 3
+            if collect_kv:  # clean pass: page write of this layer's K/V (engine.py:303-306)
+                cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
+                self.kernel_launches += 1
+        if eps_out is not None:
+            rms_bf16(ws.x, ws.h)
+            torch.mm(ws.h, m.w_out, out_dtype=torch.float32, out=eps_out)
+            self.kernel_launches += 1
+
+    def denoise(self, latent: torch.Tensor, schedule: DenoiseSchedule, ctx, cross,
+                cache: KvCache | None, chunk_index: int) -> torch.Tensor:
+        """engine.py:296-306: S Euler steps in place on `latent`, then the clean K/V pass."""
+        eps = self.ws.tmp.new_empty(self.ws.tmp.shape) if not hasattr(self, "_eps") else self._eps
+        self._eps = eps
+        for t in schedule.steps:
+            self.forward(latent, float(t), ctx, cross, cache, eps_out=eps)
+            latent.add_(eps, alpha=-float(schedule.step_scale))
+        self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
+                     chunk_index=chunk_index)
+        return latent
+
+
+def _ctx_from_cache(model: ToyModel, cache: KvCache | None):
+    """engine.py:228-237 — bookkeeping of the context fetch (restore + access clock, in the
+    reference's call order) while the data stays in place for K1."""
+    if cache is None:
+        return None
+    out = []
+    for li in range(model.config.layers):
+        lo, hi = cache.addressable_range(li, SELF_ATTN)
+        if hi > lo:
+            cache.touch_range(li, (lo, hi), SELF_ATTN)
+        out.append((cache.slab(li, SELF_ATTN), lo, hi))
+    return out
+
+
+def _cross_from_cache(model: ToyModel, cache: KvCache | None, prompt_ctx):
+    """engine.py:240-250."""
+    if cache is not None:
+        lo, hi = cache.addressable_range(0, CROSS_ATTN)
+        if hi > lo:
+            out = []
+            for li in range(model.config.layers):
+                a, b = cache.addressable_range(li, CROSS_ATTN)
+                cache.touch_range(li, (a, b), CROSS_ATTN)
+                s = cache.slab(li, CROSS_ATTN)
+                out.append((s.k, s.v, a - s.origin, b - a))
+            return out
+    if prompt_ctx is None:
+        return None
+    out = []
+    for k, v in _cross_kv(model, prompt_ctx):
+        kb, vb = k.to(torch.bfloat16).contiguous(), v.to(torch.bfloat16).contiguous()
+        out.append((kb, vb, 0, kb.shape[0]))
+    return out
+
+
+_RUNNERS: dict = {}
+
+
+def _runner(model: ToyModel) -> BlockRunner:
+    r = _RUNNERS.get(id(model))
+    if r is None or r.model is not model:
+        r = _RUNNERS[id(model)] = BlockRunner(model)
+    return r
+
+
+def denoise_step(model: ToyModel, latent, t: float, step_scale: float, cache: KvCache | None = None,
+                 prompt_ctx: np.ndarray | None = None) -> torch.Tensor:
+    """engine.py:253-269 — one Euler update; the cache is read-only. Returns a CUDA tensor."""
+    c = model.config
+    lat = torch.as_tensor(np.asarray(latent, np.float32) if not isinstance(latent, torch.Tensor)
+                          else latent).to(require_cuda(), torch.float32).clone()
+    if lat.dim() != 2 or lat.shape[1] != c.model_dim:
+        raise DimensionError("latent must be [tokens, model_dim]")
+    r = _runner(model) if lat.shape[0] == c.block_len else BlockRunner.__new__(BlockRunner)
+    if lat.shape[0] != c.block_len:
+        r.__init__(model)
+        r.ws = _Workspace(lat.shape[0], c.model_dim, model.attn_width, r.dev)
+    eps = torch.empty_like(lat)
+    r.forward(lat, float(t), _ctx_from_cache(model, cache), _cross_from_cache(model, cache, prompt_ctx),
+              cache, eps_out=eps)
+    return lat.sub_(eps, alpha=float(step_scale))
+
+
+def decode_frames(model: ToyModel, latent) -> list:
+    """engine.py:272-277 — affine map of each latent row to a clamped uint8 frame (fp32)."""
+    h, w = model.config.frame_shape
+    x = torch.as_tensor(latent).to(require_cuda(), torch.float32)
+    xr = x / torch.sqrt((x * x).mean(dim=-1, keepdim=True) + 1e-6)
+    px = torch.clamp(127.5 + 48.0 * (xr @ model.w_decode), 0.0, 255.0).to(torch.uint8)
+    return list(px.view(-1, h, w).cpu().numpy())
+
+
+def default_kv_config(model_cfg: ModelConfig, **overrides) -> KvConfig:
+    """engine.py:315-324."""
+    kw = dict(num_layers=model_cfg.layers, head_dim=model_cfg.model_dim, page_len=16,
+              capacity_pages_device=4096, capacity_pages_host=4096)
+    kw.update(overrides)
+    return KvConfig(**kw)
+
+
+def _prompt_for_chunk(schedule, chunk: int) -> str:
+    """engine.py:327-332."""
+    text = schedule[0][1]
+    for c, p in schedule:
+        if c <= chunk:
+            text = p
+    return text
+
+
+def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSchedule, prompt_ctx,
+                   chunk_index: int, seed: int, prompt_text: str = "", noise=None,
+                   to_host: bool = True) -> GeneratedBlock:
+    """engine.py:285-312 — denoise one block from seeded noise, append its clean K/V."""
+    schedule.validate()
+    c = model.config
+    if noise is None:
+        noise = _init_noise(c, seed, chunk_index)
+    lat = (noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)).to(
+        require_cuda(), torch.float32, non_blocking=True).clone()
+    ctx = _ctx_from_cache(model, cache)
+    cross = _cross_from_cache(model, cache, prompt_ctx)
+    _runner(model).denoise(lat, schedule, ctx, cross, cache, chunk_index)
+    if not to_host:
+        return GeneratedBlock(chunk_index, lat, [], prompt_text)
+    frames = decode_frames(model, lat)
+    return GeneratedBlock(chunk_index, lat.cpu().numpy(), frames, prompt_text)
+
+
+class Engine:
+    """engine.py:335-411 — one generation stream; prompt updates from other threads are
+    merged at block boundaries, never retroactively."""
+
+    def __init__(self, model: ToyModel, kv_config: KvConfig | None = None, profiler=None,
+                 cache_dtype: torch.dtype = torch.bfloat16):
+        self.model = model
+        self.kv_config = kv_config or default_kv_config(model.config)
+        self.profiler = profiler
+        self.cache_dtype = cache_dtype
+        self._lock = threading.Lock()
+        self._generating_chunk = -1
+        self._pending: list = []
+        self._schedule: list = []
+        self.event_log: list = []
+        self.cache: KvCache | None = None
+
+    def apply_prompt_update(self, effective_chunk: int, prompt_text: str) -> bool:
+        """engine.py:351-359 — accept iff the target chunk is after the one in flight."""
+        if not prompt_text:
+            return False
+        with self._lock:
+            if effective_chunk <= self._generating_chunk:
+                return False
+            self._pending.append((effective_chunk, prompt_text))
+            return True
+
+    def _merge_pending(self):
+        for chunk, text in self._pending:
+            entries = [e for e in self._schedule if e[0] != chunk]
+            entries.append((chunk, text))
+            self._schedule = sorted(entries)
+        self._pending.clear()
+
+    def generate(self, request: GenerationRequest, sinks=(), noise_provider=None,
+                 to_host: bool = True) -> list:
+        """engine.py:368-411. `noise_provider(chunk)` (optional) supplies the block's noise
+        (default: the reference's seeded host noise, prefetched on a worker thread)."""
+        request.validate()
+        c = self.model.config
+        T = c.block_len
+        reserve = T * request.num_blocks
+        if request.kv_window is not None:
+            reserve = min(reserve, request.kv_window + 2 * T + c.block_len)
+        self.cache = KvCache(self.kv_config, dtype=self.cache_dtype, reserve_tokens=reserve,
+                             row_width=self.model.attn_width)
+        with self._lock:
+            self._schedule = list(request.prompt_schedule)
+            self._generating_chunk = -1
+        make_noise = noise_provider or (lambda ch: _init_noise(c, request.seed, ch))
+        pool = ThreadPoolExecutor(1)
+        nxt = pool.submit(make_noise, 0)
+        blocks = []
+        current_prompt = None
+        prof = self.profiler
+        try:
+            for chunk in range(request.num_blocks):
+                with self._lock:
+                    self._merge_pending()
+                    self._generating_chunk = chunk
+                    prompt = _prompt_for_chunk(self._schedule, chunk)
+                if prompt != current_prompt:
+                    if current_prompt is not None:
+                        self.cache.clear_cross_attention()
+                        self.event_log.append(("clear_cross_attention", chunk))
+                    emb = embed_prompt(self.model, prompt)
+                    for li, (kc, vc) in enumerate(_cross_kv(self.model, emb)):
+                        self.cache.append_block(li, kc, vc, kind=CROSS_ATTN, chunk_index=chunk)
+                    current_prompt = prompt
+                noise = nxt.result()
+                if chunk + 1 < request.num_blocks:
+                    nxt = pool.submit(make_noise, chunk + 1)
+                span = prof.scoped("generate_block") if prof else None
+                if span:
+                    span.__enter__()
+                block = generate_block(self.model, self.cache, request.schedule, None, chunk,
+                                       request.seed, prompt_text=prompt, noise=noise,
+                                       to_host=to_host)
+                if span:
+                    span.__exit__(None, None, None)
+                if request.kv_window is not None:
+                    self.cache.evict_window(request.kv_window)
+                self.event_log.append(("block", chunk))
+                for sink in sinks:
+                    sink(block)
+                blocks.append(block)
+        finally:
+            pool.shutdown(wait=False)
+        with self._lock:
+            self._generating_chunk = request.num_blocks
+        return blocks
+
+
+def generate_sequence(model: ToyModel, request: GenerationRequest, sinks=(),
+                      kv_config: KvConfig | None = None, profiler=None) -> list:
+    """engine.py:414-421."""
+    return Engine(model, kv_config, profiler).generate(request, sinks)
+
+
+# -- pipeline registry (engine.py:495-528) ------------------------------------------------
+
+
+@dataclass(frozen=True)
+class Pipeline:
+    """Hooks a model family plugs into the common generate-and-cache loop."""
+    name: str
+    build_model: Callable
+    denoise_step: Callable
+    decode_frames: Callable
+
+
+_PIPELINES: dict = {}
+
+
+def register_pipeline(pipeline: Pipeline):
+    _PIPELINES[pipeline.name] = pipeline
+
+
+def get_pipeline(name: str) -> Pipeline:
+    try:
+        return _PIPELINES[name]
+    except KeyError:
+        raise ConfigError(f"unknown pipeline {name!r}; registered: {sorted(_PIPELINES)}") from None
+
+
+for _name in ("toy", "b200"):
+    register_pipeline(Pipeline(name=_name, build_model=build_model, denoise_step=denoise_step,
+                               decode_frames=decode_frames))

@@ -134,59 +134,146 @@ class _Slab:
         self.k, self.v = k, v
 
 
+class PageTable:
+    """ctypes handle of the native bit-exact page table (csrc/pagetable.cpp). Host-only:
+    no device memory, usable without a GPU (tests/test_pagetable.py)."""
+
+    def __init__(self, config: KvConfig):
+        config.validate()
+        self.config = config
+        h = ctypes.c_void_p()
+        _abi.check(_abi.lib().ifx_pt_create(config.num_layers, config.head_dim, config.page_len,
+                                             config.capacity_pages_device,
+                                             config.capacity_pages_host, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _abi.lib().ifx_pt_destroy(h)
+            self._h = None
+
+    @staticmethod
+    def kind_code(kind) -> int:
+        if kind not in _KIND:
+            raise ConfigError(f"unknown kind {kind!r}")
+        return _KIND[kind]
+
+    def append(self, layer: int, kind: str, t: int, chunk_index: int):
+        """-> (rc, block_id, start, written, page_ids); rc != 0 keeps `written` rows."""
+        bid, start, written, npages = (ctypes.c_int64() for _ in range(4))
+        cap = t // self.config.page_len + 2
+        pages = (ctypes.c_int64 * cap)()
+        rc = _abi.lib().ifx_pt_append(self._h, layer, self.kind_code(kind), t, chunk_index,
+                                      ctypes.byref(bid), ctypes.byref(start), ctypes.byref(written),
+                                      pages, cap, ctypes.byref(npages))
+        return rc, bid.value, start.value, written.value, list(pages[:npages.value])
+
+    def offload(self, block_ids) -> int:
+        ids = [int(b) for b in block_ids]
+        arr = (ctypes.c_int64 * max(1, len(ids)))(*ids)
+        moved = ctypes.c_int64()
+        _abi.check(_abi.lib().ifx_pt_offload(self._h, arr, len(ids), ctypes.byref(moved)))
+        return moved.value
+
+    def evict_window(self, keep: int) -> int:
+        freed = ctypes.c_int64()
+        _abi.check(_abi.lib().ifx_pt_evict_window(self._h, int(keep), ctypes.byref(freed)))
+        return freed.value
+
+    def clear_cross(self) -> int:
+        n = ctypes.c_int64()
+        _abi.check(_abi.lib().ifx_pt_clear_cross(self._h, ctypes.byref(n)))
+        return n.value
+
+    def touch_range(self, layer: int, kind: str, a: int, b: int) -> None:
+        _abi.check(_abi.lib().ifx_pt_touch_range(self._h, layer, self.kind_code(kind), a, b))
+
+    def touch_indices(self, layer: int, kind: str, idx) -> None:
+        arr = (ctypes.c_int64 * max(1, len(idx)))(*idx)
+        _abi.check(_abi.lib().ifx_pt_touch_indices(self._h, layer, self.kind_code(kind), arr,
+                                                   len(idx)))
+
+    def range(self, layer: int, kind: str):
+        base, total = ctypes.c_int64(), ctypes.c_int64()
+        _abi.check(_abi.lib().ifx_pt_range(self._h, layer, self.kind_code(kind),
+                                           ctypes.byref(base), ctypes.byref(total)))
+        return base.value, total.value
+
+    def stats(self) -> list:
+        L = self.config.num_layers
+        out = (ctypes.c_int64 * (3 + L))()
+        _abi.check(_abi.lib().ifx_pt_stats(self._h, out, 3 + L))
+        return list(out)
+
+    def state(self) -> dict:
+        """Canonical full bookkeeping state (same schema as oracle.kvcache.KvStore.state)."""
+        n = ctypes.c_int64()
+        _abi.check(_abi.lib().ifx_pt_snapshot(self._h, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_int64 * n.value)()
+        _abi.check(_abi.lib().ifx_pt_snapshot(self._h, buf, n.value, ctypes.byref(n)))
+        it = iter(buf)
+        nx = lambda: next(it)  # noqa: E731
+        st = {"clock": nx(), "next_page": nx(), "next_block": nx(), "device_used": nx(),
+              "host_used": nx()}
+        streams = []
+        for _ in range(nx()):
+            layer, kind, base, total, npg = nx(), nx(), nx(), nx(), nx()
+            pages = [[nx(), nx(), nx(), nx(), nx()] for _ in range(npg)]
+            streams.append([layer, _KIND_NAME[kind], base, total, pages])
+        blocks = []
+        for _ in range(nx()):
+            bid, layer, kind, a, b, chunk, npg = (nx() for _ in range(7))
+            blocks.append([bid, layer, _KIND_NAME[kind], a, b, [nx() for _ in range(npg)], chunk])
+        st["streams"], st["blocks"] = streams, blocks
+        return st
+
+
 class KvCache:
     """Drop-in for `inferix.kvcache.KvCache` (kvcache.py:105-404); create via create_cache().
 
     Extra keyword arguments (B200 only): `dtype` of the device slabs (torch.float32 for
     bit-exact API parity, torch.bfloat16 for the engine), `reserve_tokens` rows to
-    pre-allocate per self-attention stream."""
+    pre-allocate per self-attention stream, `row_width` of the device rows when it
+    differs from head_dim (the engine stores per-head zero-padded rows)."""
 
     def __init__(self, config: KvConfig, dtype: torch.dtype = torch.float32,
-                 reserve_tokens: int = 0):
+                 reserve_tokens: int = 0, row_width: int | None = None):
         config.validate()
         self.config = config
         self.dtype = dtype
         self._lock = threading.RLock()
-        h = ctypes.c_void_p()
-        _abi.check(_abi.lib().ifx_pt_create(config.num_layers, config.head_dim, config.page_len,
-                                             config.capacity_pages_device,
-                                             config.capacity_pages_host, ctypes.byref(h)))
-        self._pt = h
-        w = config.stored_width
+        self._pt = PageTable(config)
+        if row_width is not None and config.latent is not None:
+            raise ConfigError("row_width override is not supported in latent mode")
+        w = row_width or config.stored_width
+        self._row_width = w
         self._slabs = {}
         for layer in range(config.num_layers):
             self._slabs[(layer, SELF_ATTN)] = _Slab(w, dtype, reserve_tokens)
             self._slabs[(layer, CROSS_ATTN)] = _Slab(w, dtype, 64)
         self._latent_down = self._latent_up = None
         if config.latent is not None:
-            self._latent_down = torch.as_tensor(np.asarray(config.latent.down_proj, np.float32)).cuda()
-            self._latent_up = torch.as_tensor(np.asarray(config.latent.up_proj, np.float32)).cuda()
+            dev = require_cuda()
+            self._latent_down = torch.as_tensor(np.asarray(config.latent.down_proj, np.float32)).to(dev)
+            self._latent_up = torch.as_tensor(np.asarray(config.latent.up_proj, np.float32)).to(dev)
 
-    def __del__(self):
-        pt = getattr(self, "_pt", None)
-        if pt is not None and pt.value:
-            _abi.lib().ifx_pt_destroy(pt)
-            self._pt = None
-
-    # -- helpers ------------------------------------------------------------------------
-    def _kind(self, kind) -> int:
-        if kind not in _KIND:
-            raise ConfigError(f"unknown kind {kind!r}")
-        return _KIND[kind]
+    @property
+    def page_table(self) -> PageTable:
+        return self._pt
 
     def slab(self, layer: int, kind: str = SELF_ATTN) -> _Slab:
-        """Device rows of a stream (engine / K1 read them in place)."""
+        """Device rows of a stream (the engine's K1 reads them in place)."""
         return self._slabs[(layer, kind)]
 
     @staticmethod
     def _as_rows(x) -> torch.Tensor:
         if isinstance(x, torch.Tensor):
-            t = x if x.is_cuda else x.cuda()
-            if t.dtype not in (torch.float32, torch.bfloat16):
-                t = t.float()
-            return t
+            t = x if x.is_cuda else x.to(require_cuda())
+            return t if t.dtype in (torch.float32, torch.bfloat16) else t.float()
         a = np.asarray(x, dtype=np.float32)
-        return torch.from_numpy(np.ascontiguousarray(a)).cuda() if a.ndim == 2 else torch.from_numpy(a)
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        return t.to(require_cuda()) if a.ndim == 2 else t
 
     # -- mutations ------------------------------------------------------------------------
     def append_block(self, layer: int, k, v, kind: str = SELF_ATTN, chunk_index: int = 0,
@@ -199,70 +286,55 @@ class KvCache:
         t, d = k.shape
         if t < 1:
             raise DimensionError("append needs at least one token")
-        if d != cfg.head_dim:
+        if d != cfg.head_dim and d != self._row_width:
             raise DimensionError(f"width {d} != head_dim {cfg.head_dim}")
         if not 0 <= layer < cfg.num_layers:
             raise OutOfRangeError(f"layer {layer} out of range")
-        ck = self._kind(kind)
+        PageTable.kind_code(kind)
         if self._latent_down is not None:
             k = (k.float() @ self._latent_down).contiguous()
             v = (v.float() @ self._latent_down).contiguous()
-        if k.stride(1) != 1 or k.stride(0) != v.stride(0) or v.stride(1) != 1:
+        if k.stride(1) != 1 or v.stride(1) != 1 or k.stride(0) != v.stride(0):
             k, v = k.contiguous(), v.contiguous()
         with self._lock:
-            bid, start, written, npages = (ctypes.c_int64() for _ in range(4))
-            cap = t // cfg.page_len + 2
-            pages = (ctypes.c_int64 * cap)()
-            rc = _abi.lib().ifx_pt_append(self._pt, layer, ck, t, chunk_index, ctypes.byref(bid),
-                                          ctypes.byref(start), ctypes.byref(written), pages, cap,
-                                          ctypes.byref(npages))
-            n = written.value
-            if n > 0:  # rows already packed, even if the allocation then failed (kvcache.py:210-223)
-                base, total = self.addressable_range(layer, kind)
+            rc, bid, start, written, pages = self._pt.append(layer, kind, t, chunk_index)
+            if written > 0:  # rows already packed even if allocation then failed (kvcache.py:210-223)
+                base, total = self._pt.range(layer, kind)
                 s = self._slabs[(layer, kind)]
-                first = total - n
                 s.ensure(base, total, cfg.page_len)
                 _abi.check(_abi.lib().ifx_kv_append(
                     k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype),
                     s.k.data_ptr(), s.v.data_ptr(), s.width, dtype_code(s.dtype),
-                    first - s.origin, n, s.width, stream_ptr(stream)), "kv_append")
+                    total - written - s.origin, written, s.width, stream_ptr(stream)), "kv_append")
             _abi.check(rc, "append_block")
-            return BlockEntry(bid.value, layer, (start.value, start.value + t),
-                              list(pages[:npages.value]), kind, chunk_index)
+            return BlockEntry(bid, layer, (start, start + t), pages, kind, chunk_index)
 
     def offload_blocks(self, block_ids) -> int:
         """kvcache.py:236-256 (tier bookkeeping; data stays resident in HBM)."""
-        ids = [int(b) for b in block_ids]
-        arr = (ctypes.c_int64 * max(1, len(ids)))(*ids)
-        moved = ctypes.c_int64()
         with self._lock:
-            _abi.check(_abi.lib().ifx_pt_offload(self._pt, arr, len(ids), ctypes.byref(moved)))
-        return moved.value
+            return self._pt.offload(block_ids)
 
     def evict_window(self, keep_last_n_tokens: int) -> int:
         """kvcache.py:258-285."""
-        freed = ctypes.c_int64()
         with self._lock:
-            _abi.check(_abi.lib().ifx_pt_evict_window(self._pt, int(keep_last_n_tokens),
-                                                      ctypes.byref(freed)))
-        return freed.value
+            return self._pt.evict_window(keep_last_n_tokens)
 
     def clear_cross_attention(self) -> int:
         """kvcache.py:287-299."""
-        n = ctypes.c_int64()
         with self._lock:
-            _abi.check(_abi.lib().ifx_pt_clear_cross(self._pt, ctypes.byref(n)))
+            n = self._pt.clear_cross()
             for layer in range(self.config.num_layers):
                 self._slabs[(layer, CROSS_ATTN)].reset()
-        return n.value
+            return n
 
     # -- reads ----------------------------------------------------------------------------
     def touch_range(self, layer: int, token_range, kind: str = SELF_ATTN) -> None:
-        """Bookkeeping half of fetch_range (restore-on-read + access clock, kvcache.py:303-339)
-        without moving data — what the engine calls before K1 reads the slab in place."""
+        """Bookkeeping half of fetch_range (restore-on-read + per-token access clock,
+        kvcache.py:303-339) without moving data — what the engine calls before K1 reads
+        the slab in place."""
         a, b = token_range
         with self._lock:
-            _abi.check(_abi.lib().ifx_pt_touch_range(self._pt, layer, self._kind(kind), a, b))
+            self._pt.touch_range(layer, kind, a, b)
 
     def _gather(self, layer, kind, rows: torch.Tensor | None, first: int, n: int):
         s = self._slabs[(layer, kind)]
@@ -283,7 +355,7 @@ class KvCache:
         if not 0 <= layer < self.config.num_layers:
             raise OutOfRangeError(f"layer {layer} out of range")
         with self._lock:
-            self.touch_range(layer, (a, b), kind)
+            self._pt.touch_range(layer, kind, a, b)
             return self._gather(layer, kind, None, a, b - a)
 
     def fetch_indices(self, layer: int, indices, kind: str = SELF_ATTN):
@@ -292,61 +364,30 @@ class KvCache:
         if not 0 <= layer < self.config.num_layers:
             raise OutOfRangeError(f"layer {layer} out of range")
         with self._lock:
-            arr = (ctypes.c_int64 * max(1, len(idx)))(*idx)
-            _abi.check(_abi.lib().ifx_pt_touch_indices(self._pt, layer, self._kind(kind), arr,
-                                                       len(idx)))
+            self._pt.touch_indices(layer, kind, idx)
             if not idx:
-                w = self.config.head_dim
-                dev = require_cuda()
-                return (torch.empty(0, w, device=dev, dtype=torch.float32),
-                        torch.empty(0, w, device=dev, dtype=torch.float32))
+                w, dev = self.config.head_dim, require_cuda()
+                return (torch.empty(0, w, device=dev), torch.empty(0, w, device=dev))
             s = self._slabs[(layer, kind)]
-            rows = torch.tensor(idx, dtype=torch.int64).cuda() - s.origin
+            rows = torch.tensor(idx, dtype=torch.int64).to(s.k.device) - s.origin
             return self._gather(layer, kind, rows, 0, len(idx))
 
     def addressable_range(self, layer: int, kind: str = SELF_ATTN):
         """kvcache.py:355-357."""
-        base, total = ctypes.c_int64(), ctypes.c_int64()
-        _abi.check(_abi.lib().ifx_pt_range(self._pt, layer, self._kind(kind), ctypes.byref(base),
-                                           ctypes.byref(total)))
-        return base.value, total.value
+        return self._pt.range(layer, kind)
 
     def memory_stats(self) -> KvStats:
         """kvcache.py:359-372 (bytes_logical counts fp32 K+V like the reference)."""
-        L = self.config.num_layers
-        out = (ctypes.c_int64 * (3 + L))()
         with self._lock:
-            _abi.check(_abi.lib().ifx_pt_stats(self._pt, out, 3 + L))
+            out = self._pt.stats()
         tokens = out[2]
+        L = self.config.num_layers
         return KvStats(out[0], out[1], tokens, {l: out[3 + l] for l in range(L)},
                        tokens * self.config.stored_width * 4 * 2)
 
-    def _snapshot(self) -> list:
-        n = ctypes.c_int64()
-        _abi.check(_abi.lib().ifx_pt_snapshot(self._pt, None, 0, ctypes.byref(n)))
-        buf = (ctypes.c_int64 * n.value)()
-        _abi.check(_abi.lib().ifx_pt_snapshot(self._pt, buf, n.value, ctypes.byref(n)))
-        return list(buf)
-
     def state(self) -> dict:
-        """Canonical full bookkeeping state (same schema as oracle.kvcache.KvStore.state)."""
         with self._lock:
-            r = self._snapshot()
-        it = iter(r)
-        nx = lambda: next(it)  # noqa: E731
-        st = {"clock": nx(), "next_page": nx(), "next_block": nx(), "device_used": nx(),
-              "host_used": nx()}
-        streams = []
-        for _ in range(nx()):
-            layer, kind, base, total, npg = nx(), nx(), nx(), nx(), nx()
-            pages = [[nx(), nx(), nx(), nx(), nx()] for _ in range(npg)]
-            streams.append([layer, _KIND_NAME[kind], base, total, pages])
-        blocks = []
-        for _ in range(nx()):
-            bid, layer, kind, a, b, chunk, npg = (nx() for _ in range(7))
-            blocks.append([bid, layer, _KIND_NAME[kind], a, b, [nx() for _ in range(npg)], chunk])
-        st["streams"], st["blocks"] = streams, blocks
-        return st
+            return self._pt.state()
 
     def block_entries(self) -> list:
         """kvcache.py:374-376."""
@@ -355,9 +396,8 @@ class KvCache:
     def dump(self, path) -> None:
         """kvcache.py:380-404 — INFKV1 snapshot (fp32 rows, pages sorted by id)."""
         cfg = self.config
-        st = self.state()
         pages = []
-        for layer, kind, _base, _total, pgs in st["streams"]:
+        for layer, kind, _base, _total, pgs in self.state()["streams"]:
             for pid, tier, filled, start, _la in pgs:
                 pages.append((pid, tier, filled, start, layer, kind))
         pages.sort()
