@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py — block-diffusion decode hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One "step" is one full generate-and-cache rollout of the configured workload: every
+block runs 4 Euler denoise passes + the clean K/V pass over all layers, attending the
+paged KV cache of prior blocks, then appends its K/V (engine.py:285-312, 368-411).
+Default workload (N=1) is BASELINE.json configs[1]: Wan2.1-1.3B-shaped (30 layers, 12
+heads x 128, 4680 tokens = 3 latent frames per block), 7 blocks = 21 latent frames.
+
+value    latent frames/s over the K timed rollouts, inputs (noise) resident in HBM,
+         CUDA events on the engine stream, barrier + synchronize on both sides.
+e2e      the same metric through the public API `Engine.generate()` with host noise
+         (numpy default_rng, exactly the reference's inputs) copied H2D and every block's
+         latent + decoded frames copied D2H inside the timed region.
+roofline the dominant kernel, K1 attention: algorithmic FLOPs 4*T*(C+T)*D per launch
+         summed over the timed region / summed CUDA-event durations of those launches,
+         against MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long
+         step).
+cpu_baseline  the numpy oracle port (oracle/engine.py:layer_pass) on the host cores:
+         two layer-passes at the exact shape (b = 0 and 1 cached blocks), extrapolated
+         linearly in b to the same rollout.
+
+--impl reference: the reference's CPU algorithm (the oracle port; the Python reference
+cannot travel to the GPU box) on all host cores, same metric/config; each step is one
+bounded sample (a pair of layer-passes), extrapolated to the rollout.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "latent frames/sec & attention TFLOP/s (% bf16 peak) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "latent frames/s"
+FRAMES_PER_BLOCK = 3  # 3 latent frames x 1560 tokens (480p) per block
+STEPS = [1.0, 0.75, 0.5, 0.25]
+
+CONFIGS = {
+    "c1": dict(layers=2, heads=4, head_dim=64, block_len=768, blocks=3, frame_shape=(16, 16),
+               weights="reference",
+               desc="c1: tiny random-init DiT (2L, 4 heads x 64, dim 256), 768 tok/block, 3 blocks x 3 frames, 4 steps"),
+    "c2": dict(layers=30, heads=12, head_dim=128, block_len=4680, blocks=7, frame_shape=(16, 16),
+               weights="reference",
+               desc="c2: Wan2.1-1.3B-shaped (30L, 12 heads x 128, dim 1536), 1560 tok/frame x 3-frame blocks, 7 blocks (21 latent frames), 4 steps"),
+    "c3": dict(layers=30, heads=12, head_dim=128, block_len=4680, blocks=21, frame_shape=(16, 16),
+               weights="reference",
+               desc="c3: 1.3B shape long context, 21 blocks (20 cached)"),
+    "c4": dict(layers=40, heads=40, head_dim=128, block_len=4680, blocks=3, frame_shape=(16, 16),
+               weights="device",
+               desc="c4: Wan2.1-14B-shaped (40L, 40 heads x 128, dim 5120), 3 blocks, 4 steps"),
+}
+
+
+def attn_flops_per_rollout(c) -> float:
+    """4*T*(C+T)*D per (layer, pass); P = steps + 1 passes per block."""
+    T, D = c["block_len"], c["heads"] * c["head_dim"]
+    P = len(STEPS) + 1
+    return sum(4.0 * T * (b * T + T) * D * c["layers"] * P for b in range(c["blocks"]))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p.get("bf16_tflops_sustained") or p["bf16_tflops"], "measured (sustained)"
+    except Exception:
+        return 1400.0, "fallback (B200_PROFILING.md sustained)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+
+    def summary(self) -> dict:
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(float(r[1]) for r in rows),
+                "sm_max_mhz": max(float(r[2]) for r in rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit()),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_layer_pass_times(c, n_layers_b0=1, bs=(0, 1), threads=None):
+    """Time oracle layer-passes (oracle/engine.py:layer_pass) at the exact (T, D, H)."""
+    import numpy as np
+
+    from oracle import engine as OE
+
+    T, H, dh = c["block_len"], c["heads"], c["head_dim"]
+    D = H * dh
+    g = np.random.default_rng(0)
+    s = lambda r, k: (g.standard_normal((r, k)).astype(np.float32) * np.float32(0.5 / np.sqrt(r)))  # noqa: E731
+    w = {"wq": s(D, D), "wk": s(D, D), "wv": s(D, D), "wo": s(D, D), "cq": s(D, D), "co": s(D, D),
+         "w1": s(D, 2 * D), "w2": s(2 * D, D)}
+    x = g.standard_normal((T, D)).astype(np.float32)
+    xk = g.standard_normal((3, D)).astype(np.float32)
+    out = {}
+    for b in bs:
+        ck = g.standard_normal((b * T, D)).astype(np.float32)
+        t0 = time.perf_counter()
+        OE.layer_pass(w, H, x, ck, ck, xk, xk)
+        out[b] = time.perf_counter() - t0
+    return out
+
+
+def extrapolate_rollout_seconds(c, t_by_b: dict) -> float:
+    """Linear-in-b fit of one layer-pass time, summed over the rollout's blocks."""
+    b0, b1 = min(t_by_b), max(t_by_b)
+    t0, t1 = t_by_b[b0], t_by_b[b1]
+    slope = (t1 - t0) / (b1 - b0) if b1 > b0 else 0.0
+    P = len(STEPS) + 1
+    return sum((t0 + slope * (b - b0)) * c["layers"] * P for b in range(c["blocks"]))
+
+
+def cpu_baseline(c, cfgname):
+    t = cpu_layer_pass_times(c)
+    secs = extrapolate_rollout_seconds(c, t)
+    return {"value": c["blocks"] * FRAMES_PER_BLOCK / secs, "unit": UNIT,
+            "cores": os.cpu_count(), "kind": "port",
+            "sample": (f"oracle numpy layer-pass at {cfgname} shape for b=0,1 cached blocks "
+                       f"({t[0]:.2f}s, {t[1]:.2f}s), linear in b, x{c['layers']} layers x5 passes "
+                       f"x{c['blocks']} blocks = {secs:.0f}s/rollout (extrapolated)")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    nthreads = os.cpu_count()
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(v, str(nthreads))
+    c = CONFIGS[args.config or "c2"]
+    for _ in range(args.warmup):  # warm BLAS / page in (b=0 only)
+        cpu_layer_pass_times(c, bs=(0,))
+    samples = []
+    for _ in range(args.steps):
+        t = cpu_layer_pass_times(c)
+        samples.append(extrapolate_rollout_seconds(c, t))
+    secs = statistics.mean(samples)
+    value = c["blocks"] * FRAMES_PER_BLOCK / secs
+    sample = (f"per step: oracle numpy layer-passes at b=0,1 cached blocks, extrapolated linearly "
+              f"to the {c['blocks']}-block rollout ({secs:.0f}s/rollout)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded numpy)",
+            "config": {"workload": c["desc"], "extrapolated": True},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfgname = args.config or "c2"
+    c = CONFIGS[cfgname]
+    if world > 1:
+        return run_ulysses_bench(args, c, cfgname, world, rank, local)
+
+    from paper_2511_20714_b200 import _device
+    from paper_2511_20714_b200 import engine as E
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
+                       block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
+                       weight_seed=0)
+    model = E.build_model(mc, weights=c["weights"])
+    T, D = mc.block_len, mc.model_dim
+    nb = c["blocks"]
+    kvc = E.default_kv_config(mc, capacity_pages_device=10**8, capacity_pages_host=4096)
+    req = E.GenerationRequest(nb, E.DenoiseSchedule(STEPS), seed=0)
+    host_noise = [E._init_noise(mc, 0, ch) for ch in range(nb)]
+    dev_noise = [torch.from_numpy(n).cuda() for n in host_noise]
+    eng = E.Engine(model, kvc)
+    runner = E._runner(model)
+
+    def rollout_device():
+        return eng.generate(req, noise_provider=lambda ch: dev_noise[ch], to_host=False)
+
+    for _ in range(args.warmup):
+        rollout_device()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K rollouts, inputs resident in HBM
+    runner.attn_events = []
+    launches0 = _device.LAUNCHES[0]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.cuda.nvtx.range_push("timed")
+        for _ in range(args.steps):
+            rollout_device()
+        torch.cuda.nvtx.range_pop()
+        e1.record()
+        torch.cuda.synchronize()
+    launches = _device.LAUNCHES[0] - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    attn_ms = sum(a.elapsed_time(b) for a, b in runner.attn_events)
+    n_attn = len(runner.attn_events)
+    runner.attn_events = None
+    clocks = clk.summary()
+    value = nb * FRAMES_PER_BLOCK / (ms / 1e3)
+    flops = attn_flops_per_rollout(c) * args.steps
+    achieved = flops / (attn_ms / 1e3) / 1e12
+    peak, peak_src = load_peaks()
+
+    # ---- e2e: public API, host noise generated + copied H2D, latents + frames D2H
+    rollout_host = lambda: eng.generate(req)  # noqa: E731
+    rollout_host()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        blocks = rollout_host()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    h, w = mc.frame_shape
+    h2d = nb * T * D * 4 + 3 * mc.prompt_dim * 4
+    d2h = nb * (T * D * 4 + T * h * w)
+    assert all(np.isfinite(b.latent).all() for b in blocks)
+
+    cpu = None if args.no_cpu_baseline else cpu_baseline(c, cfgname)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(cfgname)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (reference-seeded noise, PCG64 random-init weights)",
+        "config": {"workload": c["desc"], "layers": mc.layers, "heads": mc.heads,
+                   "head_dim": mc.head_dim, "tokens_per_block": T, "blocks": nb,
+                   "denoise_steps": len(STEPS), "kv_cache": "bf16 paged (page_len 16), HBM slabs",
+                   "l2": "inputs larger than L2 (weights 1.4 GB, KV slabs up to 6 GB)",
+                   "parallelism": "single GPU"},
+        "attention_tflops": achieved,
+        "attention_frac_of_peak": achieved / peak,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "K1 attn_fwd_kernel<128,true> (tcgen05/TMEM/TMA)",
+                     "launches": n_attn, "kernel_ms_per_step": attn_ms / args.steps,
+                     "share_of_step": attn_ms / args.steps / ms},
+        "e2e": {"value": nb * FRAMES_PER_BLOCK / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ulysses_bench(args, c, cfgname, world, rank, local):
+    """bench.py for N > 1: one rollout strong-scaled over N GPUs with Ulysses."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_20714_b200 import _device
+    from paper_2511_20714_b200 import engine as E
+    from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
+                       block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
+                       weight_seed=0)
+    model = E.ToyModel(mc, weights="device", head_multiple=world)
+    comm = UlyssesComm()
+    nb = c["blocks"]
+    kvc = E.default_kv_config(mc, capacity_pages_device=10**8, capacity_pages_host=4096)
+    req = E.GenerationRequest(nb, E.DenoiseSchedule(STEPS), seed=0)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    noise = [torch.randn(mc.block_len, mc.model_dim, device="cuda", generator=g) for _ in range(nb)]
+    eng = UlyssesEngine(model, comm, kvc)
+    roll = lambda: eng.generate(req, noise_provider=lambda ch: noise[ch], gather=False)  # noqa: E731
+    for _ in range(args.warmup):
+        roll()
+    torch.cuda.synchronize()
+    dist.barrier()
+    eng.runner.attn_events = []
+    l0 = _device.LAUNCHES[0]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            roll()
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    attn_ms = sum(a.elapsed_time(b) for a, b in eng.runner.attn_events)
+    eng.runner.attn_events = None
+    launches = _device.LAUNCHES[0] - l0
+    peak, peak_src = load_peaks()
+    # algorithmic FLOPs of this rank's heads (dummy padding heads excluded)
+    flops_rank = attn_flops_per_rollout(c) * args.steps / world
+    achieved = flops_rank / (attn_ms / 1e3) / 1e12 if attn_ms > 0 else None
+    # e2e: host noise (reference seeding) in, gathered latents out
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        lats = eng.generate(req)
+        host = [l.cpu() for l in lats]
+    torch.cuda.synchronize()
+    e2e = torch.tensor([(time.perf_counter() - t0) / args.steps], device="cuda")
+    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    clocks = clk.summary()
+    if rank == 0:
+        T, D = mc.block_len, mc.model_dim
+        line = {"metric": METRIC, "value": nb * FRAMES_PER_BLOCK / (ms / 1e3), "unit": UNIT,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (device-seeded noise, random-init weights)",
+                "config": {"workload": c["desc"], "parallelism": f"ulysses{world}",
+                           "heads_padded": model.heads_pad, "l2": "inputs larger than L2"},
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                             "frac": achieved / peak if achieved else None, "traffic": None,
+                             "peak_source": peak_src, "scope": "rank 0's K1 launches"},
+                "e2e": {"value": nb * FRAMES_PER_BLOCK / float(e2e.item()), "unit": UNIT,
+                        "h2d_bytes_per_step": nb * T * D * 4 // world,
+                        "d2h_bytes_per_step": nb * T * D * 4},
+                "comm": {"a2a_messages": comm.messages, "a2a_bytes": comm.bytes},
+                "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

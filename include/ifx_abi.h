@@ -150,12 +150,14 @@ int ifx_attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream);
 int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
                  float* x_out, void* y, void* stream);
 
-/* Ulysses re-shard pack/unpack (parallel.py:150-169): seq-sharded [n, H*dh] <-> per-peer
- * contiguous [W][n, (H/W)*dh] chunks for a single all-to-all. */
-int ifx_ulysses_pack(const void* src, int64_t n, int64_t width, int64_t src_ld, int64_t world,
-                     int type, void* dst, void* stream);
-int ifx_ulysses_unpack(const void* src, int64_t n, int64_t width, int64_t world, int type,
-                       void* dst, int64_t dst_ld, void* stream);
+/* Ulysses head<->sequence re-shard (parallel.py:150-169). A row-major [n][groups][world]
+ * [chunk] activation (e.g. groups=3 for fused Q|K|V, each split into per-peer head chunks)
+ * is packed as [world][n][groups][chunk] so one all-to-all moves every peer's heads
+ * contiguously; unpack is the inverse. Element type F32 or BF16; chunk*size % 16 == 0. */
+int ifx_ulysses_pack(const void* src, int64_t n, int64_t groups, int64_t world, int64_t chunk,
+                     int64_t src_ld, int type, void* dst, void* stream);
+int ifx_ulysses_unpack(const void* src, int64_t n, int64_t groups, int64_t world, int64_t chunk,
+                       int type, void* dst, int64_t dst_ld, void* stream);
 
 #ifdef __cplusplus
 }

@@ -97,8 +97,8 @@ def lib() -> ctypes.CDLL:
             L.ifx_attn_fwd.argtypes = [ctypes.POINTER(AttnParams), P]
             L.ifx_attn_fwd_variant.argtypes = [ctypes.POINTER(AttnParams), ctypes.c_int, P]
             L.ifx_rms_bf16.argtypes = [P, I64, I64, P, ctypes.c_float, P, P, P]
-            L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, ctypes.c_int, P, P]
-            L.ifx_ulysses_unpack.argtypes = [P, I64, I64, I64, ctypes.c_int, P, I64, P]
+            L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]
+            L.ifx_ulysses_unpack.argtypes = [P, I64, I64, I64, I64, ctypes.c_int, P, I64, P]
             _lib = L
     return _lib
 

@@ -15,6 +15,14 @@ import torch
 from . import _abi
 from .errors import DimensionError
 
+# Count of OUR kernels enqueued (K1/K2/K7/RMS/Ulysses); bench.py reports the delta over
+# its timed region as `gpu_launches`.
+LAUNCHES = [0]
+
+
+def count_launch(n: int = 1) -> None:
+    LAUNCHES[0] += n
+
 
 def require_cuda() -> torch.device:
     if not torch.cuda.is_available():
@@ -82,6 +90,7 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
     else:
         rc = L.ifx_attn_fwd_variant(ctypes.byref(p), variant, stream_ptr(stream))
     _abi.check(rc, "attn_fwd")
+    LAUNCHES[0] += 1
     return out
 
 
@@ -91,6 +100,7 @@ def rms_bf16(x: torch.Tensor, out: torch.Tensor, tvec: torch.Tensor | None = Non
     rows, width = x.shape
     _abi.check(_abi.lib().ifx_rms_bf16(x.data_ptr(), rows, width, ptr(tvec), float(t),
                                        ptr(x_out), out.data_ptr(), stream_ptr(stream)), "rms")
+    LAUNCHES[0] += 1
     return out
 
 

@@ -160,26 +160,26 @@ int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec,
   return ifx::cuda_fail(e, "rms launch");
 }
 
-int ifx_ulysses_pack(const void* src, int64_t n, int64_t width, int64_t src_ld, int64_t world,
-                     int type, void* dst, void* stream) {
+int ifx_ulysses_pack(const void* src, int64_t n, int64_t groups, int64_t world, int64_t chunk,
+                     int64_t src_ld, int type, void* dst, void* stream) {
   const int esz = type == IFX_BF16 ? 2 : 4;
-  if (world < 1 || width % world) return ifx::fail(IFX_EDIM, "width not divisible by world");
-  const int64_t chunk_b = width / world * esz;
-  if (chunk_b % 16 || (src_ld * esz) % 16) return ifx::fail(IFX_EDIM, "chunks must be 16-byte multiples");
+  if (world < 1 || groups < 1 || chunk < 1 || n < 0) return ifx::fail(IFX_EDIM, "bad re-shard sizes");
+  if ((chunk * esz) % 16 || (src_ld * esz) % 16 || src_ld < groups * world * chunk)
+    return ifx::fail(IFX_EDIM, "re-shard chunks must be 16-byte multiples inside the row");
   if (n == 0) return IFX_OK;
-  int e = ifx::ulysses_launch(src, dst, n, world, chunk_b, src_ld * esz, true,
+  int e = ifx::ulysses_launch(src, dst, n, groups, world, chunk * esz, src_ld * esz, true,
                               static_cast<cudaStream_t>(stream));
   return ifx::cuda_fail(e, "ulysses pack");
 }
 
-int ifx_ulysses_unpack(const void* src, int64_t n, int64_t width, int64_t world, int type,
-                       void* dst, int64_t dst_ld, void* stream) {
+int ifx_ulysses_unpack(const void* src, int64_t n, int64_t groups, int64_t world, int64_t chunk,
+                       int type, void* dst, int64_t dst_ld, void* stream) {
   const int esz = type == IFX_BF16 ? 2 : 4;
-  if (world < 1 || width % world) return ifx::fail(IFX_EDIM, "width not divisible by world");
-  const int64_t chunk_b = width / world * esz;
-  if (chunk_b % 16 || (dst_ld * esz) % 16) return ifx::fail(IFX_EDIM, "chunks must be 16-byte multiples");
+  if (world < 1 || groups < 1 || chunk < 1 || n < 0) return ifx::fail(IFX_EDIM, "bad re-shard sizes");
+  if ((chunk * esz) % 16 || (dst_ld * esz) % 16 || dst_ld < groups * world * chunk)
+    return ifx::fail(IFX_EDIM, "re-shard chunks must be 16-byte multiples inside the row");
   if (n == 0) return IFX_OK;
-  int e = ifx::ulysses_launch(src, dst, n, world, chunk_b, dst_ld * esz, false,
+  int e = ifx::ulysses_launch(src, dst, n, groups, world, chunk * esz, dst_ld * esz, false,
                               static_cast<cudaStream_t>(stream));
   return ifx::cuda_fail(e, "ulysses unpack");
 }

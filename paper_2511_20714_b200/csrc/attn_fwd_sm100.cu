@@ -37,6 +37,18 @@ constexpr int BN = 128;          // keys per tile
 constexpr int NS = 2;            // smem stages for K and for V
 constexpr int NTHREADS = 192;    // 6 warps
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if max grows > 2^8
+constexpr int kPolyEvery = 4;              // every 4th exp2 of a full tile runs on the FMA pipe
+
+// 2^x on the FMA/ALU pipes (round-to-nearest split, cubic on [-0.5, 0.5], exponent add):
+// rel. error < 5e-4, far below bf16 P rounding. x is clamped to >= -125 (result ~0).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: low mantissa bits = round(x)
+  const float r = t - 12582912.f;
+  const float f = x - r;
+  const float p = fmaf(fmaf(fmaf(0.0555041087f, f, 0.2402265070f), f, 0.6931471806f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 
 template <int HD, bool kPInTmem>
 struct Layout {
@@ -260,9 +272,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (!ok) sv[i] = -INFINITY;
         }
       }
-      float mx = sv[0];
+      // 8 independent chains: one softmax warp per SM sub-partition has no other warp to
+      // hide FMNMX/FADD latency behind, so the reductions must carry their own ILP
+      float m8[8];
 #pragma unroll
-      for (int i = 1; i < BN; ++i) mx = fmaxf(mx, sv[i]);
+      for (int i = 0; i < 8; ++i) m8[i] = sv[i];
+#pragma unroll
+      for (int i = 8; i < BN; ++i) m8[i & 7] = fmaxf(m8[i & 7], sv[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       const float m_tile = mx * sl2;  // -inf if nothing visible
       m_exact = fmaxf(m_exact, m_tile);
       float alpha = 1.f;
@@ -273,13 +291,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         m_run = m_tile;
       }
       const float m_sub = (m_run == -INFINITY) ? 0.f : m_run;
-      float sum = 0.f;
+      float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (t.valid == BN && mrow == nullptr) {
+        // full unmasked tile: 1 in kPolyEvery exponentials on the FMA pipe (MUFU offload)
 #pragma unroll
-      for (int i = 0; i < BN; ++i) {
-        const float p = ex2(fmaf(sv[i], sl2, -m_sub));  // exp2(-inf) = 0 for masked keys
-        sv[i] = p;
-        sum += p;
+        for (int i = 0; i < BN; ++i) {
+          const float x = fmaf(sv[i], sl2, -m_sub);
+          const float p = (i % kPolyEvery == kPolyEvery - 1) ? ex2_poly(x) : ex2(x);
+          sv[i] = p;
+          s8[i & 7] += p;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < BN; ++i) {
+          const float p = ex2(fmaf(sv[i], sl2, -m_sub));  // exp2(-inf) = 0 for masked keys
+          sv[i] = p;
+          s8[i & 7] += p;
+        }
       }
+      const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
       l_run = l_run * alpha + sum;
 
       // tcgen05.ld/st are warp-collective: rescale if any row of this warp needs it

@@ -121,18 +121,22 @@ __global__ void rms_bf16_kernel(const float* __restrict__ x, int64_t rows, int64
   }
 }
 
-// ---- Ulysses: [n, W*w] <-> [W][n, w] (16-byte vectors) ---------------------------------
+// ---- Ulysses re-shard (parallel.py:150-169): row-major [n][G][W][c] <-> packed [W][n][G][c]
+// (G column groups, e.g. Q|K|V, each split into W per-peer chunks of c elements), so one
+// all-to-all moves every peer's chunk contiguously. 16-byte vectors.
 __global__ void ulysses_transpose(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
-                                  int64_t n, int64_t world, int64_t chunk_vecs, int64_t ld_b,
-                                  bool pack) {
-  const int64_t total = n * world * chunk_vecs;
+                                  int64_t n, int64_t groups, int64_t world, int64_t chunk_vecs,
+                                  int64_t ld_b, bool pack) {
+  const int64_t total = n * groups * world * chunk_vecs;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = i % chunk_vecs;
-    const int64_t rr = i / chunk_vecs;
-    const int64_t r = rr % n, p = rr / n;  // p = peer
-    const int64_t packed = ((p * n + r) * chunk_vecs + c) * 16;
-    const int64_t rowmaj = r * ld_b + (p * chunk_vecs + c) * 16;
+    int64_t rest = i / chunk_vecs;
+    const int64_t g = rest % groups;
+    rest /= groups;
+    const int64_t r = rest % n, p = rest / n;  // packed order: p, r, g, c
+    const int64_t packed = i * 16;
+    const int64_t rowmaj = r * ld_b + ((g * world + p) * chunk_vecs + c) * 16;
     if (pack)
       *reinterpret_cast<uint4*>(dst + packed) = ld_nc(src + rowmaj);
     else
@@ -193,12 +197,13 @@ int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, f
   return (int)cudaGetLastError();
 }
 
-int ulysses_launch(const void* src, void* dst, int64_t n, int64_t world, int64_t chunk_bytes,
-                   int64_t ld_bytes, bool pack, cudaStream_t st) {
+int ulysses_launch(const void* src, void* dst, int64_t n, int64_t groups, int64_t world,
+                   int64_t chunk_bytes, int64_t ld_bytes, bool pack, cudaStream_t st) {
   const int threads = 256;
   const int64_t cv = chunk_bytes / 16;
-  ulysses_transpose<<<grid_for(n * world * cv, threads), threads, 0, st>>>(
-      static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), n, world, cv, ld_bytes, pack);
+  ulysses_transpose<<<grid_for(n * groups * world * cv, threads), threads, 0, st>>>(
+      static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), n, groups, world, cv, ld_bytes,
+      pack);
   return (int)cudaGetLastError();
 }
 

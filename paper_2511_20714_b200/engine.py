@@ -119,31 +119,33 @@ def padded_head_dim(head_dim: int) -> int:
     raise ConfigError("head_dim > 128 is not supported by the B200 attention kernel")
 
 
-def _pad_cols(w: torch.Tensor, heads: int, dh: int, dhp: int) -> torch.Tensor:
-    if dh == dhp:
+def _pad_cols(w: torch.Tensor, heads: int, heads_pad: int, dh: int, dhp: int) -> torch.Tensor:
+    """[in, heads*dh] -> [in, heads_pad*dhp]: per-head zero columns + zero dummy heads."""
+    if dh == dhp and heads == heads_pad:
         return w
-    out = w.new_zeros(w.shape[0], heads, dhp)
-    out[:, :, :dh] = w.view(w.shape[0], heads, dh)
-    return out.view(w.shape[0], heads * dhp)
+    out = w.new_zeros(w.shape[0], heads_pad, dhp)
+    out[:, :heads, :dh] = w.view(w.shape[0], heads, dh)
+    return out.view(w.shape[0], heads_pad * dhp)
 
 
-def _pad_rows(w: torch.Tensor, heads: int, dh: int, dhp: int) -> torch.Tensor:
-    if dh == dhp:
+def _pad_rows(w: torch.Tensor, heads: int, heads_pad: int, dh: int, dhp: int) -> torch.Tensor:
+    """[heads*dh, out] -> [heads_pad*dhp, out] with zero rows for padding."""
+    if dh == dhp and heads == heads_pad:
         return w
-    out = w.new_zeros(heads, dhp, w.shape[1])
-    out[:, :dh] = w.view(heads, dh, w.shape[1])
-    return out.view(heads * dhp, w.shape[1])
+    out = w.new_zeros(heads_pad, dhp, w.shape[1])
+    out[:heads, :dh] = w.view(heads, dh, w.shape[1])
+    return out.view(heads_pad * dhp, w.shape[1])
 
 
 class _LayerWeights:
-    """Device weights of one layer: fused [D, 3Dp] QKV, bf16 GEMM operands (Dp = heads x
-    padded head width); the prompt projections ck/cv stay fp32 (they run once per prompt,
-    engine.py:224-225)."""
+    """Device weights of one layer: fused [D, 3Dp] QKV, bf16 GEMM operands (Dp = padded
+    heads x padded head width; padding is exact zeros); the prompt projections ck/cv
+    stay fp32 (they run once per prompt, engine.py:224-225)."""
 
-    def __init__(self, w: dict, dev, heads: int, dh: int, dhp: int):
+    def __init__(self, w: dict, dev, heads: int, heads_pad: int, dh: int, dhp: int):
         f32 = lambda a: torch.as_tensor(a).to(dev, torch.float32)  # noqa: E731
-        cols = lambda a: _pad_cols(f32(a), heads, dh, dhp)  # noqa: E731
-        rows = lambda a: _pad_rows(f32(a), heads, dh, dhp)  # noqa: E731
+        cols = lambda a: _pad_cols(f32(a), heads, heads_pad, dh, dhp)  # noqa: E731
+        rows = lambda a: _pad_rows(f32(a), heads, heads_pad, dh, dhp)  # noqa: E731
         bf = torch.bfloat16
         self.wqkv = torch.cat([cols(w["wq"]), cols(w["wk"]), cols(w["wv"])], dim=1).to(bf).contiguous()
         self.wo, self.cq, self.co = rows(w["wo"]).to(bf), cols(w["cq"]).to(bf), rows(w["co"]).to(bf)
@@ -157,16 +159,21 @@ class ToyModel:
     weights="reference": identical PCG64 draws to the reference (bit-identical fp32
     source, then cast to bf16 for the GEMMs). weights="device": torch.randn on the GPU
     (same shapes / scales; for the 14B-shaped configs where host generation of ~10^10
-    normals is impractical — not bit-comparable with the reference)."""
+    normals is impractical — not bit-comparable with the reference).
 
-    def __init__(self, config: ModelConfig, weights: str = "reference"):
+    head_multiple: pad the head count with zero dummy heads to a multiple of this (Ulysses
+    over W ranks needs heads % W == 0, parallel.py:143-144; dummy heads output exact 0)."""
+
+    def __init__(self, config: ModelConfig, weights: str = "reference", head_multiple: int = 1):
         config.validate()
         self.config = config
         dev = require_cuda()
         d, p = config.model_dim, config.prompt_dim
         h, wd = config.frame_shape
         self.dh_pad = padded_head_dim(config.head_dim)
-        lw = lambda ws: _LayerWeights(ws, dev, config.heads, config.head_dim, self.dh_pad)  # noqa: E731
+        self.heads_pad = -(-config.heads // head_multiple) * head_multiple
+        lw = lambda ws: _LayerWeights(ws, dev, config.heads, self.heads_pad, config.head_dim,  # noqa: E731
+                                      self.dh_pad)
         shapes = {"wq": (d, d), "wk": (d, d), "wv": (d, d), "wo": (d, d), "cq": (d, d),
                   "ck": (p, d), "cv": (p, d), "co": (d, d), "w1": (d, 2 * d), "w2": (2 * d, d)}
         if weights == "reference":
@@ -205,8 +212,8 @@ class ToyModel:
 
     @property
     def attn_width(self) -> int:
-        """Row width of Q/K/V/O and of the KV slabs (heads x padded head width)."""
-        return self.config.heads * self.dh_pad
+        """Row width of Q/K/V/O and of the KV slabs (padded heads x padded head width)."""
+        return self.heads_pad * self.dh_pad
 
 
 def build_model(config: ModelConfig, **kw) -> ToyModel:
@@ -270,14 +277,13 @@ class BlockRunner:
         self.dev = require_cuda()
         self.ws = _Workspace(c.block_len, c.model_dim, model.attn_width, self.dev)
         self.attn_events = None
-        self.kernel_launches = 0
 
     def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
                 collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None):
         """One pass. ctx[l] = (slab, base, total) or None; cross[l] = (k, v, row0, n) or None."""
         m, ws = self.model, self.ws
         c = m.config
-        H, dhp, Dp = c.heads, m.dh_pad, m.attn_width
+        H, dhp, Dp = m.heads_pad, m.dh_pad, m.attn_width
         sc = 1.0 / math.sqrt(c.head_dim)
         q, kc, vc = ws.qkv[:, :Dp], ws.qkv[:, Dp:2 * Dp], ws.qkv[:, 2 * Dp:]
         for li, lw in enumerate(m.layers):
@@ -308,19 +314,15 @@ class BlockRunner:
                 torch.mm(ws.h, lw.cq, out=ws.q2)
                 attn_fwd(ws.q2, H, dhp, ws.attn, xk, xv, row0, n, scale=sc)
                 _residual(ws.x, ws.attn, lw.co, ws.tmp)
-                self.kernel_launches += 2
             rms_bf16(ws.x, ws.h)
             torch.mm(ws.h, lw.w1, out=ws.ffn)
             ws.ffn.relu_()
             _residual(ws.x, ws.ffn, lw.w2, ws.tmp)
-            self.kernel_launches += 3
             if collect_kv:  # clean pass: page write of this layer's K/V (engine.py:303-306)
                 cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
-                self.kernel_launches += 1
         if eps_out is not None:
             rms_bf16(ws.x, ws.h)
             torch.mm(ws.h, m.w_out, out_dtype=torch.float32, out=eps_out)
-            self.kernel_launches += 1
 
     def denoise(self, latent: torch.Tensor, schedule: DenoiseSchedule, ctx, cross,
                 cache: KvCache | None, chunk_index: int) -> torch.Tensor:

@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._device import dtype_code, require_cuda, row_ld, stream_ptr
+from ._device import count_launch, dtype_code, require_cuda, row_ld, stream_ptr
 from .errors import ConfigError, DimensionError, OutOfRangeError
 
 DUMP_MAGIC = b"INFKV1"  # kvcache.py:22
@@ -235,10 +235,12 @@ class KvCache:
     Extra keyword arguments (B200 only): `dtype` of the device slabs (torch.float32 for
     bit-exact API parity, torch.bfloat16 for the engine), `reserve_tokens` rows to
     pre-allocate per self-attention stream, `row_width` of the device rows when it
-    differs from head_dim (the engine stores per-head zero-padded rows)."""
+    differs from head_dim (the engine stores per-head zero-padded rows; a Ulysses rank
+    stores only its heads), `cross_row_width` likewise for the cross-attention streams."""
 
     def __init__(self, config: KvConfig, dtype: torch.dtype = torch.float32,
-                 reserve_tokens: int = 0, row_width: int | None = None):
+                 reserve_tokens: int = 0, row_width: int | None = None,
+                 cross_row_width: int | None = None):
         config.validate()
         self.config = config
         self.dtype = dtype
@@ -247,11 +249,12 @@ class KvCache:
         if row_width is not None and config.latent is not None:
             raise ConfigError("row_width override is not supported in latent mode")
         w = row_width or config.stored_width
-        self._row_width = w
+        wc = cross_row_width or w
+        self._row_width = {SELF_ATTN: w, CROSS_ATTN: wc}
         self._slabs = {}
         for layer in range(config.num_layers):
             self._slabs[(layer, SELF_ATTN)] = _Slab(w, dtype, reserve_tokens)
-            self._slabs[(layer, CROSS_ATTN)] = _Slab(w, dtype, 64)
+            self._slabs[(layer, CROSS_ATTN)] = _Slab(wc, dtype, 64)
         self._latent_down = self._latent_up = None
         if config.latent is not None:
             dev = require_cuda()
@@ -286,7 +289,7 @@ class KvCache:
         t, d = k.shape
         if t < 1:
             raise DimensionError("append needs at least one token")
-        if d != cfg.head_dim and d != self._row_width:
+        if d != cfg.head_dim and d != self._row_width.get(kind):
             raise DimensionError(f"width {d} != head_dim {cfg.head_dim}")
         if not 0 <= layer < cfg.num_layers:
             raise OutOfRangeError(f"layer {layer} out of range")
@@ -306,6 +309,7 @@ class KvCache:
                     k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype),
                     s.k.data_ptr(), s.v.data_ptr(), s.width, dtype_code(s.dtype),
                     total - written - s.origin, written, s.width, stream_ptr(stream)), "kv_append")
+                count_launch()
             _abi.check(rc, "append_block")
             return BlockEntry(bid, layer, (start, start + t), pages, kind, chunk_index)
 
@@ -345,6 +349,7 @@ class KvCache:
                 s.k.data_ptr(), s.v.data_ptr(), s.width, dtype_code(s.dtype),
                 None if rows is None else rows.data_ptr(), first - s.origin, n, s.width,
                 ko.data_ptr(), vo.data_ptr(), stream_ptr()), "kv_gather")
+            count_launch()
         if self._latent_up is not None:
             ko, vo = ko.float() @ self._latent_up, vo.float() @ self._latent_up
         return ko, vo

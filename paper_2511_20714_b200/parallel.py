@@ -1,0 +1,414 @@
+"""Ulysses sequence/head parallelism on B200 — drop-in for `inferix.parallel`'s Ulysses path.
+
+Reference: /root/reference/pkg/src/inferix/parallel.py. Two layers:
+
+1. The reference's in-process API (WorkerGroup / all_to_all / ulysses_attention /
+   dense_reference / predict_communication / choose_strategy, parallel.py:38-169,304-364)
+   with the same trace and byte accounting (FLOAT_BYTES = 4) so the cost model stays
+   checkable; local attention runs in K1.
+
+2. The real thing, one process per GPU (`torch.distributed`, NCCL over NVLink/NVSwitch):
+   `UlyssesComm` re-shards a rank's sequence slice of the fused Q|K|V projection into the
+   full sequence of its head group with ONE all-to-all (pack kernel -> a2a), and the
+   attention output back with one all-to-all (a2a -> unpack kernel). `UlyssesEngine`
+   runs the generate-and-cache loop with activations sequence-sharded, attention
+   head-sharded, the KV cache head-sharded and rank-local (never communicated), the page
+   table replicated and identical on every rank, and cross-attention sequence-sharded
+   against replicated prompt K/V (no communication).
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from .attention import scaled_dot_attention
+from .errors import DimensionError
+
+FLOAT_BYTES = 4  # parallel.py:38 — the reference's cost model counts fp32 elements
+
+
+# ===================================================================== reference API
+def _payload_bytes(payload) -> int:
+    """parallel.py:41-49."""
+    if isinstance(payload, (np.ndarray, torch.Tensor)):
+        return int(np.prod(tuple(payload.shape))) * FLOAT_BYTES
+    if isinstance(payload, (tuple, list)):
+        return sum(_payload_bytes(p) for p in payload)
+    raise DimensionError(f"untraceable payload type {type(payload)!r}")
+
+
+@dataclass
+class TraceRecord:
+    """parallel.py:52-60."""
+    step: int
+    sender: int
+    receiver: int
+    bytes: int
+    tag: str
+
+    def to_line(self) -> str:
+        return f"{self.step}\t{self.sender}\t{self.receiver}\t{self.bytes}\t{self.tag}"
+
+
+class WorkerGroup:
+    """parallel.py:63-98 — world_size simulated ranks with FIFO channels and a send trace."""
+
+    def __init__(self, world_size: int):
+        if world_size < 1:
+            raise DimensionError("world_size must be >= 1")
+        self.world_size = world_size
+        self.channels = {(i, j): [] for i in range(world_size) for j in range(world_size)}
+        self.trace: list = []
+        self._lock = threading.Lock()
+        self._step = 0
+
+    def send(self, sender: int, receiver: int, payload, tag: str = ""):
+        with self._lock:
+            self.trace.append(TraceRecord(self._step, sender, receiver, _payload_bytes(payload), tag))
+            self.channels[(sender, receiver)].append(payload)
+
+    def recv(self, sender: int, receiver: int, timeout: float = 10.0):
+        with self._lock:
+            return self.channels[(sender, receiver)].pop(0)
+
+    def advance_step(self):
+        with self._lock:
+            self._step += 1
+
+    def total_bytes(self, tag=None) -> int:
+        return sum(r.bytes for r in self.trace if tag is None or r.tag == tag)
+
+    def message_count(self, tag=None) -> int:
+        return sum(1 for r in self.trace if tag is None or r.tag == tag)
+
+    def export_trace(self) -> str:
+        return "\n".join(r.to_line() for r in self.trace)
+
+
+def all_to_all(group: WorkerGroup, per_worker_send):
+    """parallel.py:101-111 — recv[j][i] == send[i][j]; every pair is one message."""
+    w = group.world_size
+    if len(per_worker_send) != w or any(len(row) != w for row in per_worker_send):
+        raise DimensionError("send matrix must be world_size x world_size")
+    for i in range(w):
+        for j in range(w):
+            group.send(i, j, per_worker_send[i][j], tag="a2a")
+    recv = [[group.recv(i, j) for i in range(w)] for j in range(w)]
+    group.advance_step()
+    return recv
+
+
+def equal_shards(seq_len: int, world_size: int) -> list:
+    """parallel.py:312-314."""
+    base, rem = divmod(seq_len, world_size)
+    return [base + (1 if i < rem else 0) for i in range(world_size)]
+
+
+def _dev(x) -> torch.Tensor:
+    return x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, np.float32)).cuda()
+
+
+def _mha_dense(q, k, v, heads, mask):
+    """parallel.py:121-127 — per-head K1 launches."""
+    dh = q.shape[1] // heads
+    return torch.cat([scaled_dot_attention(q[:, h * dh:(h + 1) * dh], k[:, h * dh:(h + 1) * dh],
+                                           v[:, h * dh:(h + 1) * dh], mask)
+                      for h in range(heads)], dim=1)
+
+
+def dense_reference(q_shards, k_shards, v_shards, heads, mask):
+    """parallel.py:130-137."""
+    q = torch.cat([_dev(s) for s in q_shards])
+    k = torch.cat([_dev(s) for s in k_shards])
+    v = torch.cat([_dev(s) for s in v_shards])
+    out = _mha_dense(q, k, v, heads, _dev_mask(mask))
+    cuts = np.cumsum([0] + [s.shape[0] for s in q_shards])
+    return [out[cuts[i]:cuts[i + 1]] for i in range(len(q_shards))]
+
+
+def _dev_mask(mask) -> torch.Tensor:
+    return mask.bool() if isinstance(mask, torch.Tensor) else torch.as_tensor(np.asarray(mask, bool)).cuda()
+
+
+def ulysses_attention(group: WorkerGroup, q_shards, k_shards, v_shards, heads, mask):
+    """parallel.py:140-169 — sequence-sharded in/out via head repartitioning (simulated
+    ranks, device tensors, K1 local attention)."""
+    w = group.world_size
+    if heads % w != 0:
+        raise DimensionError(f"heads {heads} not divisible by world_size {w}")
+    qs, ks, vs = ([_dev(s) for s in x] for x in (q_shards, k_shards, v_shards))
+    d = qs[0].shape[1]
+    hpw = heads // w
+    cw = hpw * (d // heads)
+    col = lambda j: slice(j * cw, (j + 1) * cw)  # noqa: E731
+    send = [[(qs[i][:, col(j)], ks[i][:, col(j)], vs[i][:, col(j)]) for j in range(w)] for i in range(w)]
+    recv = all_to_all(group, send)
+    m = _dev_mask(mask)
+    outs = []
+    for j in range(w):
+        q = torch.cat([recv[j][i][0] for i in range(w)])
+        k = torch.cat([recv[j][i][1] for i in range(w)])
+        v = torch.cat([recv[j][i][2] for i in range(w)])
+        outs.append(_mha_dense(q, k, v, hpw, m))
+    cuts = np.cumsum([0] + [s.shape[0] for s in qs])
+    back = [[outs[j][cuts[i]:cuts[i + 1]] for i in range(w)] for j in range(w)]
+    recv_back = all_to_all(group, back)
+    return [torch.cat(recv_back[i], dim=1) for i in range(w)]
+
+
+@dataclass
+class LinkCostModel:
+    """parallel.py:305-309 — cost = cost_per_message * messages + cost_per_byte * bytes."""
+    cost_per_message: float = 1e-6
+    cost_per_byte: float = 1e-9
+
+
+def predict_communication(strategy, shard_lens, heads, head_dim, world_size, elem_bytes=FLOAT_BYTES):
+    """parallel.py:317-343 — (messages, bytes) on the wire, self-sends excluded.
+    `elem_bytes` (B200 extension) = 2 for the bf16 activations UlyssesComm moves."""
+    w, d = world_size, heads * head_dim
+    if w == 1:
+        return 0, 0
+    n = sum(shard_lens)
+    if strategy == "ulysses":
+        return 2 * w * (w - 1), (w - 1) * 4 * n * (d // w) * elem_bytes
+    if strategy == "ring_pass_kv":
+        return w * (w - 1), (w - 1) * 2 * n * d * elem_bytes
+    if strategy == "ring_pass_q":
+        rot = n * d + n * (d + 2 * heads)
+        return w * (w - 1) + w, ((w - 1) * rot + n * (d + 2 * heads)) * elem_bytes
+    raise DimensionError(f"unknown strategy {strategy!r}")
+
+
+STRATEGIES = ("ulysses", "ring_pass_kv", "ring_pass_q")
+
+
+def choose_strategy(seq_len, heads, world_size, link_cost_model: LinkCostModel, head_dim: int = 8):
+    """parallel.py:349-364 — argmin predicted cost; ties break in listed order."""
+    shard_lens = equal_shards(seq_len, world_size)
+    best = None
+    for name in STRATEGIES:
+        if name == "ulysses" and heads % world_size != 0:
+            continue
+        msgs, nbytes = predict_communication(name, shard_lens, heads, head_dim, world_size)
+        cost = link_cost_model.cost_per_message * msgs + link_cost_model.cost_per_byte * nbytes
+        if best is None or cost < best[1]:
+            best = (name, cost, msgs, nbytes)
+    name, cost, msgs, nbytes = best
+    return {"strategy": name, "cost": cost, "messages": msgs, "bytes": nbytes}
+
+
+# ===================================================================== real multi-GPU path
+def _pack_cuda(src: torch.Tensor, groups: int, world: int, chunk: int) -> torch.Tensor:
+    from ._device import count_launch, dtype_code, row_ld, stream_ptr
+    n = src.shape[0]
+    dst = torch.empty(world, n, groups, chunk, device=src.device, dtype=src.dtype)
+    _abi.check(_abi.lib().ifx_ulysses_pack(src.data_ptr(), n, groups, world, chunk, row_ld(src),
+                                           dtype_code(src.dtype), dst.data_ptr(), stream_ptr()),
+               "ulysses_pack")
+    count_launch()
+    return dst
+
+
+def _unpack_cuda(src: torch.Tensor, out: torch.Tensor, groups: int, world: int, chunk: int):
+    from ._device import count_launch, dtype_code, row_ld, stream_ptr
+    n = out.shape[0]
+    _abi.check(_abi.lib().ifx_ulysses_unpack(src.data_ptr(), n, groups, world, chunk,
+                                             dtype_code(out.dtype), out.data_ptr(), row_ld(out),
+                                             stream_ptr()), "ulysses_unpack")
+    count_launch()
+    return out
+
+
+class UlyssesComm:
+    """Head<->sequence re-shard over a torch.distributed group (NCCL on NVLink/NVSwitch).
+
+    seq_to_head: rank r's [n, G*W*c] (G groups, e.g. Q|K|V, each W per-peer head chunks of
+    c columns) -> [W*n, G*c], the FULL sequence (ranks hold contiguous sequence slices in
+    rank order) for rank r's heads. head_to_seq is the inverse for one group.
+    One all-to-all per direction; `trace` accumulates (messages, bytes) excluding self."""
+
+    def __init__(self, group=None, pack=None, unpack=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self._pack = pack or _pack_cuda
+        self._unpack = unpack or _unpack_cuda
+        self.messages = 0
+        self.bytes = 0
+
+    def _a2a(self, send: torch.Tensor) -> torch.Tensor:
+        recv = torch.empty_like(send)
+        if send.is_cuda and self.dist.get_backend(self.group) != "nccl":
+            # non-NCCL group (e.g. gloo tests of several ranks sharing one GPU): stage on host
+            r = torch.empty(send.shape, dtype=send.dtype)
+            self.dist.all_to_all_single(r, send.cpu(), group=self.group)
+            recv.copy_(r)
+        else:
+            self.dist.all_to_all_single(recv, send, group=self.group)
+        w = self.world
+        self.messages += w - 1
+        self.bytes += send.numel() * send.element_size() * (w - 1) // w
+        return recv
+
+    def seq_to_head(self, x: torch.Tensor, groups: int) -> torch.Tensor:
+        n = x.shape[0]
+        chunk = x.shape[1] // (groups * self.world)
+        packed = self._pack(x, groups, self.world, chunk)  # [W, n, G, c]
+        recv = self._a2a(packed)                            # [W(src), n, G, c]
+        return recv.view(self.world * n, groups * chunk)
+
+    def head_to_seq(self, y: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        chunk = y.shape[1]
+        n = y.shape[0] // self.world
+        recv = self._a2a(y.contiguous().view(self.world, n, 1, chunk))  # [W(src heads), n, 1, c]
+        return self._unpack(recv, out, 1, self.world, chunk)
+
+
+class UlyssesRunner:
+    """BlockRunner (engine.py) for one Ulysses rank: sequence-sharded activations,
+    head-sharded attention over the rank-local KV shard (engine.py:185-221 semantics)."""
+
+    def __init__(self, model, comm: UlyssesComm, attn=None):
+        from ._device import attn_fwd
+        self.model, self.comm = model, comm
+        c = model.config
+        W = comm.world
+        if model.heads_pad % W:
+            raise DimensionError(f"heads {model.heads_pad} not divisible by world_size {W}")
+        if c.block_len % W:
+            raise DimensionError(f"block_len {c.block_len} not divisible by world_size {W}")
+        self.n = c.block_len // W
+        self.hl = model.heads_pad // W
+        self.wl = self.hl * model.dh_pad
+        self._attn = attn or attn_fwd
+        dev = model.time_vec.device
+        D, Dp, n, T = c.model_dim, model.attn_width, self.n, c.block_len
+        self.x = torch.empty(n, D, device=dev)
+        self.h = torch.empty(n, D, device=dev, dtype=torch.bfloat16)
+        self.qkv = torch.empty(n, 3 * Dp, device=dev, dtype=torch.bfloat16)
+        self.attn_h = torch.empty(T, self.wl, device=dev, dtype=torch.bfloat16)
+        self.attn_s = torch.empty(n, Dp, device=dev, dtype=torch.bfloat16)
+        self.q2 = torch.empty(n, Dp, device=dev, dtype=torch.bfloat16)
+        self.ffn = torch.empty(n, 2 * D, device=dev, dtype=torch.bfloat16)
+        self.tmp = torch.empty(n, D, device=dev)
+        self.eps = torch.empty(n, D, device=dev)
+        self.attn_events = None
+
+    def _rms(self, x, out, tvec=None, t=0.0, x_out=None):
+        from ._device import rms_bf16
+        return rms_bf16(x, out, tvec, t, x_out)
+
+    def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None):
+        from .kvcache import SELF_ATTN
+        m = self.model
+        c = m.config
+        dhp, wl = m.dh_pad, self.wl
+        sc = 1.0 / math.sqrt(c.head_dim)
+        for li, lw in enumerate(m.layers):
+            if li == 0:
+                self._rms(latent, self.h, m.time_vec, t, self.x)
+            else:
+                self._rms(self.x, self.h)
+            torch.mm(self.h, lw.wqkv, out=self.qkv)
+            qkv_h = self.comm.seq_to_head(self.qkv, 3)          # [T, 3*wl] local heads
+            q, kc, vc = qkv_h[:, :wl], qkv_h[:, wl:2 * wl], qkv_h[:, 2 * wl:]
+            ev = self.attn_events
+            if ev is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            s, base, total = ctx[li]
+            if total > base:
+                self._attn(q, self.hl, dhp, self.attn_h, s.k, s.v, base - s.origin, total - base,
+                           kc, vc, scale=sc)
+            else:
+                self._attn(q, self.hl, dhp, self.attn_h, cur_k=kc, cur_v=vc, scale=sc)
+            if ev is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                ev.append((e0, e1))
+            self.comm.head_to_seq(self.attn_h, self.attn_s)      # [n, Dp]
+            torch.mm(self.attn_s, lw.wo, out_dtype=torch.float32, out=self.tmp)
+            self.x.add_(self.tmp)
+            if cross is not None:  # sequence-sharded vs replicated prompt K/V: no comm
+                xk, xv, row0, nx = cross[li]
+                self._rms(self.x, self.h)
+                torch.mm(self.h, lw.cq, out=self.q2)
+                self._attn(self.q2, m.heads_pad, dhp, self.attn_s, xk, xv, row0, nx, scale=sc)
+                torch.mm(self.attn_s, lw.co, out_dtype=torch.float32, out=self.tmp)
+                self.x.add_(self.tmp)
+            self._rms(self.x, self.h)
+            torch.mm(self.h, lw.w1, out=self.ffn)
+            self.ffn.relu_()
+            torch.mm(self.ffn, lw.w2, out_dtype=torch.float32, out=self.tmp)
+            self.x.add_(self.tmp)
+            if collect_kv:  # rank-local page write of this rank's heads
+                cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
+        if eps_out is not None:
+            self._rms(self.x, self.h)
+            torch.mm(self.h, m.w_out, out_dtype=torch.float32, out=eps_out)
+
+    def denoise(self, latent, schedule, ctx, cross, cache, chunk_index):
+        for t in schedule.steps:
+            self.forward(latent, float(t), ctx, cross, cache, eps_out=self.eps)
+            latent.add_(self.eps, alpha=-float(schedule.step_scale))
+        self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
+                     chunk_index=chunk_index)
+        return latent
+
+
+class UlyssesEngine:
+    """Engine.generate (engine.py:368-411) across the ranks of `comm`. Every rank runs the
+    same page-table calls in the same order, so bookkeeping stays identical everywhere."""
+
+    def __init__(self, model, comm: UlyssesComm, kv_config=None, attn=None):
+        from .engine import default_kv_config
+        self.model, self.comm = model, comm
+        self.kv_config = kv_config or default_kv_config(model.config)
+        self.runner = UlyssesRunner(model, comm, attn)
+        self.cache = None
+
+    def generate(self, request, noise_provider=None, gather: bool = True):
+        """Returns per-block full latents (gathered) if `gather`, else local shards."""
+        from .engine import (_cross_from_cache, _ctx_from_cache, _cross_kv, _init_noise,
+                             _prompt_for_chunk, embed_prompt)
+        from .kvcache import CROSS_ATTN, KvCache
+        request.validate()
+        m, c, r = self.model, self.model.config, self.runner
+        T, n, rank = c.block_len, r.n, self.comm.rank
+        self.cache = KvCache(self.kv_config, dtype=torch.bfloat16,
+                             reserve_tokens=T * request.num_blocks, row_width=r.wl,
+                             cross_row_width=m.attn_width)
+        make_noise = noise_provider or (lambda ch: _init_noise(c, request.seed, ch))
+        cur = None
+        out = []
+        for chunk in range(request.num_blocks):
+            prompt = _prompt_for_chunk(request.prompt_schedule, chunk)
+            if prompt != cur:
+                if cur is not None:
+                    self.cache.clear_cross_attention()
+                for li, (kc, vc) in enumerate(_cross_kv(m, embed_prompt(m, prompt))):
+                    self.cache.append_block(li, kc, vc, kind=CROSS_ATTN, chunk_index=chunk)
+                cur = prompt
+            noise = make_noise(chunk)
+            full = noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)
+            lat = full[rank * n:(rank + 1) * n].to(m.time_vec.device, torch.float32).clone()
+            ctx = _ctx_from_cache(m, self.cache)
+            cross = _cross_from_cache(m, self.cache, None)
+            r.denoise(lat, request.schedule, ctx, cross, self.cache, chunk)
+            if request.kv_window is not None:
+                self.cache.evict_window(request.kv_window)
+            if gather:
+                parts = [torch.empty_like(lat) for _ in range(self.comm.world)]
+                self.comm.dist.all_gather(parts, lat, group=self.comm.group)
+                lat = torch.cat(parts)
+            out.append(lat)
+        return out

@@ -136,22 +136,25 @@ def test_rms_matches_torch():
     assert (y.float() - ref).abs().max().item() < 2e-2
 
 
-def test_ulysses_pack_unpack_roundtrip():
+@pytest.mark.parametrize("groups", [1, 3])
+def test_ulysses_pack_unpack_roundtrip(groups):
     from paper_2511_20714_b200 import _abi
     from paper_2511_20714_b200._device import stream_ptr
 
     L = _abi.lib()
-    n, width, world = 93, 1536, 4
-    x = torch.randn(n, width, device="cuda").bfloat16()
-    packed = torch.empty(world, n, width // world, device="cuda", dtype=torch.bfloat16)
-    _abi.check(L.ifx_ulysses_pack(x.data_ptr(), n, width, width, world, _abi.BF16,
+    n, world, chunk = 93, 4, 384
+    width = groups * world * chunk
+    x = torch.randn(n, width + 64, device="cuda").bfloat16()  # row stride > width
+    packed = torch.empty(world, n, groups, chunk, device="cuda", dtype=torch.bfloat16)
+    _abi.check(L.ifx_ulysses_pack(x.data_ptr(), n, groups, world, chunk, width + 64, _abi.BF16,
                                   packed.data_ptr(), stream_ptr()))
-    back = torch.empty_like(x)
-    _abi.check(L.ifx_ulysses_unpack(packed.data_ptr(), n, width, world, _abi.BF16,
+    back = torch.zeros(n, width, device="cuda", dtype=torch.bfloat16)
+    _abi.check(L.ifx_ulysses_unpack(packed.data_ptr(), n, groups, world, chunk, _abi.BF16,
                                     back.data_ptr(), width, stream_ptr()))
     torch.cuda.synchronize()
-    assert torch.equal(packed, x.view(n, world, width // world).permute(1, 0, 2))
-    assert torch.equal(back, x)
+    ref = x[:, :width].reshape(n, groups, world, chunk).permute(2, 0, 1, 3)
+    assert torch.equal(packed, ref)
+    assert torch.equal(back, x[:, :width])
 
 
 def test_addmm_out_dtype_fp32_residual():
