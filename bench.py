@@ -249,8 +249,10 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         torch.cuda.nvtx.range_push("timed")
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             rollout_device()
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # enqueue time (no sync inside)
         torch.cuda.nvtx.range_pop()
         e1.record()
         torch.cuda.synchronize()
@@ -304,6 +306,7 @@ def run_ours(args):
         "e2e": {"value": nb * FRAMES_PER_BLOCK / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
         "gpu_launches": launches,
+        "host_enqueue_ms_per_step": host_ms,
         "clocks": clocks,
         "cpu_baseline": cpu,
     }

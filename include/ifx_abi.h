@@ -134,15 +134,14 @@ typedef struct ifx_attn_params {
    * (attention.py:89); NULL = every key visible (engine.py:209) */
   const uint8_t* mask;
   int64_t mask_ld;
-  /* optional split-KV partials for merge (attention.py:127-173): when lse != NULL the
-   * kernel also writes per (head,row) running max (log2 domain) and denominator. */
+  /* optional partial-softmax statistics (attention.py:127-154): when row_max != NULL the
+   * kernel also writes per (head, row) the exact row max (log2 units, [heads, n_q]) and
+   * the denominator relative to it, so callers can merge partials (attention.py:157-173) */
   float* row_max;
   float* row_sum;
 } ifx_attn_params;
 
 int ifx_attn_fwd(const ifx_attn_params* p, void* stream);
-/* test hook: variant 0 = P staged in smem (SS MMA), 1 = P kept in TMEM (TS MMA, the default) */
-int ifx_attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream);
 
 /* Fused RMS-norm (engine.py:171-173) + optional time conditioning, fp32 in, bf16 out:
  * y = bf16( (x + t*tvec) / sqrt(mean((x + t*tvec)^2) + eps) ). If x_out != NULL the

@@ -39,7 +39,7 @@ EXPORTS = (
     "ifx_pt_clear_cross", "ifx_pt_touch_range", "ifx_pt_touch_indices", "ifx_pt_range",
     "ifx_pt_stats", "ifx_pt_snapshot",
     "ifx_kv_append", "ifx_kv_gather",
-    "ifx_attn_fwd", "ifx_attn_fwd_variant",
+    "ifx_attn_fwd",
     "ifx_rms_bf16", "ifx_ulysses_pack", "ifx_ulysses_unpack",
 )
 
@@ -95,7 +95,6 @@ def lib() -> ctypes.CDLL:
             L.ifx_kv_append.argtypes = [P, P, I64, ctypes.c_int, P, P, I64, ctypes.c_int, I64, I64, I64, P]
             L.ifx_kv_gather.argtypes = [P, P, I64, ctypes.c_int, P, I64, I64, I64, P, P, P]
             L.ifx_attn_fwd.argtypes = [ctypes.POINTER(AttnParams), P]
-            L.ifx_attn_fwd_variant.argtypes = [ctypes.POINTER(AttnParams), ctypes.c_int, P]
             L.ifx_rms_bf16.argtypes = [P, I64, I64, P, ctypes.c_float, P, P, P]
             L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]
             L.ifx_ulysses_unpack.argtypes = [P, I64, I64, I64, I64, ctypes.c_int, P, I64, P]

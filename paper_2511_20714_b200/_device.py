@@ -62,7 +62,7 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
              cur_k: torch.Tensor | None = None, cur_v: torch.Tensor | None = None,
              scale: float | None = None, mask: torch.Tensor | None = None,
              row_max: torch.Tensor | None = None, row_sum: torch.Tensor | None = None,
-             variant: int | None = None, stream=None) -> torch.Tensor:
+             stream=None) -> torch.Tensor:
     """Enqueue K1 (attn_fwd_sm100.cu): out = softmax(q [ctx∥cur]^T * scale) [ctx∥cur].
 
     q/out: [n_q, heads*head_dim] bf16 (row-strided views allowed). ctx_*: slabs whose rows
@@ -84,11 +84,7 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
         p.mask, p.mask_ld = mask.data_ptr(), mask.stride(0)
     if row_max is not None:
         p.row_max, p.row_sum = row_max.data_ptr(), row_sum.data_ptr()
-    L = _abi.lib()
-    if variant is None:
-        rc = L.ifx_attn_fwd(ctypes.byref(p), stream_ptr(stream))
-    else:
-        rc = L.ifx_attn_fwd_variant(ctypes.byref(p), variant, stream_ptr(stream))
+    rc = _abi.lib().ifx_attn_fwd(ctypes.byref(p), stream_ptr(stream))
     _abi.check(rc, "attn_fwd")
     LAUNCHES[0] += 1
     return out

@@ -4,7 +4,6 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
-#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -61,7 +60,7 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols
   return IFX_OK;
 }
 
-int attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream) {
+int attn_fwd(const ifx_attn_params* p, void* stream) {
   if (p->head_dim != 64 && p->head_dim != 128)
     return fail(IFX_EUNSUPPORTED, "head_dim must be 64 or 128");
   if (p->heads < 1 || p->n_q < 0 || p->n_ctx < 0 || p->n_cur < 0)
@@ -96,7 +95,7 @@ int attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream) {
   a.mask_ld = p->mask_ld;
   a.row_max = p->row_max;
   a.row_sum = p->row_sum;
-  int e = attn_fwd_launch(a, (int)p->head_dim, variant, (int)p->n_q, (int)p->heads,
+  int e = attn_fwd_launch(a, (int)p->head_dim, (int)p->n_q, (int)p->heads,
                           static_cast<cudaStream_t>(stream));
   return cuda_fail(e, "attn_fwd launch");
 }
@@ -108,15 +107,7 @@ extern "C" {
 const char* ifx_last_error(void) { return ifx::g_last_error.c_str(); }
 int ifx_version(void) { return 1; }
 
-// default: P kept in TMEM (TS MMA) — measured faster than staging P in smem
-int ifx_attn_fwd(const ifx_attn_params* p, void* stream) {
-  return ifx::attn_fwd_variant(p, 1, stream);
-}
-
-// test hook: 0 = P staged in smem (SS MMA), 1 = P in TMEM (TS MMA)
-int ifx_attn_fwd_variant(const ifx_attn_params* p, int variant, void* stream) {
-  return ifx::attn_fwd_variant(p, variant, stream);
-}
+int ifx_attn_fwd(const ifx_attn_params* p, void* stream) { return ifx::attn_fwd(p, stream); }
 
 int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_type, void* k_slab,
                   void* v_slab, int64_t slab_ld, int slab_type, int64_t dst_row, int64_t t,

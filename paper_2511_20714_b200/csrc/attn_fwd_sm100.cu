@@ -2,18 +2,25 @@
 //
 // Replaces the reference's per-head numpy loop `_mha` -> `scaled_dot_attention`
 // (/root/reference/pkg/src/inferix/engine.py:176-182,206-210, attention.py:74-94) and the
-// context concat it needs. softmax(Q K^T * scale) V with online (flash) softmax; every key
+// context concat it needs: softmax(Q K^T * scale) V with online (flash) softmax; every key
 // is visible (engine.py:209) unless a dense mask is given (API parity, attention.py:89).
 //
-// Blackwell structure (one CTA = one 128-query tile of one head, 1 CTA/SM):
-//   warp 0      TMA producer: Q once, then K_j / V_j tiles (128 keys x head_dim) into a
-//               2-stage smem ring, 128B-swizzled, completion on mbarriers (tx bytes)
-//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into TMEM (double-buffered),
-//               then O += P_{j-1} V_{j-1} into TMEM; tcgen05.commit frees smem / signals
-//   warps 2-5   softmax: thread r owns query row r (TMEM lane r): tcgen05.ld the S row,
-//               row max / exp2 / row sum in fp32, lazy O rescale (only when the running
-//               max grows by > 2^8), P as bf16 -> smem (SW128, K-major) or TMEM, epilogue
-//               O / l -> bf16 -> global.
+// One CTA = one 128-query tile of one head (37 tiles x 12 heads = 444 = 3 x 148 CTAs at
+// the Wan-1.3B shape: exact waves), 320 threads:
+//   warp 0      TMA producer: Q once, then K_j / V_j tiles (128 keys x head_dim, SW128)
+//               into 2-stage smem rings; mbarrier tx completion
+//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into TMEM (double-buffered S),
+//               O += P_{j-1} V_{j-1} with P read from TMEM (TS form); tcgen05.commit frees
+//               smem stages and signals the softmax warps
+//   warps 2-9   softmax, TWO warps per TMEM lane quarter: warp (q4, half) owns query rows
+//               32*q4..+31 and key columns 64*half..+63 of every S tile. The halves swap
+//               partial row maxima through smem (64-thread named barrier), then each does
+//               its 64 exponentials (1 in 4 on the FMA pipe), writes its 32 packed bf16 P
+//               columns into the upper half of the S buffer, rescales its half of O lazily
+//               (only when the running max grows by > 2^8) and stores its half of the output.
+// Why two warps per quarter (profiles/r02_attn_diagnostics.md): a single softmax warp per
+// SM sub-partition serialises TMEM loads (~120 B/clk/SM at 1 warp, ~220 at 2) with the
+// MUFU work (16 ex2/clk/SM); the second warp overlaps one with the other.
 // Keys come from two segments so the block's own K/V never need to be copied next to the
 // cache: segment 0 = slab rows [ctx_row0, ctx_row0 + n_ctx), segment 1 = rows [0, n_cur)
 // of the fresh QKV projection. Ragged tails are masked in softmax (TMA zero-fills rows past
@@ -34,10 +41,13 @@ using namespace ptx;
 
 constexpr int BM = 128;          // query rows per CTA (= TMEM lanes)
 constexpr int BN = 128;          // keys per tile
+constexpr int HALF = BN / 2;     // key columns per softmax warp
 constexpr int NS = 2;            // smem stages for K and for V
-constexpr int NTHREADS = 192;    // 6 warps
+constexpr int NB = 3;            // S buffers in TMEM (P_b aliases S_b): QK(j) never waits on PV(j-1)
+constexpr int NTHREADS = 320;    // 10 warps
+constexpr int NSOFT = 256;       // softmax threads
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if max grows > 2^8
-constexpr int kPolyEvery = 4;              // every 4th exp2 of a full tile runs on the FMA pipe
+constexpr int kPolyEvery = 4;              // every 4th exp2 of a full tile on the FMA pipe
 
 // 2^x on the FMA/ALU pipes (round-to-nearest split, cubic on [-0.5, 0.5], exponent add):
 // rel. error < 5e-4, far below bf16 P rounding. x is clamped to >= -125 (result ~0).
@@ -50,29 +60,46 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-template <int HD, bool kPInTmem>
+// the same on a pair with packed fp32x2 ops (FADD2 / FFMA2)
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 p = __ffma2_rn(make_float2(0.0555041087f, 0.0555041087f), f,
+                        make_float2(0.2402265070f, 0.2402265070f));
+  p = __ffma2_rn(p, f, make_float2(0.6931471806f, 0.6931471806f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <int HD>
 struct Layout {
-  static constexpr int KCH = HD / 64;                 // 64-column (128 B) chunks of head_dim
+  static constexpr int KCH = HD / 64;
   static constexpr int Q_BYTES = BM * HD * 2;
   static constexpr int KV_BYTES = BN * HD * 2;
-  static constexpr int P_BYTES = kPInTmem ? 0 : BM * BN * 2;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
-  static constexpr int OFF_P = OFF_V + NS * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-  static constexpr int NBAR = 1 + 4 * NS + 2 * 4;
-  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + align slack
-  // TMEM columns: S0 [0,128) S1 [128,256) O [256, 256+HD); P (TS mode) aliases S[b] cols [64,128)
-  static constexpr uint32_t TM_O = 256;
-  static constexpr uint32_t TM_P_OFF = 64;
+  static constexpr int OFF_RED = OFF_V + NS * KV_BYTES;  // float [2 tiles][2 halves][BM]
+  static constexpr int OFF_BAR = OFF_RED + 2 * 2 * BM * 4;
+  static constexpr int NBAR = 1 + 4 * NS + 4 * NB;
+  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
+  // TMEM columns: S0 [0,128) S1 [128,256) S2 [256,384) O [384, 384+HD);
+  // P_b = packed bf16 in S_b [64,128)
+  static constexpr uint32_t TM_O = 128 * NB;
+  static constexpr uint32_t TM_P = 64;
 };
 
 struct Tile {
-  int seg;    // 0 ctx, 1 cur
-  int row;    // first row inside the segment's tensor
-  int kv0;    // logical key index of column 0
-  int valid;  // valid keys in this tile
+  int seg, row, kv0, valid;
 };
 
 __device__ __forceinline__ Tile tile_of(const AttnKernelArgs& a, int j, int n0) {
@@ -91,17 +118,17 @@ __device__ __forceinline__ Tile tile_of(const AttnKernelArgs& a, int j, int n0) 
   return t;
 }
 
-template <int HD, bool kPInTmem>
+template <int HD>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ AttnKernelArgs a) {
-  using L = Layout<HD, kPInTmem>;
+  using L = Layout<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sK = smem + L::OFF_K;
   uint8_t* sV = smem + L::OFF_V;
-  uint8_t* sP = smem + L::OFF_P;
+  float* red = reinterpret_cast<float*>(smem + L::OFF_RED);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
@@ -109,9 +136,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* v_full = k_empty + NS;
   uint64_t* v_empty = v_full + NS;
   uint64_t* s_full = v_empty + NS;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* pv_done = p_full + 2;
+  uint64_t* s_empty = s_full + NB;
+  uint64_t* p_full = s_empty + NB;
+  uint64_t* pv_done = p_full + NB;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NBAR);
 
   const int warp = warp_id();
@@ -129,10 +156,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(v_full + s, 1);
       mbar_init(v_empty + s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(s_full + b, 1);
-      mbar_init(s_empty + b, 128);
-      mbar_init(p_full + b, 128);
+      mbar_init(s_empty + b, NSOFT);
+      mbar_init(p_full + b, NSOFT);
       mbar_init(pv_done + b, 1);
     }
     fence_barrier_init();
@@ -181,17 +208,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ===================== MMA issuer =====================
     if (elect_one()) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);  // Q, K both K-major
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, HD, 0, 1);  // P K-major, V MN-major
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, HD, 0, 1);  // P (TMEM), V MN-major
       mbar_wait(q_full, 0);
       tc_fence_after();
       const uint32_t q_base = smem_u32(sQ);
       for (int j = 0; j <= n_tiles; ++j) {
         if (j < n_tiles) {
           const int s = j % NS;
-          const int b = j & 1;
+          const int b = j % NB;
+          const uint32_t bph = (j / NB) & 1;
           mbar_wait(k_full + s, (j / NS) & 1);
-          mbar_wait(s_empty + b, ((j >> 1) & 1) ^ 1);
-          if (kPInTmem && j >= 2) mbar_wait(pv_done + b, ((j >> 1) & 1) ^ 1);  // P_{j-2} read
+          mbar_wait(s_empty + b, bph ^ 1);                    // S_b of tile j-NB read
+          if (j >= NB) mbar_wait(pv_done + b, bph ^ 1);       // P_b (aliases S_b) consumed
           tc_fence_after();
           const uint32_t k_base = smem_u32(sK + s * L::KV_BYTES);
 #pragma unroll
@@ -207,8 +235,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (j >= 1) {
           const int jp = j - 1;
           const int s = jp % NS;
-          const int b = jp & 1;
-          mbar_wait(p_full + b, (jp >> 1) & 1);
+          const int b = jp % NB;
+          mbar_wait(p_full + b, (jp / NB) & 1);
           mbar_wait(v_full + s, (jp / NS) & 1);
           tc_fence_after();
           const uint32_t v_base = smem_u32(sV + s * L::KV_BYTES);
@@ -217,15 +245,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // V tile: KCH chunks [BN keys x 64 dims], rows of 128 B; MN-major B operand:
             // LBO = stride between 64-dim chunks, SBO = 8 key rows; K step = 16 rows.
             const uint64_t bdesc = smem_desc_sw128(v_base + kk * 16 * 128, BN * 128, 1024);
-            if constexpr (kPInTmem) {
-              mma_bf16_ts(tmem + L::TM_O, tmem + b * 128 + L::TM_P_OFF + kk * 8, bdesc, idesc_pv,
-                          (jp > 0 || kk > 0));
-            } else {
-              const uint32_t p_base = smem_u32(sP + b * L::P_BYTES);
-              const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-              mma_bf16_ss(tmem + L::TM_O, smem_desc_sw128(p_base + off, 16, 1024), bdesc,
-                          idesc_pv, (jp > 0 || kk > 0));
-            }
+            mma_bf16_ts(tmem + L::TM_O, tmem + b * 128 + L::TM_P + kk * 8, bdesc, idesc_pv,
+                        (jp > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(v_empty + s);
           mma_commit(pv_done + b);
@@ -234,28 +255,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncwarp();
   } else {
-    // ===================== softmax / correction / epilogue =====================
-    const int q4 = warp & 3;            // TMEM lane quarter this warp may access
-    const int row = q4 * 32 + lane;     // query row within the tile
+    // ===================== softmax (2 warps per TMEM lane quarter) =====================
+    const int q4 = warp & 3;                  // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;         // key-column half of every S tile
+    const int row = q4 * 32 + lane;           // query row within the tile
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const int grow = q0 + row;
     const float sl2 = a.scale_log2;
-    float m_run = -INFINITY;  // running max, log2-scaled units
-    float l_run = 0.f;
-    float m_exact = -INFINITY;  // true running max (only for the partial-stats output)
-    bool o_live = false;      // some PV has accumulated into O
+    const int pair_bar = 1 + q4;              // named barrier of the two warps of quarter q4
+    float m_run = -INFINITY;                  // running max used for exponents (log2 units)
+    float l_half = 0.f;                       // denominator over this warp's columns
+    float m_exact = -INFINITY;                // true running max (partial-stats output)
     const uint8_t* mrow = (a.mask != nullptr && grow < a.n_q) ? a.mask + (int64_t)grow * a.mask_ld
                                                               : nullptr;
     for (int j = 0; j < n_tiles; ++j) {
-      const int b = j & 1;
+      const int b = j % NB;
       const Tile t = tile_of(a, j, n0);
-      mbar_wait(s_full + b, (j >> 1) & 1);
+      const int c0 = half * HALF;  // first key column of this warp
+      mbar_wait(s_full + b, (j / NB) & 1);
       tc_fence_after();
-      float sv[BN];
+      float sv[HALF];
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < HALF / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tmem + lane_off + b * 128 + c * 32, r);
+        tmem_ld32(tmem + lane_off + b * 128 + c0 + c * 32, r);
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
       }
@@ -263,116 +286,118 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_before();
       mbar_arrive(s_empty + b);
 
-      // visibility: ragged tile tail, optional dense mask
-      if (t.valid < BN || mrow != nullptr) {
+      const bool full = (t.valid == BN) && mrow == nullptr;
+      if (!full) {
 #pragma unroll
-        for (int i = 0; i < BN; ++i) {
-          bool ok = i < t.valid;
-          if (ok && mrow != nullptr) ok = mrow[t.kv0 + i] != 0;
+        for (int i = 0; i < HALF; ++i) {
+          bool ok = c0 + i < t.valid;
+          if (ok && mrow != nullptr) ok = mrow[t.kv0 + c0 + i] != 0;
           if (!ok) sv[i] = -INFINITY;
         }
       }
-      // 8 independent chains: one softmax warp per SM sub-partition has no other warp to
-      // hide FMNMX/FADD latency behind, so the reductions must carry their own ILP
-      float m8[8];
+      float m4[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) m8[i] = sv[i];
+      for (int i = 0; i < 4; ++i) m4[i] = sv[i];
 #pragma unroll
-      for (int i = 8; i < BN; ++i) m8[i & 7] = fmaxf(m8[i & 7], sv[i]);
-      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      for (int i = 4; i < HALF; ++i) m4[i & 3] = fmaxf(m4[i & 3], sv[i]);
+      const float pm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      // swap partial maxima with the other half (also orders both halves' S loads before
+      // either writes P into the S buffer's upper columns)
+      float* rb = red + ((j & 1) * 2) * BM;
+      rb[half * BM + row] = pm;
+      named_sync(pair_bar, 64);
+      const float mx = fmaxf(pm, rb[(half ^ 1) * BM + row]);
       const float m_tile = mx * sl2;  // -inf if nothing visible
       m_exact = fmaxf(m_exact, m_tile);
       float alpha = 1.f;
       bool rescale_o = false;
-      if (m_tile > m_run + kRescaleThreshold || (m_run == -INFINITY && m_tile > -INFINITY)) {
+      if (m_tile > m_run + kRescaleThreshold) {
         alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_tile);
-        rescale_o = o_live && m_run != -INFINITY;
+        rescale_o = j > 0 && m_run != -INFINITY;
         m_run = m_tile;
       }
       const float m_sub = (m_run == -INFINITY) ? 0.f : m_run;
-      float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (t.valid == BN && mrow == nullptr) {
-        // full unmasked tile: 1 in kPolyEvery exponentials on the FMA pipe (MUFU offload)
+      // packed fp32x2 arithmetic (FFMA2 / FADD2) halves the FMA-pipe instruction count;
+      // MUFU.EX2 stays scalar (the bf16x2/f16x2 forms issue two MUFU ops on sm_100)
+      const float2 sl2v = make_float2(sl2, sl2);
+      const float2 negm = make_float2(-m_sub, -m_sub);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                       make_float2(0.f, 0.f)};
+      if (full) {
 #pragma unroll
-        for (int i = 0; i < BN; ++i) {
-          const float x = fmaf(sv[i], sl2, -m_sub);
-          const float p = (i % kPolyEvery == kPolyEvery - 1) ? ex2_poly(x) : ex2(x);
-          sv[i] = p;
-          s8[i & 7] += p;
+        for (int i = 0; i < HALF / 2; ++i) {
+          const float2 x = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), sl2v, negm);
+          float2 p;
+          if ((i & 3) == 3) {
+            p = ex2_poly2(x);  // 1 pair in 4 = 25% of the exponentials on the FMA pipe
+          } else {
+            p.x = ex2(x.x);
+            p.y = ex2(x.y);
+          }
+          sv[2 * i] = p.x;
+          sv[2 * i + 1] = p.y;
+          acc[i & 3] = __fadd2_rn(acc[i & 3], p);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < BN; ++i) {
-          const float p = ex2(fmaf(sv[i], sl2, -m_sub));  // exp2(-inf) = 0 for masked keys
-          sv[i] = p;
-          s8[i & 7] += p;
+        for (int i = 0; i < HALF / 2; ++i) {
+          const float2 x = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), sl2v, negm);
+          const float2 p = make_float2(ex2(x.x), ex2(x.y));  // exp2(-inf) = 0 for masked keys
+          sv[2 * i] = p.x;
+          sv[2 * i + 1] = p.y;
+          acc[i & 3] = __fadd2_rn(acc[i & 3], p);
         }
       }
-      const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
-      l_run = l_run * alpha + sum;
+      const float2 a01 = __fadd2_rn(acc[0], acc[1]), a23 = __fadd2_rn(acc[2], acc[3]);
+      const float2 a4 = __fadd2_rn(a01, a23);
+      l_half = l_half * alpha + (a4.x + a4.y);
 
       // tcgen05.ld/st are warp-collective: rescale if any row of this warp needs it
-      if (__any_sync(0xffffffffu, rescale_o)) {  // O *= alpha once PV_{j-1} has landed
+      if (__any_sync(0xffffffffu, rescale_o)) {  // O[:, my half] *= alpha once PV_{j-1} landed
         const float f = rescale_o ? alpha : 1.f;
         const int jp = j - 1;
-        mbar_wait(pv_done + (jp & 1), (jp >> 1) & 1);
+        mbar_wait(pv_done + (jp % NB), (jp / NB) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = 0; c < HD / 64; ++c) {
           uint32_t r[32];
-          tmem_ld32(tmem + lane_off + L::TM_O + c * 32, r);
+          const uint32_t ta = tmem + lane_off + L::TM_O + half * (HD / 2) + c * 32;
+          tmem_ld32(ta, r);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-          tmem_st32(tmem + lane_off + L::TM_O + c * 32, r);
+          tmem_st32(ta, r);
         }
-        tmem_wait_st();
       }
-
-      if constexpr (kPInTmem) {
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[16];
+      for (int c = 0; c < HALF / 32; ++c) {
+        uint32_t r[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) r[i] = pack_bf16(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]);
-          tmem_st16(tmem + lane_off + b * 128 + L::TM_P_OFF + c * 16, r);
-        }
-        tmem_wait_st();
-      } else {
-        // P[b] was last read by PV_{j-2}
-        mbar_wait(pv_done + b, ((j >> 1) & 1) ^ 1);
-        uint8_t* pb = sP + b * L::P_BYTES;
-#pragma unroll
-        for (int c16 = 0; c16 < BN / 8; ++c16) {
-          uint4 v;
-          v.x = pack_bf16(sv[c16 * 8 + 0], sv[c16 * 8 + 1]);
-          v.y = pack_bf16(sv[c16 * 8 + 2], sv[c16 * 8 + 3]);
-          v.z = pack_bf16(sv[c16 * 8 + 4], sv[c16 * 8 + 5]);
-          v.w = pack_bf16(sv[c16 * 8 + 6], sv[c16 * 8 + 7]);
-          const int chunk = c16 & 7;
-          uint8_t* dst = pb + (c16 >> 3) * (BM * 128) + row * 128 + ((chunk ^ (row & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = v;
-        }
-        fence_proxy_async_smem();
+        for (int i = 0; i < 16; ++i) r[i] = pack_bf16(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]);
+        tmem_st16(tmem + lane_off + b * 128 + L::TM_P + half * (HALF / 2) + c * 16, r);
       }
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_full + b);
-      o_live = true;
     }
 
-    // ---------------- epilogue: O / l -> bf16 -> global ----------------
+    // ---------------- epilogue: O / l -> bf16 -> global (this warp's half of O) --------
     if (n_tiles > 0) {
       const int jl = n_tiles - 1;
-      mbar_wait(pv_done + (jl & 1), (jl >> 1) & 1);
+      mbar_wait(pv_done + (jl % NB), (jl / NB) & 1);
       tc_fence_after();
     }
+    float* rl = red + 4 * BM * 0;  // reuse tile-buffer 0 for the denominator swap
+    named_sync(pair_bar, 64);      // both halves done reading red[] of the last tile
+    rl[half * BM + row] = l_half;
+    named_sync(pair_bar, 64);
+    const float l_run = l_half + rl[(half ^ 1) * BM + row];
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    __nv_bfloat16* orow = a.o + (int64_t)grow * a.o_ld + head * HD;
+    __nv_bfloat16* orow = a.o + (int64_t)grow * a.o_ld + head * HD + half * (HD / 2);
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = 0; c < HD / 64; ++c) {
       uint32_t r[32];
-      tmem_ld32(tmem + lane_off + L::TM_O + c * 32, r);
+      tmem_ld32(tmem + lane_off + L::TM_O + half * (HD / 2) + c * 32, r);
       tmem_wait_ld();
       if (grow < a.n_q) {
 #pragma unroll
@@ -386,7 +411,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     }
-    if (a.row_max != nullptr && grow < a.n_q) {
+    if (a.row_max != nullptr && grow < a.n_q && half == 0) {
       // re-reference the denominator to the exact max (attention.py:140-154 convention)
       const bool live = m_exact > -INFINITY;
       a.row_max[(int64_t)head * a.n_q + grow] = m_exact;
@@ -402,11 +427,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-template <int HD, bool kPInTmem>
+template <int HD>
 int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
-  using L = Layout<HD, kPInTmem>;
-  auto* fn = attn_fwd_kernel<HD, kPInTmem>;
-  static bool attr_set = false;  // per instantiation
+  using L = Layout<HD>;
+  auto* fn = attn_fwd_kernel<HD>;
+  static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
     if (e != cudaSuccess) return (int)e;
@@ -419,11 +444,9 @@ int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
 
 }  // namespace
 
-int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int variant, int n_q, int heads,
-                    cudaStream_t st) {
-  const bool p_tmem = variant == 1;
-  if (head_dim == 128) return p_tmem ? launch<128, true>(a, n_q, heads, st) : launch<128, false>(a, n_q, heads, st);
-  if (head_dim == 64) return p_tmem ? launch<64, true>(a, n_q, heads, st) : launch<64, false>(a, n_q, heads, st);
+int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int n_q, int heads, cudaStream_t st) {
+  if (head_dim == 128) return launch<128>(a, n_q, heads, st);
+  if (head_dim == 64) return launch<64>(a, n_q, heads, st);
   return -1;
 }
 

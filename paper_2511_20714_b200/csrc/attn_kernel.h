@@ -25,8 +25,7 @@ struct AttnKernelArgs {
   float* row_sum;
 };
 
-// variant 0: P staged in smem (SS MMA); 1: P kept in TMEM (TS MMA). Returns cudaError_t.
-int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int variant, int n_q, int heads,
-                    cudaStream_t st);
+// Grid (ceil(n_q/128), heads) x 320 threads. Returns cudaError_t.
+int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int n_q, int heads, cudaStream_t st);
 
 }  // namespace ifx

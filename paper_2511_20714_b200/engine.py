@@ -257,12 +257,18 @@ class _Workspace:
         self.attn = torch.empty(T, Dp, device=dev, dtype=torch.bfloat16)
         self.ffn = torch.empty(T, 2 * D, device=dev, dtype=torch.bfloat16)
         self.tmp = torch.empty(T, D, device=dev, dtype=torch.float32)
+        self.zero_bias = torch.zeros(2 * D, device=dev, dtype=torch.bfloat16)
 
 
-def _residual(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor, tmp: torch.Tensor):
-    """x += a @ w with bf16 operands and fp32 output/accumulation (cuBLAS)."""
-    torch.mm(a, w, out_dtype=torch.float32, out=tmp)
-    x.add_(tmp)
+def _residual(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor, tmp: torch.Tensor = None):
+    """x += a @ w with bf16 operands, fp32 accumulation and fp32 in-place epilogue (one
+    cuBLASLt call with beta = 1; 24 us vs 33 us for mm + add at the c2 shape)."""
+    torch.addmm(x, a, w, out_dtype=torch.float32, out=x)
+
+
+def _ffn_up(h: torch.Tensor, w1: torch.Tensor, zero_bias: torch.Tensor, out: torch.Tensor):
+    """relu(h @ w1) with the ReLU in the cuBLASLt epilogue (engine.py:216)."""
+    torch._addmm_activation(zero_bias, h, w1, use_gelu=False, out=out)
 
 
 class BlockRunner:
@@ -315,8 +321,7 @@ class BlockRunner:
                 attn_fwd(ws.q2, H, dhp, ws.attn, xk, xv, row0, n, scale=sc)
                 _residual(ws.x, ws.attn, lw.co, ws.tmp)
             rms_bf16(ws.x, ws.h)
-            torch.mm(ws.h, lw.w1, out=ws.ffn)
-            ws.ffn.relu_()
+            _ffn_up(ws.h, lw.w1, ws.zero_bias, ws.ffn)
             _residual(ws.x, ws.ffn, lw.w2, ws.tmp)
             if collect_kv:  # clean pass: page write of this layer's K/V (engine.py:303-306)
                 cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)

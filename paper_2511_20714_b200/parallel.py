@@ -299,8 +299,8 @@ class UlyssesRunner:
         self.attn_s = torch.empty(n, Dp, device=dev, dtype=torch.bfloat16)
         self.q2 = torch.empty(n, Dp, device=dev, dtype=torch.bfloat16)
         self.ffn = torch.empty(n, 2 * D, device=dev, dtype=torch.bfloat16)
-        self.tmp = torch.empty(n, D, device=dev)
         self.eps = torch.empty(n, D, device=dev)
+        self.zero_bias = torch.zeros(2 * D, device=dev, dtype=torch.bfloat16)
         self.attn_events = None
 
     def _rms(self, x, out, tvec=None, t=0.0, x_out=None):
@@ -308,6 +308,7 @@ class UlyssesRunner:
         return rms_bf16(x, out, tvec, t, x_out)
 
     def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None):
+        from .engine import _ffn_up, _residual
         from .kvcache import SELF_ATTN
         m = self.model
         c = m.config
@@ -336,20 +337,16 @@ class UlyssesRunner:
                 e1.record()
                 ev.append((e0, e1))
             self.comm.head_to_seq(self.attn_h, self.attn_s)      # [n, Dp]
-            torch.mm(self.attn_s, lw.wo, out_dtype=torch.float32, out=self.tmp)
-            self.x.add_(self.tmp)
+            _residual(self.x, self.attn_s, lw.wo)
             if cross is not None:  # sequence-sharded vs replicated prompt K/V: no comm
                 xk, xv, row0, nx = cross[li]
                 self._rms(self.x, self.h)
                 torch.mm(self.h, lw.cq, out=self.q2)
                 self._attn(self.q2, m.heads_pad, dhp, self.attn_s, xk, xv, row0, nx, scale=sc)
-                torch.mm(self.attn_s, lw.co, out_dtype=torch.float32, out=self.tmp)
-                self.x.add_(self.tmp)
+                _residual(self.x, self.attn_s, lw.co)
             self._rms(self.x, self.h)
-            torch.mm(self.h, lw.w1, out=self.ffn)
-            self.ffn.relu_()
-            torch.mm(self.ffn, lw.w2, out_dtype=torch.float32, out=self.tmp)
-            self.x.add_(self.tmp)
+            _ffn_up(self.h, lw.w1, self.zero_bias, self.ffn)
+            _residual(self.x, self.ffn, lw.w2)
             if collect_kv:  # rank-local page write of this rank's heads
                 cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
         if eps_out is not None:

@@ -1,6 +1,6 @@
 """Quick K1 timing at the Wan-1.3B shape (T=4680, H=12, dh=128) for b cached blocks.
 
-    python tools/attn_probe.py [--variant 0|1]
+    python tools/attn_probe.py [--quick]
 
 Prints algorithmic TFLOP/s = 4*T*(C+T)*D / kernel time (CUDA events, warm, inputs > L2).
 """
@@ -15,20 +15,19 @@ from paper_2511_20714_b200._device import attn_fwd
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
     T, H, dh = 4680, 12, 128
     D = H * dh
     res = []
-    for b in (0, 1, 3, 6, 20):
+    for b in ((0, 1, 3, 6, 20) if not args.quick else (3,)):
         C = b * T
         qkv = torch.randn(T, 3 * D, device="cuda").bfloat16()
         ks = torch.randn(max(C, 1), D, device="cuda").bfloat16()
         vs = torch.randn(max(C, 1), D, device="cuda").bfloat16()
         out = torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
-        f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:],
-                             variant=args.variant)
+        f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:])
         for _ in range(3):
             f()
         torch.cuda.synchronize()
