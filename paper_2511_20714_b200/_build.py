@@ -18,7 +18,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["attn_fwd_sm100.cu", "kv_ops.cu", "abi.cpp", "pagetable.cpp"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", *os.environ.get("IFX_NVCC_EXTRA", "").split(), "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-I", os.path.join(ROOT, "include")]
 
 

@@ -43,7 +43,7 @@ constexpr int BM = 128;          // query rows per CTA (= TMEM lanes)
 constexpr int BN = 128;          // keys per tile
 constexpr int HALF = BN / 2;     // key columns per softmax warp
 constexpr int NS = 2;            // smem stages for K and for V
-constexpr int NB = 3;            // S buffers in TMEM (P_b aliases S_b): QK(j) never waits on PV(j-1)
+constexpr int NB = 2;            // S buffers in TMEM (P aliases S)
 constexpr int NTHREADS = 320;    // 10 warps
 constexpr int NSOFT = 256;       // softmax threads
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if max grows > 2^8
@@ -88,14 +88,15 @@ struct Layout {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
-  static constexpr int OFF_RED = OFF_V + NS * KV_BYTES;  // float [2 tiles][2 halves][BM]
-  static constexpr int OFF_BAR = OFF_RED + 2 * 2 * BM * 4;
-  static constexpr int NBAR = 1 + 4 * NS + 4 * NB;
+  static constexpr int OFF_RED = OFF_V + NS * KV_BYTES;  // float [2 halves][3][BM] merge swap
+  static constexpr int OFF_BAR = OFF_RED + 2 * 3 * BM * 4;
+  static constexpr int NBAR = 1 + 4 * NS + 5 * NB;  // ... s_full s_empty p_full[2] pv_done
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
-  // TMEM columns: S0 [0,128) S1 [128,256) S2 [256,384) O [384, 384+HD);
-  // P_b = packed bf16 in S_b [64,128)
-  static constexpr uint32_t TM_O = 128 * NB;
-  static constexpr uint32_t TM_P = 64;
+  // TMEM columns: S0 [0,128) S1 [128,256) O_lo [256, 256+HD) O_hi [384, 384+HD).
+  // Key half h of S_b (columns 64h..64h+63) is overwritten in place by its packed bf16 P
+  // (32 columns at 64h): each softmax warp only ever writes the S columns it read.
+  __host__ __device__ static constexpr uint32_t TM_O(int h) { return 256 + 128 * h; }
+  __host__ __device__ static constexpr uint32_t TM_P(int h) { return 64 * h; }
 };
 
 struct Tile {
@@ -137,8 +138,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* v_empty = v_full + NS;
   uint64_t* s_full = v_empty + NS;
   uint64_t* s_empty = s_full + NB;
-  uint64_t* p_full = s_empty + NB;
-  uint64_t* pv_done = p_full + NB;
+  uint64_t* p_full = s_empty + NB;   // [NB][2 key halves]
+  uint64_t* pv_done = p_full + 2 * NB;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NBAR);
 
   const int warp = warp_id();
@@ -159,7 +160,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int b = 0; b < NB; ++b) {
       mbar_init(s_full + b, 1);
       mbar_init(s_empty + b, NSOFT);
-      mbar_init(p_full + b, NSOFT);
+      mbar_init(p_full + 2 * b, NSOFT / 2);
+      mbar_init(p_full + 2 * b + 1, NSOFT / 2);
       mbar_init(pv_done + b, 1);
     }
     fence_barrier_init();
@@ -219,7 +221,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t bph = (j / NB) & 1;
           mbar_wait(k_full + s, (j / NS) & 1);
           mbar_wait(s_empty + b, bph ^ 1);                    // S_b of tile j-NB read
-          if (j >= NB) mbar_wait(pv_done + b, bph ^ 1);       // P_b (aliases S_b) consumed
+          // P_b aliases S_b: explicit wait (measured free: the in-order-only variant was no faster)
+          if (j >= NB) mbar_wait(pv_done + b, bph ^ 1);
           tc_fence_after();
           const uint32_t k_base = smem_u32(sK + s * L::KV_BYTES);
 #pragma unroll
@@ -236,17 +239,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int jp = j - 1;
           const int s = jp % NS;
           const int b = jp % NB;
-          mbar_wait(p_full + b, (jp / NB) & 1);
           mbar_wait(v_full + s, (jp / NS) & 1);
-          tc_fence_after();
           const uint32_t v_base = smem_u32(sV + s * L::KV_BYTES);
+          // O_h += P_h V[64h .. 64h+63]: each key half has its own running max, so its own
+          // accumulator; issued as soon as that half's softmax warps published P_h
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            // V tile: KCH chunks [BN keys x 64 dims], rows of 128 B; MN-major B operand:
-            // LBO = stride between 64-dim chunks, SBO = 8 key rows; K step = 16 rows.
-            const uint64_t bdesc = smem_desc_sw128(v_base + kk * 16 * 128, BN * 128, 1024);
-            mma_bf16_ts(tmem + L::TM_O, tmem + b * 128 + L::TM_P + kk * 8, bdesc, idesc_pv,
-                        (jp > 0 || kk > 0) ? 1u : 0u);
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait(p_full + 2 * b + h, (jp / NB) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < HALF / 16; ++kk) {
+              // V tile: KCH chunks [BN keys x 64 dims], rows of 128 B; MN-major B operand:
+              // LBO = stride between 64-dim chunks, SBO = 8 key rows; K step = 16 rows.
+              const uint64_t bdesc =
+                  smem_desc_sw128(v_base + (h * (HALF / 16) + kk) * 16 * 128, BN * 128, 1024);
+              mma_bf16_ts(tmem + L::TM_O(h), tmem + b * 128 + L::TM_P(h) + kk * 8, bdesc,
+                          idesc_pv, (jp > 0 || kk > 0) ? 1u : 0u);
+            }
           }
           mma_commit(v_empty + s);
           mma_commit(pv_done + b);
@@ -300,13 +309,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int i = 0; i < 4; ++i) m4[i] = sv[i];
 #pragma unroll
       for (int i = 4; i < HALF; ++i) m4[i & 3] = fmaxf(m4[i & 3], sv[i]);
-      const float pm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-      // swap partial maxima with the other half (also orders both halves' S loads before
-      // either writes P into the S buffer's upper columns)
-      float* rb = red + ((j & 1) * 2) * BM;
-      rb[half * BM + row] = pm;
-      named_sync(pair_bar, 64);
-      const float mx = fmaxf(pm, rb[(half ^ 1) * BM + row]);
+      // this key half's own online softmax: no per-tile exchange with the other half
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       const float m_tile = mx * sl2;  // -inf if nothing visible
       m_exact = fmaxf(m_exact, m_tile);
       float alpha = 1.f;
@@ -353,15 +357,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       l_half = l_half * alpha + (a4.x + a4.y);
 
       // tcgen05.ld/st are warp-collective: rescale if any row of this warp needs it
-      if (__any_sync(0xffffffffu, rescale_o)) {  // O[:, my half] *= alpha once PV_{j-1} landed
+      if (__any_sync(0xffffffffu, rescale_o)) {  // O_half *= alpha once PV_{j-1} landed
         const float f = rescale_o ? alpha : 1.f;
         const int jp = j - 1;
         mbar_wait(pv_done + (jp % NB), (jp / NB) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c) {
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
           uint32_t r[32];
-          const uint32_t ta = tmem + lane_off + L::TM_O + half * (HD / 2) + c * 32;
+          const uint32_t ta = tmem + lane_off + L::TM_O(half) + c * 32;
           tmem_ld32(ta, r);
           tmem_wait_ld();
 #pragma unroll
@@ -374,11 +378,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t r[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) r[i] = pack_bf16(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]);
-        tmem_st16(tmem + lane_off + b * 128 + L::TM_P + half * (HALF / 2) + c * 16, r);
+        tmem_st16(tmem + lane_off + b * 128 + L::TM_P(half) + c * 16, r);
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full + b);
+      mbar_arrive(p_full + 2 * b + half);
     }
 
     // ---------------- epilogue: O / l -> bf16 -> global (this warp's half of O) --------
@@ -387,35 +391,57 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(pv_done + (jl % NB), (jl / NB) & 1);
       tc_fence_after();
     }
-    float* rl = red + 4 * BM * 0;  // reuse tile-buffer 0 for the denominator swap
-    named_sync(pair_bar, 64);      // both halves done reading red[] of the last tile
-    rl[half * BM + row] = l_half;
+    // merge the two key halves' partials (attention.py:157-180): swap (max, denominator,
+    // exact max) with the partner warp, then each warp stores half of the head dims
+    float* me = red + half * 3 * BM;
+    me[row] = m_run;
+    me[BM + row] = l_half;
+    me[2 * BM + row] = m_exact;
     named_sync(pair_bar, 64);
-    const float l_run = l_half + rl[(half ^ 1) * BM + row];
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    const float* ot = red + (half ^ 1) * 3 * BM;
+    const float m_o = ot[row], l_o = ot[BM + row], mx_o = ot[2 * BM + row];
+    const float M = fmaxf(m_run, m_o);
+    const float w_me = (m_run == -INFINITY) ? 0.f : ex2(m_run - M);
+    const float w_ot = (m_o == -INFINITY) ? 0.f : ex2(m_o - M);
+    const float den = l_half * w_me + l_o * w_ot;
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    const float w_lo = (half == 0 ? w_me : w_ot) * inv;  // weight of O_lo
+    const float w_hi = (half == 0 ? w_ot : w_me) * inv;  // weight of O_hi
     __nv_bfloat16* orow = a.o + (int64_t)grow * a.o_ld + head * HD + half * (HD / 2);
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < HD / 64; ++c) {
-      uint32_t r[32];
-      tmem_ld32(tmem + lane_off + L::TM_O + half * (HD / 2) + c * 32, r);
+      uint32_t r0[32], r1[32];
+      const uint32_t col = half * (HD / 2) + c * 32;
+      tmem_ld32(tmem + lane_off + L::TM_O(0) + col, r0);
+      tmem_ld32(tmem + lane_off + L::TM_O(1) + col, r1);
       tmem_wait_ld();
       if (grow < a.n_q) {
 #pragma unroll
         for (int v4 = 0; v4 < 4; ++v4) {
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int i = v4 * 8 + e;
+            // a half that saw no key has weight 0 and an undefined accumulator
+            const float x0 = w_lo != 0.f ? __uint_as_float(r0[i]) * w_lo : 0.f;
+            const float x1 = w_hi != 0.f ? __uint_as_float(r1[i]) * w_hi : 0.f;
+            o[e] = x0 + x1;
+          }
           uint4 w;
-          w.x = pack_bf16(__uint_as_float(r[v4 * 8 + 0]) * inv, __uint_as_float(r[v4 * 8 + 1]) * inv);
-          w.y = pack_bf16(__uint_as_float(r[v4 * 8 + 2]) * inv, __uint_as_float(r[v4 * 8 + 3]) * inv);
-          w.z = pack_bf16(__uint_as_float(r[v4 * 8 + 4]) * inv, __uint_as_float(r[v4 * 8 + 5]) * inv);
-          w.w = pack_bf16(__uint_as_float(r[v4 * 8 + 6]) * inv, __uint_as_float(r[v4 * 8 + 7]) * inv);
+          w.x = pack_bf16(o[0], o[1]);
+          w.y = pack_bf16(o[2], o[3]);
+          w.z = pack_bf16(o[4], o[5]);
+          w.w = pack_bf16(o[6], o[7]);
           *reinterpret_cast<uint4*>(orow + c * 32 + v4 * 8) = w;
         }
       }
     }
     if (a.row_max != nullptr && grow < a.n_q && half == 0) {
-      // re-reference the denominator to the exact max (attention.py:140-154 convention)
-      const bool live = m_exact > -INFINITY;
-      a.row_max[(int64_t)head * a.n_q + grow] = m_exact;
-      a.row_sum[(int64_t)head * a.n_q + grow] = live ? l_run * ex2(m_run - m_exact) : 0.f;
+      // exact max over both halves, denominator re-referenced to it (attention.py:140-154)
+      const float mx = fmaxf(m_exact, mx_o);
+      const bool live = mx > -INFINITY;
+      a.row_max[(int64_t)head * a.n_q + grow] = mx;
+      a.row_sum[(int64_t)head * a.n_q + grow] = live ? den * ex2(M - mx) : 0.f;
     }
   }
 

@@ -240,6 +240,15 @@ def _init_noise(cfg: ModelConfig, seed: int, chunk_index: int) -> np.ndarray:
     return rng.standard_normal((cfg.block_len, cfg.model_dim)).astype(np.float32)
 
 
+def _init_noise_pinned(cfg: ModelConfig, seed: int, chunk_index: int) -> torch.Tensor:
+    """_init_noise into pinned host memory (async H2D). Same float64 draw + fp32 cast as
+    engine.py:280-282, so the values are bit-identical."""
+    out = torch.empty((cfg.block_len, cfg.model_dim), dtype=torch.float32, pin_memory=True)
+    rng = np.random.default_rng([seed, chunk_index])
+    np.copyto(out.numpy(), rng.standard_normal((cfg.block_len, cfg.model_dim)), casting="same_kind")
+    return out
+
+
 def _cross_kv(model: ToyModel, prompt_emb: np.ndarray):
     """engine.py:224-225 on device (fp32)."""
     e = torch.as_tensor(prompt_emb).cuda()
@@ -405,12 +414,16 @@ def denoise_step(model: ToyModel, latent, t: float, step_scale: float, cache: Kv
     return lat.sub_(eps, alpha=float(step_scale))
 
 
+def _decode_px(model: ToyModel, x: torch.Tensor) -> torch.Tensor:
+    """engine.py:272-277 on device: uint8 [T, h*w] = clip(127.5 + 48 * rms(x) @ w_decode)."""
+    xr = x / torch.sqrt((x * x).mean(dim=-1, keepdim=True) + 1e-6)
+    return torch.clamp(127.5 + 48.0 * (xr @ model.w_decode), 0.0, 255.0).to(torch.uint8)
+
+
 def decode_frames(model: ToyModel, latent) -> list:
     """engine.py:272-277 — affine map of each latent row to a clamped uint8 frame (fp32)."""
     h, w = model.config.frame_shape
-    x = torch.as_tensor(latent).to(require_cuda(), torch.float32)
-    xr = x / torch.sqrt((x * x).mean(dim=-1, keepdim=True) + 1e-6)
-    px = torch.clamp(127.5 + 48.0 * (xr @ model.w_decode), 0.0, 255.0).to(torch.uint8)
+    px = _decode_px(model, torch.as_tensor(latent).to(require_cuda(), torch.float32))
     return list(px.view(-1, h, w).cpu().numpy())
 
 
@@ -438,16 +451,24 @@ def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSche
     schedule.validate()
     c = model.config
     if noise is None:
-        noise = _init_noise(c, seed, chunk_index)
-    lat = (noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)).to(
-        require_cuda(), torch.float32, non_blocking=True).clone()
+        noise = _init_noise_pinned(c, seed, chunk_index)
+    src = noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)
+    lat = torch.empty(src.shape, device=require_cuda(), dtype=torch.float32)
+    lat.copy_(src, non_blocking=True)  # async H2D when the noise lives in pinned memory
     ctx = _ctx_from_cache(model, cache)
     cross = _cross_from_cache(model, cache, prompt_ctx)
     _runner(model).denoise(lat, schedule, ctx, cross, cache, chunk_index)
     if not to_host:
         return GeneratedBlock(chunk_index, lat, [], prompt_text)
-    frames = decode_frames(model, lat)
-    return GeneratedBlock(chunk_index, lat.cpu().numpy(), frames, prompt_text)
+    # frames decoded on device; latent + frames land in pinned host buffers (one sync)
+    h, w = c.frame_shape
+    px = _decode_px(model, lat)
+    lat_h = torch.empty(lat.shape, dtype=torch.float32, pin_memory=True)
+    px_h = torch.empty(px.shape, dtype=torch.uint8, pin_memory=True)
+    lat_h.copy_(lat, non_blocking=True)
+    px_h.copy_(px, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return GeneratedBlock(chunk_index, lat_h.numpy(), list(px_h.view(-1, h, w).numpy()), prompt_text)
 
 
 class Engine:
@@ -499,7 +520,7 @@ class Engine:
         with self._lock:
             self._schedule = list(request.prompt_schedule)
             self._generating_chunk = -1
-        make_noise = noise_provider or (lambda ch: _init_noise(c, request.seed, ch))
+        make_noise = noise_provider or (lambda ch: _init_noise_pinned(c, request.seed, ch))
         pool = ThreadPoolExecutor(1)
         nxt = pool.submit(make_noise, 0)
         blocks = []

@@ -150,7 +150,10 @@ class PageTable:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            _abi.lib().ifx_pt_destroy(h)
+            try:
+                _abi.lib().ifx_pt_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     @staticmethod
