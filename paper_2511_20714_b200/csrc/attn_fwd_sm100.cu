@@ -10,17 +10,19 @@
 //   warp 0      TMA producer: Q once, then K_j / V_j tiles (128 keys x head_dim, SW128)
 //               into 2-stage smem rings; mbarrier tx completion
 //   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into TMEM (double-buffered S),
-//               O += P_{j-1} V_{j-1} with P read from TMEM (TS form); tcgen05.commit frees
-//               smem stages and signals the softmax warps
-//   warps 2-9   softmax, TWO warps per TMEM lane quarter: warp (q4, half) owns query rows
-//               32*q4..+31 and key columns 64*half..+63 of every S tile. The halves swap
-//               partial row maxima through smem (64-thread named barrier), then each does
-//               its 64 exponentials (1 in 4 on the FMA pipe), writes its 32 packed bf16 P
-//               columns into the upper half of the S buffer, rescales its half of O lazily
-//               (only when the running max grows by > 2^8) and stores its half of the output.
-// Why two warps per quarter (profiles/r02_attn_diagnostics.md): a single softmax warp per
-// SM sub-partition serialises TMEM loads (~120 B/clk/SM at 1 warp, ~220 at 2) with the
-// MUFU work (16 ex2/clk/SM); the second warp overlaps one with the other.
+//               then per key half h: O_h += P_h V_h (P read from TMEM, TS form) as soon as
+//               that half's P is published; tcgen05.commit frees smem stages / signals
+//   warps 2-9   softmax, TWO warps per TMEM lane quarter: warp (q4, h) owns query rows
+//               32*q4..+31 and key columns 64h..64h+63 of every S tile and runs its OWN
+//               online softmax over them (own running max / denominator, own accumulator
+//               O_h), so the two warps of a sub-partition never synchronise per tile and
+//               overlap freely (one in TMEM loads while the other is on MUFU/FMA). 64
+//               exponentials per warp per tile, 1 pair in 4 as a cubic on the FMA pipe,
+//               FFMA2/FADD2 packed math; P (bf16) overwrites the S columns it came from;
+//               lazy O rescale (only when the running max grows by > 2^8). The epilogue
+//               merges (O_0, m_0, l_0) and (O_1, m_1, l_1) (attention.py:157-180) and each
+//               warp stores half of the head dims.
+// Design study with the measurements behind each choice: profiles/r02_attn_variants.md.
 // Keys come from two segments so the block's own K/V never need to be copied next to the
 // cache: segment 0 = slab rows [ctx_row0, ctx_row0 + n_ctx), segment 1 = rows [0, n_cur)
 // of the fresh QKV projection. Ragged tails are masked in softmax (TMA zero-fills rows past
