@@ -149,6 +149,16 @@ int ifx_attn_fwd(const ifx_attn_params* p, void* stream);
 int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
                  float* x_out, void* y, void* stream);
 
+/* 3D RoPE (B200 extension; the reference has no positional encoding, attention.py:6):
+ * rotate, in place, the interleaved pairs (2k, 2k+1), k < pairs, of every head of the Q
+ * columns [q_col0 + h*head_stride, ...) and K columns [k_col0 + ...) of `rows` bf16 rows
+ * (row stride ld) by the angle whose cos/sin are tables[(tab_row0 + r) * pairs + k] (fp32).
+ * Applied once after the QKV projection, so cached K is stored post-RoPE. Semantics:
+ * oracle/rope.py (Wan2.1-style frame/row/column split of the head dims). */
+int ifx_rope_qk(void* qkv, int64_t rows, int64_t ld, int64_t heads, int64_t head_stride,
+                int64_t pairs, int64_t q_col0, int64_t k_col0, const float* cos_t,
+                const float* sin_t, int64_t tab_row0, void* stream);
+
 /* Ulysses head<->sequence re-shard (parallel.py:150-169). A row-major [n][groups][world]
  * [chunk] activation (e.g. groups=3 for fused Q|K|V, each split into per-peer head chunks)
  * is packed as [world][n][groups][chunk] so one all-to-all moves every peer's heads

@@ -16,6 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .attention import multi_head, windowed_block_causal_mask
+from .rope import apply_rope, rope_tables
 from .errors import ConfigError, DimensionError
 from .kvcache import CROSS_ATTN, SELF_ATTN, KvConfig, create_cache
 
@@ -34,6 +35,9 @@ class ModelConfig:
     frame_shape: tuple = (16, 16)
     prompt_dim: int = 16
     weight_seed: int = 0
+    # B200 extension (not in the reference): 3D RoPE over (frames_per_block, grid_h, grid_w)
+    rope_grid: tuple | None = None
+    rope_theta: float = 10000.0
 
     def validate(self):
         for n in ("layers", "heads", "head_dim", "block_len", "prompt_dim"):
@@ -41,6 +45,14 @@ class ModelConfig:
                 raise ConfigError(f"{n} must be >= 1")
         if min(self.frame_shape) < 1:
             raise ConfigError("frame_shape must be positive")
+        if self.rope_grid is not None and int(np.prod(self.rope_grid)) != self.block_len:
+            raise ConfigError("rope_grid must tile block_len")
+
+    def rope(self, chunk: int):
+        """(cos, sin) of block `chunk`, or None without RoPE (oracle/rope.py)."""
+        if self.rope_grid is None:
+            return None
+        return rope_tables(self.rope_grid, chunk * self.rope_grid[0], self.head_dim, self.rope_theta)
 
     @property
     def model_dim(self) -> int:
@@ -130,14 +142,19 @@ def rms(x):
     return (x / np.sqrt(np.mean(x * x, axis=-1, keepdims=True, dtype=_F32) + _EPS)).astype(_F32)
 
 
-def forward_block(model: ToyModel, latent, t, ctx, cross, collect_kv=False):
-    """engine.py:185-221 — one pass over a block; ctx[l] = (K, V) [C, D]."""
+def forward_block(model: ToyModel, latent, t, ctx, cross, collect_kv=False, chunk=0):
+    """engine.py:185-221 — one pass over a block; ctx[l] = (K, V) [C, D]. With
+    `rope_grid` set (B200 extension) q and the block's own k are rotated at the block's
+    positions; cached context K is already rotated."""
     heads = model.config.heads
+    rope = model.config.rope(chunk)
     x = (latent + _F32(t) * model.time_vec).astype(_F32)
     kv = []
     for li, w in enumerate(model.layers):
         h = rms(x)
         q, kc, vc = h @ w["wq"], h @ w["wk"], h @ w["wv"]
+        if rope is not None:
+            q, kc = apply_rope(q, *rope, heads), apply_rope(kc, *rope, heads)
         ck, cvv = ctx[li]
         kk = np.concatenate([ck, kc]) if ck.size else kc
         vv = np.concatenate([cvv, vc]) if cvv.size else vc
@@ -221,9 +238,9 @@ def generate_block(model, cache, schedule, prompt_ctx, chunk_index, seed):
     ctx = context_from_cache(model, cache)
     cross = cross_from_cache(model, cache, prompt_ctx)
     for t in schedule.steps:
-        eps, _ = forward_block(model, lat, t, ctx, cross)
+        eps, _ = forward_block(model, lat, t, ctx, cross, chunk=chunk_index)
         lat = (lat - _F32(schedule.step_scale) * eps).astype(_F32)
-    _, kv = forward_block(model, lat, 0.0, ctx, cross, collect_kv=True)
+    _, kv = forward_block(model, lat, 0.0, ctx, cross, collect_kv=True, chunk=chunk_index)
     if cache is not None:
         for li, (k, v) in enumerate(kv):
             cache.append_block(li, k, v, kind=SELF_ATTN, chunk_index=chunk_index)
@@ -280,13 +297,20 @@ def recompute_reference(model, request: GenerationRequest):
         lat = init_noise(cfg, request.seed, chunk)
         nb = len(clean) + 1
         mask = windowed_block_causal_mask(nb, L, request.kv_window)
+        rope = None
+        if cfg.rope_grid is not None:  # every token at its own block's absolute positions
+            tabs = [cfg.rope(bi) for bi in range(nb)]
+            rope = (np.concatenate([c for c, _ in tabs]), np.concatenate([s for _, s in tabs]))
         for t in request.schedule.steps:
             tcol = np.zeros((nb * L, 1), _F32)
             tcol[(nb - 1) * L:] = _F32(t)
             x = (np.concatenate(clean + [lat]).astype(_F32) + tcol * model.time_vec).astype(_F32)
             for w in model.layers:
                 h = rms(x)
-                x = x + multi_head(h @ w["wq"], h @ w["wk"], h @ w["wv"], heads, mask) @ w["wo"]
+                q, k = h @ w["wq"], h @ w["wk"]
+                if rope is not None:
+                    q, k = apply_rope(q, *rope, heads), apply_rope(k, *rope, heads)
+                x = x + multi_head(q, k, h @ w["wv"], heads, mask) @ w["wo"]
                 h2 = rms(x)
                 y = np.empty_like(x)
                 for bi in range(nb):

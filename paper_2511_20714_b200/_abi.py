@@ -40,7 +40,7 @@ EXPORTS = (
     "ifx_pt_stats", "ifx_pt_snapshot",
     "ifx_kv_append", "ifx_kv_gather",
     "ifx_attn_fwd",
-    "ifx_rms_bf16", "ifx_ulysses_pack", "ifx_ulysses_unpack",
+    "ifx_rms_bf16", "ifx_rope_qk", "ifx_ulysses_pack", "ifx_ulysses_unpack",
 )
 
 
@@ -96,6 +96,7 @@ def lib() -> ctypes.CDLL:
             L.ifx_kv_gather.argtypes = [P, P, I64, ctypes.c_int, P, I64, I64, I64, P, P, P]
             L.ifx_attn_fwd.argtypes = [ctypes.POINTER(AttnParams), P]
             L.ifx_rms_bf16.argtypes = [P, I64, I64, P, ctypes.c_float, P, P, P]
+            L.ifx_rope_qk.argtypes = [P, I64, I64, I64, I64, I64, I64, I64, P, P, I64, P]
             L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]
             L.ifx_ulysses_unpack.argtypes = [P, I64, I64, I64, I64, ctypes.c_int, P, I64, P]
             _lib = L

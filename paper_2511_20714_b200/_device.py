@@ -100,6 +100,16 @@ def rms_bf16(x: torch.Tensor, out: torch.Tensor, tvec: torch.Tensor | None = Non
     return out
 
 
+def rope_qk(qkv: torch.Tensor, heads: int, head_stride: int, pairs: int, q_col0: int, k_col0: int,
+            cos: torch.Tensor, sin: torch.Tensor, tab_row0: int = 0, stream=None) -> torch.Tensor:
+    """Enqueue the in-place 3D RoPE of the Q and K column blocks of a bf16 QKV buffer."""
+    _abi.check(_abi.lib().ifx_rope_qk(qkv.data_ptr(), qkv.shape[0], row_ld(qkv), heads,
+                                      head_stride, pairs, q_col0, k_col0, cos.data_ptr(),
+                                      sin.data_ptr(), tab_row0, stream_ptr(stream)), "rope")
+    LAUNCHES[0] += 1
+    return qkv
+
+
 def dtype_code(dt: torch.dtype) -> int:
     if dt == torch.float32:
         return _abi.F32

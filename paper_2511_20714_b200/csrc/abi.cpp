@@ -151,6 +151,19 @@ int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec,
   return ifx::cuda_fail(e, "rms launch");
 }
 
+int ifx_rope_qk(void* qkv, int64_t rows, int64_t ld, int64_t heads, int64_t head_stride,
+                int64_t pairs, int64_t q_col0, int64_t k_col0, const float* cos_t,
+                const float* sin_t, int64_t tab_row0, void* stream) {
+  if (rows < 0 || heads < 1 || pairs < 1 || 2 * pairs > head_stride)
+    return ifx::fail(IFX_EDIM, "bad rope sizes");
+  if ((ld | head_stride | q_col0 | k_col0) & 1)
+    return ifx::fail(IFX_EDIM, "rope pairs must be 4-byte aligned");
+  if (rows == 0) return IFX_OK;
+  int e = ifx::rope_launch(qkv, rows, ld, (int)heads, head_stride, (int)pairs, q_col0, k_col0,
+                           cos_t, sin_t, tab_row0, static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "rope launch");
+}
+
 int ifx_ulysses_pack(const void* src, int64_t n, int64_t groups, int64_t world, int64_t chunk,
                      int64_t src_ld, int type, void* dst, void* stream) {
   const int esz = type == IFX_BF16 ? 2 : 4;

@@ -13,6 +13,9 @@ int kv_gather_launch(const void* ks, const void* vs, int64_t ld, int esz, const 
                      cudaStream_t st);
 int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
                float* x_out, void* y, cudaStream_t st);
+int rope_launch(void* qkv, int64_t rows, int64_t ld, int heads, int64_t head_stride, int pairs,
+                int64_t q_col0, int64_t k_col0, const float* cos_t, const float* sin_t,
+                int64_t tab_row0, cudaStream_t st);
 int ulysses_launch(const void* src, void* dst, int64_t n, int64_t groups, int64_t world,
                    int64_t chunk_bytes, int64_t ld_bytes, bool pack, cudaStream_t st);
 }  // namespace ifx

@@ -144,6 +144,33 @@ __global__ void ulysses_transpose(const uint8_t* __restrict__ src, uint8_t* __re
   }
 }
 
+// ---- 3D RoPE on the Q and K column blocks of a fused QKV buffer, in place (bf16) --------
+// One thread per (row, head, pair): rotates the interleaved pair (2k, 2k+1) of q and of k by
+// the row's angle k (cos/sin tables [tab_rows, pairs], fp32). Semantics: oracle/rope.py.
+__global__ void rope_qk_kernel(__nv_bfloat16* __restrict__ qkv, int64_t rows, int64_t ld,
+                               int heads, int64_t head_stride, int pairs, int64_t q_col0,
+                               int64_t k_col0, const float* __restrict__ cos_t,
+                               const float* __restrict__ sin_t, int64_t tab_row0) {
+  const int64_t total = rows * heads * pairs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % pairs);
+    const int64_t rest = i / pairs;
+    const int h = (int)(rest % heads);
+    const int64_t r = rest / heads;
+    const int64_t t = (tab_row0 + r) * pairs + k;
+    const float c = __ldg(cos_t + t), s = __ldg(sin_t + t);
+    const int64_t off = r * ld + h * head_stride + 2 * k;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      __nv_bfloat162* p =
+          reinterpret_cast<__nv_bfloat162*>(qkv + off + (which == 0 ? q_col0 : k_col0));
+      const float2 v = __bfloat1622float2(*p);
+      *p = __floats2bfloat162_rn(v.x * c - v.y * s, v.x * s + v.y * c);
+    }
+  }
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t blocks = (work + threads - 1) / threads;
   const int64_t cap = (int64_t)kSMs * 8;
@@ -194,6 +221,16 @@ int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, f
   const int g = (int)(blocks < (int64_t)kSMs * 16 ? blocks : (int64_t)kSMs * 16);
   rms_bf16_kernel<<<g, threads, 0, st>>>(x, rows, width, tvec, t, x_out,
                                          static_cast<__nv_bfloat16*>(y));
+  return (int)cudaGetLastError();
+}
+
+int rope_launch(void* qkv, int64_t rows, int64_t ld, int heads, int64_t head_stride, int pairs,
+                int64_t q_col0, int64_t k_col0, const float* cos_t, const float* sin_t,
+                int64_t tab_row0, cudaStream_t st) {
+  const int threads = 256;
+  rope_qk_kernel<<<grid_for(rows * heads * pairs, threads), threads, 0, st>>>(
+      static_cast<__nv_bfloat16*>(qkv), rows, ld, heads, head_stride, pairs, q_col0, k_col0, cos_t,
+      sin_t, tab_row0);
   return (int)cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ from typing import Callable
 import numpy as np
 import torch
 
-from ._device import attn_fwd, require_cuda, rms_bf16
+from ._device import attn_fwd, require_cuda, rms_bf16, rope_qk
 from .errors import ConfigError, DimensionError
 from .kvcache import CROSS_ATTN, SELF_ATTN, KvCache, KvConfig
 
@@ -47,6 +47,10 @@ class ModelConfig:
     frame_shape: tuple = (16, 16)
     prompt_dim: int = 16
     weight_seed: int = 0
+    # B200 extension (the reference has no positional encoding, attention.py:6): 3D RoPE on
+    # Q/K over (frames_per_block, latent_h, latent_w); None = off (reference semantics)
+    rope_grid: tuple | None = None
+    rope_theta: float = 10000.0
 
     def validate(self):
         for name in ("layers", "heads", "head_dim", "block_len", "prompt_dim"):
@@ -54,10 +58,35 @@ class ModelConfig:
                 raise ConfigError(f"{name} must be >= 1")
         if self.frame_shape[0] < 1 or self.frame_shape[1] < 1:
             raise ConfigError("frame_shape must be positive")
+        if self.rope_grid is not None and math.prod(self.rope_grid) != self.block_len:
+            raise ConfigError("rope_grid must tile block_len")
+        if self.rope_grid is not None and self.head_dim % 2:
+            raise ConfigError("RoPE needs an even head_dim")
 
     @property
     def model_dim(self) -> int:
         return self.heads * self.head_dim
+
+
+def rope_tables(cfg: ModelConfig, chunk: int, dev) -> tuple | None:
+    """cos/sin [block_len, head_dim/2] fp32 on device for block `chunk` (None without RoPE).
+
+    head_dim d splits into d - 4*(d//6) frame dims and 2*(d//6) each for latent row /
+    column; token i of block b sits at frame b*F + i//(h*w), row (i % (h*w))//w, column
+    i % w; pair k of a part of size n rotates by pos * theta^(-2k/n). Angles in fp64."""
+    if cfg.rope_grid is None:
+        return None
+    F, gh, gw = cfg.rope_grid
+    d = cfg.head_dim
+    i = torch.arange(F * gh * gw, device=dev, dtype=torch.int64)
+    pos = (chunk * F + i // (gh * gw), (i % (gh * gw)) // gw, i % gw)
+    s = d // 6
+    angs = []
+    for p, n in zip(pos, (d - 4 * s, 2 * s, 2 * s)):
+        inv = cfg.rope_theta ** (-torch.arange(0, n, 2, device=dev, dtype=torch.float64) / n)
+        angs.append(p.to(torch.float64)[:, None] * inv[None, :])
+    ang = torch.cat(angs, dim=1)
+    return torch.cos(ang).float().contiguous(), torch.sin(ang).float().contiguous()
 
 
 @dataclass
@@ -294,8 +323,10 @@ class BlockRunner:
         self.attn_events = None
 
     def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
-                collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None):
-        """One pass. ctx[l] = (slab, base, total) or None; cross[l] = (k, v, row0, n) or None."""
+                collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None,
+                rope=None):
+        """One pass. ctx[l] = (slab, base, total) or None; cross[l] = (k, v, row0, n) or None;
+        rope = (cos, sin) tables of this block (rope_tables) or None."""
         m, ws = self.model, self.ws
         c = m.config
         H, dhp, Dp = m.heads_pad, m.dh_pad, m.attn_width
@@ -307,6 +338,8 @@ class BlockRunner:
             else:
                 rms_bf16(ws.x, ws.h)
             torch.mm(ws.h, lw.wqkv, out=ws.qkv)
+            if rope is not None:  # Q and the block's own K, before K1 and the page write
+                rope_qk(ws.qkv, H, dhp, c.head_dim // 2, 0, Dp, rope[0], rope[1])
             ev = self.attn_events
             if ev is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
@@ -343,11 +376,12 @@ class BlockRunner:
         """engine.py:296-306: S Euler steps in place on `latent`, then the clean K/V pass."""
         eps = self.ws.tmp.new_empty(self.ws.tmp.shape) if not hasattr(self, "_eps") else self._eps
         self._eps = eps
+        rope = rope_tables(self.model.config, chunk_index, self.dev)
         for t in schedule.steps:
-            self.forward(latent, float(t), ctx, cross, cache, eps_out=eps)
+            self.forward(latent, float(t), ctx, cross, cache, eps_out=eps, rope=rope)
             latent.add_(eps, alpha=-float(schedule.step_scale))
         self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
-                     chunk_index=chunk_index)
+                     chunk_index=chunk_index, rope=rope)
         return latent
 
 
@@ -410,7 +444,8 @@ def denoise_step(model: ToyModel, latent, t: float, step_scale: float, cache: Kv
         r.ws = _Workspace(lat.shape[0], c.model_dim, model.attn_width, r.dev)
     eps = torch.empty_like(lat)
     r.forward(lat, float(t), _ctx_from_cache(model, cache), _cross_from_cache(model, cache, prompt_ctx),
-              cache, eps_out=eps)
+              cache, eps_out=eps, rope=rope_tables(c, 0, lat.device) if lat.shape[0] == c.block_len
+              else None)
     return lat.sub_(eps, alpha=float(step_scale))
 
 

@@ -307,7 +307,8 @@ class UlyssesRunner:
         from ._device import rms_bf16
         return rms_bf16(x, out, tvec, t, x_out)
 
-    def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None):
+    def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None,
+                rope=None):
         from .engine import _ffn_up, _residual
         from .kvcache import SELF_ATTN
         m = self.model
@@ -320,6 +321,10 @@ class UlyssesRunner:
             else:
                 self._rms(self.x, self.h)
             torch.mm(self.h, lw.wqkv, out=self.qkv)
+            if rope is not None:  # this rank's rows of the block: table rows rank*n ..
+                from ._device import rope_qk
+                rope_qk(self.qkv, m.heads_pad, dhp, c.head_dim // 2, 0, m.attn_width, rope[0],
+                        rope[1], tab_row0=self.comm.rank * self.n)
             qkv_h = self.comm.seq_to_head(self.qkv, 3)          # [T, 3*wl] local heads
             q, kc, vc = qkv_h[:, :wl], qkv_h[:, wl:2 * wl], qkv_h[:, 2 * wl:]
             ev = self.attn_events
@@ -354,11 +359,13 @@ class UlyssesRunner:
             torch.mm(self.h, m.w_out, out_dtype=torch.float32, out=eps_out)
 
     def denoise(self, latent, schedule, ctx, cross, cache, chunk_index):
+        from .engine import rope_tables
+        rope = rope_tables(self.model.config, chunk_index, latent.device)
         for t in schedule.steps:
-            self.forward(latent, float(t), ctx, cross, cache, eps_out=self.eps)
+            self.forward(latent, float(t), ctx, cross, cache, eps_out=self.eps, rope=rope)
             latent.add_(self.eps, alpha=-float(schedule.step_scale))
         self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
-                     chunk_index=chunk_index)
+                     chunk_index=chunk_index, rope=rope)
         return latent
 
 

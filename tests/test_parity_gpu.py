@@ -254,3 +254,60 @@ def test_engine_full_size_properties():
     # block 1 without cache context differs from block 1 with context
     solo = E.generate_block(model, None, req.schedule, E.embed_prompt(model, "a quiet scene"), 1, 0)
     assert np.abs(solo.latent - b[1].latent).max() > 1e-3
+
+
+# ---------------------------------------------------------------- 3D RoPE (B200 extension)
+def test_rope_kernel_matches_oracle_math():
+    from oracle.rope import apply_rope, rope_tables as o_tables
+    from paper_2511_20714_b200._device import rope_qk
+    from paper_2511_20714_b200.engine import ModelConfig, rope_tables
+
+    for heads, dh, dhp in [(12, 128, 128), (3, 64, 64), (2, 12, 64)]:
+        grid = (3, 4, 5)
+        T = 60
+        cfg = ModelConfig(layers=1, heads=heads, head_dim=dh, block_len=T, rope_grid=grid)
+        cos, sin = rope_tables(cfg, 2, torch.device("cuda"))
+        oc, os_ = o_tables(grid, 2 * 3, dh)
+        np.testing.assert_allclose(_np(cos), oc, atol=1e-6)
+        np.testing.assert_allclose(_np(sin), os_, atol=1e-6)
+        Dp = heads * dhp
+        g = torch.Generator(device="cuda").manual_seed(dh)
+        qkv = torch.zeros(T, 3 * Dp, device="cuda", dtype=torch.bfloat16)
+        for h in range(heads):  # real dims only; padded dims stay zero
+            qkv[:, h * dhp:h * dhp + dh] = torch.randn(T, dh, device="cuda", generator=g).bfloat16()
+            qkv[:, Dp + h * dhp:Dp + h * dhp + dh] = torch.randn(T, dh, device="cuda", generator=g).bfloat16()
+        before = qkv.float().cpu().numpy()
+        rope_qk(qkv, heads, dhp, dh // 2, 0, Dp, cos, sin)
+        torch.cuda.synchronize()
+        after = qkv.float().cpu().numpy()
+        for col0 in (0, Dp):
+            x = np.concatenate([before[:, col0 + h * dhp:col0 + h * dhp + dh] for h in range(heads)], 1)
+            want = apply_rope(x, oc, os_, heads)
+            got = np.concatenate([after[:, col0 + h * dhp:col0 + h * dhp + dh] for h in range(heads)], 1)
+            assert np.abs(got - want).max() <= 2e-2
+        assert np.array_equal(after[:, 2 * Dp:], before[:, 2 * Dp:])  # V untouched
+
+
+@pytest.mark.parametrize("case", [(2, 4, 64, (3, 4, 4), 3, None), (2, 2, 12, (2, 2, 4), 3, 16),
+                                  (1, 12, 128, (3, 8, 10), 2, None)])
+def test_engine_with_rope_vs_oracle(case):
+    """Parity with the oracle restatement (unpinned by the reference: it has no RoPE)."""
+    from oracle import engine as OE
+    from paper_2511_20714_b200 import engine as E
+
+    L, H, dh, grid, nb, win = case
+    T = int(np.prod(grid))
+    kw = dict(layers=L, heads=H, head_dim=dh, block_len=T, frame_shape=(4, 4), prompt_dim=8,
+              rope_grid=grid)
+    req = dict(num_blocks=nb, seed=2, prompt_schedule=[(0, "a b"), (2, "c")], kv_window=win)
+    eng = E.Engine(E.build_model(E.ModelConfig(**kw)))
+    got = np.stack([b.latent for b in eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **req))])
+    om = OE.ToyModel(OE.ModelConfig(**kw))
+    oreq = OE.GenerationRequest(schedule=OE.DenoiseSchedule([1.0, 0.5]), **req)
+    want, ocache = OE.generate_sequence(om, oreq)
+    want = np.stack(want)
+    assert np.abs(got - want).max() <= ATOL_LATENT and _cos(got, want) > 0.999
+    assert eng.cache.state() == ocache.state()
+    # the cached GPU path also matches the oracle's cache-free recompute
+    rec = np.stack(OE.recompute_reference(om, oreq))
+    assert np.abs(got - rec).max() <= ATOL_LATENT

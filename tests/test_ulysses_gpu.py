@@ -55,7 +55,7 @@ CFG = dict(layers=2, heads=4, head_dim=64, block_len=256, frame_shape=(8, 8), pr
 REQ = dict(num_blocks=3, seed=0, prompt_schedule=[(0, "a quiet scene"), (2, "rain")])
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, cfg=None):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -64,7 +64,7 @@ def _rank(rank, world, port, q):
         from paper_2511_20714_b200 import engine as E
         from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
 
-        model = E.ToyModel(E.ModelConfig(**CFG), head_multiple=world)
+        model = E.ToyModel(E.ModelConfig(**(cfg or CFG)), head_multiple=world)
         eng = UlyssesEngine(model, UlyssesComm())
         lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
         q.put((rank, [l.cpu().numpy() for l in lats], eng.cache.state(), eng.comm.bytes))
@@ -72,17 +72,20 @@ def _rank(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_ulysses_engine_matches_single_gpu(world):
+CFG_ROPE = dict(CFG, rope_grid=(1, 16, 16), heads=3)  # 3 heads on 2 ranks: dummy-head padding
+
+
+@pytest.mark.parametrize("world,cfg", [(2, CFG), (2, CFG_ROPE)])
+def test_ulysses_engine_matches_single_gpu(world, cfg):
     from paper_2511_20714_b200 import engine as E
 
-    ref_model = E.build_model(E.ModelConfig(**CFG))
+    ref_model = E.build_model(E.ModelConfig(**cfg))
     ref_eng = E.Engine(ref_model)
     ref = ref_eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, cfg)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
