@@ -300,7 +300,7 @@ def run_ours(args):
         "attention_frac_of_peak": achieved / peak,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "K1 attn_fwd_kernel<128,true> (tcgen05/TMEM/TMA)",
+                     "kernel": "K1 attn_fwd_kernel<128> (tcgen05/TMEM/TMA)",
                      "launches": n_attn, "kernel_ms_per_step": attn_ms / args.steps,
                      "share_of_step": attn_ms / args.steps / ms},
         "e2e": {"value": nb * FRAMES_PER_BLOCK / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,

@@ -581,9 +581,11 @@ class Engine:
                 span = prof.scoped("generate_block") if prof else None
                 if span:
                     span.__enter__()
+                torch.cuda.nvtx.range_push(f"block{chunk}")  # ncu --nvtx-include scoping
                 block = generate_block(self.model, self.cache, request.schedule, None, chunk,
                                        request.seed, prompt_text=prompt, noise=noise,
                                        to_host=to_host)
+                torch.cuda.nvtx.range_pop()
                 if span:
                     span.__exit__(None, None, None)
                 if request.kv_window is not None:
