@@ -208,9 +208,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank (NCCL). IFX_DIST_BACKEND=gloo lets several ranks share a GPU to test
+    # the multi-rank code path on a 1-GPU box (UlyssesComm stages the a2a through the host).
+    backend = os.environ.get("IFX_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfgname = args.config or "c2"
     c = CONFIGS[cfgname]
     if world > 1:
@@ -282,11 +289,15 @@ def run_ours(args):
     assert all(np.isfinite(b.latent).all() for b in blocks)
 
     cpu = None if args.no_cpu_baseline else cpu_baseline(c, cfgname)
-    traffic = None
+    traffic, traffic_note = None, None
     tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(cfgname)
+            t_rec = json.load(f).get(cfgname)
+        if t_rec:  # DRAM bytes of one K1 launch from an ncu --set full capture
+            traffic = t_rec["dram_bytes_per_launch"]
+            traffic_note = (f"{t_rec['launch']}; algorithmic {t_rec['algorithmic_bytes_per_launch']} B; "
+                            f"{t_rec['source']}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -299,7 +310,8 @@ def run_ours(args):
         "attention_tflops": achieved,
         "attention_frac_of_peak": achieved / peak,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_launch": traffic_note,
+                     "peak_source": peak_src,
                      "kernel": "K1 attn_fwd_kernel<128> (tcgen05/TMEM/TMA)",
                      "launches": n_attn, "kernel_ms_per_step": attn_ms / args.steps,
                      "share_of_step": attn_ms / args.steps / ms},
