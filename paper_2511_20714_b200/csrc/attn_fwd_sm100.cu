@@ -17,7 +17,7 @@
 //               online softmax over them (own running max / denominator, own accumulator
 //               O_h), so the two warps of a sub-partition never synchronise per tile and
 //               overlap freely (one in TMEM loads while the other is on MUFU/FMA). 64
-//               exponentials per warp per tile, 1 pair in 4 as a cubic on the FMA pipe,
+//               exponentials per warp per tile, 3 pairs in 8 as a cubic on the FMA pipe,
 //               FFMA2/FADD2 packed math; P (bf16) overwrites the S columns it came from;
 //               lazy O rescale (only when the running max grows by > 2^8). The epilogue
 //               merges (O_0, m_0, l_0) and (O_1, m_1, l_1) (attention.py:157-180) and each
@@ -49,7 +49,11 @@ constexpr int NB = 2;            // S buffers in TMEM (P aliases S)
 constexpr int NTHREADS = 320;    // 10 warps
 constexpr int NSOFT = 256;       // softmax threads
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if max grows > 2^8
-constexpr int kPolyEvery = 4;              // every 4th exp2 of a full tile on the FMA pipe
+#ifndef IFX_POLY_PAIRS_OF_8
+#define IFX_POLY_PAIRS_OF_8 3  // measured best of 2, 3, 4 (profiles/r02_attn_variants.md)
+#endif
+// exp2 pairs (out of every 8 pairs) evaluated as a cubic on the FMA pipe instead of MUFU
+constexpr int kPolyPairsOf8 = IFX_POLY_PAIRS_OF_8;
 
 // 2^x on the FMA/ALU pipes (round-to-nearest split, cubic on [-0.5, 0.5], exponent add):
 // rel. error < 5e-4, far below bf16 P rounding. x is clamped to >= -125 (result ~0).
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int i = 0; i < HALF / 2; ++i) {
           const float2 x = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), sl2v, negm);
           float2 p;
-          if ((i & 3) == 3) {
+          if ((i & 7) >= 8 - kPolyPairsOf8) {
             p = ex2_poly2(x);  // 1 pair in 4 = 25% of the exponentials on the FMA pipe
           } else {
             p.x = ex2(x.x);
