@@ -139,9 +139,17 @@ typedef struct ifx_attn_params {
    * the denominator relative to it, so callers can merge partials (attention.py:157-173) */
   float* row_max;
   float* row_sum;
+  /* optional device scratch for split-KV (size from ifx_attn_workspace_bytes). When given
+   * and (query tiles x heads) would leave the SMs under-filled (e.g. a Ulysses rank holding
+   * few heads), the key range is split across CTAs and merged by a combine kernel
+   * (attention.py:157-180 semantics). NULL = never split. Not combined with row_max. */
+  void* workspace;
+  int64_t workspace_bytes;
 } ifx_attn_params;
 
 int ifx_attn_fwd(const ifx_attn_params* p, void* stream);
+/* bytes of `workspace` that allow ifx_attn_fwd to split the key range up to 8 ways */
+int ifx_attn_workspace_bytes(const ifx_attn_params* p, int64_t* bytes);
 
 /* Fused RMS-norm (engine.py:171-173) + optional time conditioning, fp32 in, bf16 out:
  * y = bf16( (x + t*tvec) / sqrt(mean((x + t*tvec)^2) + eps) ). If x_out != NULL the

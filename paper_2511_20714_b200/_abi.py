@@ -39,7 +39,7 @@ EXPORTS = (
     "ifx_pt_clear_cross", "ifx_pt_touch_range", "ifx_pt_touch_indices", "ifx_pt_range",
     "ifx_pt_stats", "ifx_pt_snapshot",
     "ifx_kv_append", "ifx_kv_gather",
-    "ifx_attn_fwd",
+    "ifx_attn_fwd", "ifx_attn_workspace_bytes",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_ulysses_pack", "ifx_ulysses_unpack",
 )
 
@@ -57,6 +57,7 @@ class AttnParams(ctypes.Structure):
         ("heads", ctypes.c_int64), ("head_dim", ctypes.c_int64), ("scale", ctypes.c_float),
         ("mask", ctypes.c_void_p), ("mask_ld", ctypes.c_int64),
         ("row_max", ctypes.c_void_p), ("row_sum", ctypes.c_void_p),
+        ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_int64),
     ]
 
 
@@ -95,6 +96,7 @@ def lib() -> ctypes.CDLL:
             L.ifx_kv_append.argtypes = [P, P, I64, ctypes.c_int, P, P, I64, ctypes.c_int, I64, I64, I64, P]
             L.ifx_kv_gather.argtypes = [P, P, I64, ctypes.c_int, P, I64, I64, I64, P, P, P]
             L.ifx_attn_fwd.argtypes = [ctypes.POINTER(AttnParams), P]
+            L.ifx_attn_workspace_bytes.argtypes = [ctypes.POINTER(AttnParams), PI64]
             L.ifx_rms_bf16.argtypes = [P, I64, I64, P, ctypes.c_float, P, P, P]
             L.ifx_rope_qk.argtypes = [P, I64, I64, I64, I64, I64, I64, I64, P, P, I64, P]
             L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]

@@ -56,13 +56,24 @@ def row_ld(t: torch.Tensor) -> int:
     return t.stride(0)
 
 
+_WS: dict = {}
+
+
+def _workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
+    """Grow-only per-device scratch for K1's split-KV partials (stream-ordered reuse)."""
+    w = _WS.get(dev)
+    if w is None or w.numel() < nbytes:
+        w = _WS[dev] = torch.empty(max(nbytes, 1 << 20), device=dev, dtype=torch.uint8)
+    return w
+
+
 def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
              ctx_k: torch.Tensor | None = None, ctx_v: torch.Tensor | None = None,
              ctx_row0: int = 0, n_ctx: int = 0,
              cur_k: torch.Tensor | None = None, cur_v: torch.Tensor | None = None,
              scale: float | None = None, mask: torch.Tensor | None = None,
              row_max: torch.Tensor | None = None, row_sum: torch.Tensor | None = None,
-             stream=None) -> torch.Tensor:
+             split_kv: bool = True, stream=None) -> torch.Tensor:
     """Enqueue K1 (attn_fwd_sm100.cu): out = softmax(q [ctx∥cur]^T * scale) [ctx∥cur].
 
     q/out: [n_q, heads*head_dim] bf16 (row-strided views allowed). ctx_*: slabs whose rows
@@ -84,7 +95,13 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
         p.mask, p.mask_ld = mask.data_ptr(), mask.stride(0)
     if row_max is not None:
         p.row_max, p.row_sum = row_max.data_ptr(), row_sum.data_ptr()
-    rc = _abi.lib().ifx_attn_fwd(ctypes.byref(p), stream_ptr(stream))
+    L = _abi.lib()
+    if split_kv and row_max is None:  # let the library split under-filled launches
+        need = ctypes.c_int64()
+        L.ifx_attn_workspace_bytes(ctypes.byref(p), ctypes.byref(need))
+        ws = _workspace(q.device, need.value)
+        p.workspace, p.workspace_bytes = ws.data_ptr(), ws.numel()
+    rc = L.ifx_attn_fwd(ctypes.byref(p), stream_ptr(stream))
     _abi.check(rc, "attn_fwd")
     LAUNCHES[0] += 1
     return out

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -60,6 +61,10 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols
   return IFX_OK;
 }
 
+int num_sms();
+int64_t split_workspace_bytes(const ifx_attn_params* p, int splits);
+int choose_splits(const ifx_attn_params* p);
+
 int attn_fwd(const ifx_attn_params* p, void* stream) {
   if (p->head_dim != 64 && p->head_dim != 128)
     return fail(IFX_EUNSUPPORTED, "head_dim must be 64 or 128");
@@ -95,9 +100,59 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   a.mask_ld = p->mask_ld;
   a.row_max = p->row_max;
   a.row_sum = p->row_sum;
+  a.heads = (int)p->heads;
+  a.n_splits = p->row_max != nullptr ? 1 : choose_splits(p);
+  if (a.n_splits > 1) {
+    char* ws = static_cast<char*>(p->workspace);
+    a.part_o = reinterpret_cast<__nv_bfloat16*>(ws);
+    a.part_ld = width;
+    a.part_m = reinterpret_cast<float*>(ws + a.n_splits * p->n_q * width * 2);
+    a.part_l = a.part_m + a.n_splits * p->heads * p->n_q;
+  }
   int e = attn_fwd_launch(a, (int)p->head_dim, (int)p->n_q, (int)p->heads,
                           static_cast<cudaStream_t>(stream));
   return cuda_fail(e, "attn_fwd launch");
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+int64_t split_workspace_bytes(const ifx_attn_params* p, int splits) {
+  const int64_t width = p->heads * p->head_dim;
+  return splits * p->n_q * width * 2 + 2 * splits * p->heads * p->n_q * 4 + 256;
+}
+
+// Split the key range only when (query tiles x heads) CTAs leave the SMs under-filled:
+// pick the split count with the best wave efficiency (ctas*s / sms / ceil(ctas*s / sms)),
+// at least 16 key tiles per split, within the caller's workspace.
+int choose_splits(const ifx_attn_params* p) {
+  if (p->workspace == nullptr) return 1;
+  const int sms = num_sms();
+  const int64_t ctas = ((p->n_q + 127) / 128) * p->heads;
+  if (ctas >= 3 * sms) return 1;
+  const int64_t tiles = (p->n_ctx + 127) / 128 + (p->n_cur + 127) / 128;
+  auto eff = [&](int s) {
+    const double w = (double)(ctas * s) / sms;
+    return w / std::ceil(w);
+  };
+  int best = 1;
+  double best_eff = eff(1);
+  for (int s = 2; s <= 8 && tiles / s >= 16; ++s) {
+    if (p->workspace_bytes < split_workspace_bytes(p, s)) break;
+    if (eff(s) > best_eff + 0.05) {
+      best = s;
+      best_eff = eff(s);
+    }
+  }
+  return best;
 }
 
 }  // namespace ifx
@@ -108,6 +163,11 @@ const char* ifx_last_error(void) { return ifx::g_last_error.c_str(); }
 int ifx_version(void) { return 1; }
 
 int ifx_attn_fwd(const ifx_attn_params* p, void* stream) { return ifx::attn_fwd(p, stream); }
+
+int ifx_attn_workspace_bytes(const ifx_attn_params* p, int64_t* bytes) {
+  *bytes = ifx::split_workspace_bytes(p, 8);
+  return IFX_OK;
+}
 
 int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_type, void* k_slab,
                   void* v_slab, int64_t slab_ld, int slab_type, int64_t dst_row, int64_t t,

@@ -153,7 +153,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int head = blockIdx.y;
   const int q0 = blockIdx.x * BM;
   const int n0 = (a.n_ctx + BN - 1) / BN;
-  const int n_tiles = n0 + (a.n_cur + BN - 1) / BN;
+  const int n_total = n0 + (a.n_cur + BN - 1) / BN;
+  // split-KV (blockIdx.z): this CTA walks key tiles [t0, t0 + n_tiles) and, when the key
+  // range is split, writes a partial (normalised O, max, denominator) merged by K4
+  const int split = blockIdx.z;
+  const int t0 = (int)(((int64_t)split * n_total) / a.n_splits);
+  const int n_tiles = (int)(((int64_t)(split + 1) * n_total) / a.n_splits) - t0;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tma_prefetch_desc(&a.tm_kc);
         tma_prefetch_desc(&a.tm_vc);
       }
-      if (n_tiles > n0) {
+      if (n_total > n0) {
         tma_prefetch_desc(&a.tm_kn);
         tma_prefetch_desc(&a.tm_vn);
       }
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % NS;
         const uint32_t ph = (j / NS) & 1;
-        const Tile t = tile_of(a, j, n0);
+        const Tile t = tile_of(a, t0 + j, n0);
         const CUtensorMap* mk = t.seg == 0 ? &a.tm_kc : &a.tm_kn;
         const CUtensorMap* mv = t.seg == 0 ? &a.tm_vc : &a.tm_vn;
         mbar_wait(k_empty + s, ph ^ 1);
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                                               : nullptr;
     for (int j = 0; j < n_tiles; ++j) {
       const int b = j % NB;
-      const Tile t = tile_of(a, j, n0);
+      const Tile t = tile_of(a, t0 + j, n0);
       const int c0 = half * HALF;  // first key column of this warp
       mbar_wait(s_full + b, (j / NB) & 1);
       tc_fence_after();
@@ -413,7 +418,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const float inv = den > 0.f ? 1.f / den : 0.f;
     const float w_lo = (half == 0 ? w_me : w_ot) * inv;  // weight of O_lo
     const float w_hi = (half == 0 ? w_ot : w_me) * inv;  // weight of O_hi
-    __nv_bfloat16* orow = a.o + (int64_t)grow * a.o_ld + head * HD + half * (HD / 2);
+    const bool partial = a.n_splits > 1;
+    __nv_bfloat16* orow =
+        partial ? a.part_o + ((int64_t)split * a.n_q + grow) * a.part_ld + head * HD + half * (HD / 2)
+                : a.o + (int64_t)grow * a.o_ld + head * HD + half * (HD / 2);
 #pragma unroll 1
     for (int c = 0; c < HD / 64; ++c) {
       uint32_t r0[32], r1[32];
@@ -442,7 +450,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     }
-    if (a.row_max != nullptr && grow < a.n_q && half == 0) {
+    if (partial && grow < a.n_q && half == 0) {  // K4 merges these (attention.py:157-173)
+      const int64_t k = ((int64_t)split * a.heads + head) * a.n_q + grow;
+      a.part_m[k] = M;
+      a.part_l[k] = den;
+    }
+    if (!partial && a.row_max != nullptr && grow < a.n_q && half == 0) {
       // exact max over both halves, denominator re-referenced to it (attention.py:140-154)
       const float mx = fmaxf(m_exact, mx_o);
       const bool live = mx > -INFINITY;
@@ -459,6 +472,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// K4 — merge split-KV partials (attention.py:157-180 semantics), one warp per (row, head):
+// out = sum_s w_s O_s / sum_s w_s with w_s = l_s * 2^(m_s - max_s m_s).
+template <int HD>
+__global__ void attn_combine_kernel(const AttnKernelArgs a) {
+  constexpr int PER = HD / 32;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+       w < (int64_t)a.n_q * a.heads; w += n_warps) {
+    const int row = (int)(w / a.heads), head = (int)(w % a.heads);
+    float M = -INFINITY;
+    for (int s = 0; s < a.n_splits; ++s)
+      M = fmaxf(M, a.part_m[((int64_t)s * a.heads + head) * a.n_q + row]);
+    float acc[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+    float den = 0.f;
+    for (int s = 0; s < a.n_splits; ++s) {
+      const int64_t k = ((int64_t)s * a.heads + head) * a.n_q + row;
+      const float ms = a.part_m[k];
+      const float wgt = (ms == -INFINITY) ? 0.f : a.part_l[k] * exp2f(ms - M);
+      den += wgt;
+      const __nv_bfloat16* src =
+          a.part_o + ((int64_t)s * a.n_q + row) * a.part_ld + head * HD + lane * PER;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) acc[i] += wgt * __bfloat162float(src[i]);
+    }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    __nv_bfloat16* dst = a.o + (int64_t)row * a.o_ld + head * HD + lane * PER;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) dst[i] = __float2bfloat16(acc[i] * inv);
+    if (a.row_max != nullptr && lane == 0) {
+      a.row_max[(int64_t)head * a.n_q + row] = M;
+      a.row_sum[(int64_t)head * a.n_q + row] = den;
+    }
+  }
+}
+
 template <int HD>
 int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
   using L = Layout<HD>;
@@ -469,8 +520,13 @@ int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  dim3 grid((n_q + BM - 1) / BM, heads);
+  dim3 grid((n_q + BM - 1) / BM, heads, a.n_splits);
   fn<<<grid, NTHREADS, L::SMEM, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || a.n_splits == 1) return (int)e;
+  const int64_t warps = (int64_t)n_q * heads;
+  const int blocks = (int)((warps + 7) / 8 < 148 * 16 ? (warps + 7) / 8 : 148 * 16);
+  attn_combine_kernel<HD><<<blocks, 256, 0, st>>>(a);
   return (int)cudaGetLastError();
 }
 

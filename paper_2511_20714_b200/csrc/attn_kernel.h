@@ -23,9 +23,16 @@ struct AttnKernelArgs {
   int64_t mask_ld;
   float* row_max;
   float* row_sum;
+  // split-KV (grid.z = n_splits > 1): partials merged by the K4 combine kernel
+  int heads, n_splits;
+  __nv_bfloat16* part_o;  // [n_splits, n_q, part_ld] normalised partial outputs
+  int64_t part_ld;
+  float* part_m;          // [n_splits, heads, n_q] max (log2 units)
+  float* part_l;          // [n_splits, heads, n_q] denominator w.r.t. part_m
 };
 
-// Grid (ceil(n_q/128), heads) x 320 threads. Returns cudaError_t.
+// Grid (ceil(n_q/128), heads, n_splits) x 320 threads (+ K4 combine when n_splits > 1).
+// Returns cudaError_t.
 int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int n_q, int heads, cudaStream_t st);
 
 }  // namespace ifx

@@ -17,8 +17,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--heads", type=int, default=12)
+    ap.add_argument("--no-split", action="store_true")
     args = ap.parse_args()
-    T, H, dh = 4680, 12, 128
+    T, H, dh = 4680, args.heads, 128
     D = H * dh
     res = []
     for b in ((0, 1, 3, 6, 20) if not args.quick else (3,)):
@@ -27,7 +29,8 @@ def main():
         ks = torch.randn(max(C, 1), D, device="cuda").bfloat16()
         vs = torch.randn(max(C, 1), D, device="cuda").bfloat16()
         out = torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
-        f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:])
+        f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:],
+                             split_kv=not args.no_split)
         for _ in range(3):
             f()
         torch.cuda.synchronize()
