@@ -30,58 +30,74 @@ __device__ __forceinline__ uint32_t f2_to_bf2(float a, float b) {
   return r;
 }
 
-// ---- K2: page write. One 16-byte destination vector per thread-iteration. -------------
-// same-type copy: vec = 16 bytes of src == 16 bytes of dst
+// ---- K2: page write / K7: gather. One WARP per (K|V, row): lanes stride the row's 16-byte
+// vectors, all loads of a row issued before its stores (up to 8 in flight per lane); no
+// 64-bit divisions in the hot loop. Grid-stride over 2*rows row units.
+template <int UNROLL>
+__device__ __forceinline__ void copy_row(const uint8_t* __restrict__ s, uint8_t* __restrict__ d,
+                                         int64_t row_vecs, int lane) {
+  for (int64_t c0 = lane; c0 < row_vecs; c0 += 32 * UNROLL) {
+    uint4 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      if (c0 + u * 32 < row_vecs) v[u] = ld_nc(s + (c0 + u * 32) * 16);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      if (c0 + u * 32 < row_vecs) st_na(d + (c0 + u * 32) * 16, v[u]);
+  }
+}
+
+// same-type copy: rows [0, t) of K and V -> slab rows (dst already offset to the first row)
 __global__ void append_same(const uint8_t* __restrict__ ks, const uint8_t* __restrict__ vs,
                             int64_t src_ld_b, uint8_t* __restrict__ kd, uint8_t* __restrict__ vd,
                             int64_t dst_ld_b, int64_t t, int64_t row_vecs) {
-  const int64_t total = t * row_vecs;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const bool is_v = i >= total;
-    const int64_t e = is_v ? i - total : i;
-    const int64_t r = e / row_vecs, c = e - r * row_vecs;
-    const uint8_t* s = (is_v ? vs : ks) + r * src_ld_b + c * 16;
-    uint8_t* d = (is_v ? vd : kd) + r * dst_ld_b + c * 16;
-    st_na(d, ld_nc(s));
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * t;
+       u += n_warps) {
+    const bool is_v = u >= t;
+    const int64_t r = is_v ? u - t : u;
+    copy_row<8>((is_v ? vs : ks) + r * src_ld_b, (is_v ? vd : kd) + r * dst_ld_b, row_vecs, lane);
   }
 }
-// fp32 -> bf16: each thread reads 32 B (8 floats) and writes 16 B
+// fp32 -> bf16: per 16-byte destination vector, 32 source bytes
 __global__ void append_f32_bf16(const float* __restrict__ ks, const float* __restrict__ vs,
                                 int64_t src_ld, __nv_bfloat16* __restrict__ kd,
                                 __nv_bfloat16* __restrict__ vd, int64_t dst_ld, int64_t t,
                                 int64_t row_vecs) {
-  const int64_t total = t * row_vecs;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const bool is_v = i >= total;
-    const int64_t e = is_v ? i - total : i;
-    const int64_t r = e / row_vecs, c = e - r * row_vecs;
-    const float* s = (is_v ? vs : ks) + r * src_ld + c * 8;
-    const uint4 a = ld_nc(s), b = ld_nc(s + 4);
-    uint4 o;
-    o.x = f2_to_bf2(__uint_as_float(a.x), __uint_as_float(a.y));
-    o.y = f2_to_bf2(__uint_as_float(a.z), __uint_as_float(a.w));
-    o.z = f2_to_bf2(__uint_as_float(b.x), __uint_as_float(b.y));
-    o.w = f2_to_bf2(__uint_as_float(b.z), __uint_as_float(b.w));
-    st_na((is_v ? vd : kd) + r * dst_ld + c * 8, o);
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * t;
+       u += n_warps) {
+    const bool is_v = u >= t;
+    const int64_t r = is_v ? u - t : u;
+    const float* srow = (is_v ? vs : ks) + r * src_ld;
+    __nv_bfloat16* drow = (is_v ? vd : kd) + r * dst_ld;
+    for (int64_t c = lane; c < row_vecs; c += 32) {
+      const uint4 a = ld_nc(srow + c * 8), b = ld_nc(srow + c * 8 + 4);
+      uint4 o;
+      o.x = f2_to_bf2(__uint_as_float(a.x), __uint_as_float(a.y));
+      o.y = f2_to_bf2(__uint_as_float(a.z), __uint_as_float(a.w));
+      o.z = f2_to_bf2(__uint_as_float(b.x), __uint_as_float(b.y));
+      o.w = f2_to_bf2(__uint_as_float(b.z), __uint_as_float(b.w));
+      st_na(drow + c * 8, o);
+    }
   }
 }
 
-// ---- K7: gather rows (explicit list or contiguous) ------------------------------------
+// K7: out[i] = slab[rows[i]] (rows == NULL: first_row + i), K and V
 __global__ void gather_rows(const uint8_t* __restrict__ ks, const uint8_t* __restrict__ vs,
                             int64_t ld_b, const int64_t* __restrict__ rows, int64_t first_row,
                             int64_t n, int64_t row_vecs, uint8_t* __restrict__ ko,
                             uint8_t* __restrict__ vo, int64_t row_b) {
-  const int64_t total = n * row_vecs;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const bool is_v = i >= total;
-    const int64_t e = is_v ? i - total : i;
-    const int64_t r = e / row_vecs, c = e - r * row_vecs;
-    const int64_t src_r = rows ? rows[r] : first_row + r;
-    const uint4 v = ld_nc((is_v ? vs : ks) + src_r * ld_b + c * 16);
-    *reinterpret_cast<uint4*>((is_v ? vo : ko) + r * row_b + c * 16) = v;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * n;
+       u += n_warps) {
+    const bool is_v = u >= n;
+    const int64_t i = is_v ? u - n : u;
+    const int64_t src_r = rows ? rows[i] : first_row + i;
+    copy_row<8>((is_v ? vs : ks) + src_r * ld_b, (is_v ? vo : ko) + i * row_b, row_vecs, lane);
   }
 }
 
@@ -189,14 +205,14 @@ int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf1
     const int64_t rv = width / 8;
     auto* k = static_cast<__nv_bfloat16*>(kd) + dst_row * dst_ld;
     auto* v = static_cast<__nv_bfloat16*>(vd) + dst_row * dst_ld;
-    append_f32_bf16<<<grid_for(2 * t * rv, threads), threads, 0, st>>>(
+    append_f32_bf16<<<grid_for(2 * t * 32, threads), threads, 0, st>>>(
         static_cast<const float*>(ks), static_cast<const float*>(vs), src_ld, k, v, dst_ld, t, rv);
   } else {
     const int esz = dst_bf16 ? 2 : 4;
     const int64_t rv = width * esz / 16;
     auto* k = static_cast<uint8_t*>(kd) + dst_row * dst_ld * esz;
     auto* v = static_cast<uint8_t*>(vd) + dst_row * dst_ld * esz;
-    append_same<<<grid_for(2 * t * rv, threads), threads, 0, st>>>(
+    append_same<<<grid_for(2 * t * 32, threads), threads, 0, st>>>(
         static_cast<const uint8_t*>(ks), static_cast<const uint8_t*>(vs), src_ld * esz, k, v,
         dst_ld * esz, t, rv);
   }
@@ -208,7 +224,7 @@ int kv_gather_launch(const void* ks, const void* vs, int64_t ld, int esz, const 
                      cudaStream_t st) {
   const int threads = 256;
   const int64_t rv = width * esz / 16;
-  gather_rows<<<grid_for(2 * n * rv, threads), threads, 0, st>>>(
+  gather_rows<<<grid_for(2 * n * 32, threads), threads, 0, st>>>(
       static_cast<const uint8_t*>(ks), static_cast<const uint8_t*>(vs), ld * esz, rows, first_row,
       n, rv, static_cast<uint8_t*>(ko), static_cast<uint8_t*>(vo), width * esz);
   return (int)cudaGetLastError();
