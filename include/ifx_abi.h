@@ -176,6 +176,13 @@ int ifx_ulysses_pack(const void* src, int64_t n, int64_t groups, int64_t world, 
 int ifx_ulysses_unpack(const void* src, int64_t n, int64_t groups, int64_t world, int64_t chunk,
                        int type, void* dst, int64_t dst_ld, void* stream);
 
+/* Initial block noise, host side (engine.py:280-282): writes the first n values of
+ * np.random.default_rng([seed, chunk]).standard_normal(...).astype(float32) into `out`
+ * (host memory, e.g. pinned), bit-identically, using `threads` host threads (0 = all).
+ * pcg_state = {state_hi, state_lo, inc_hi, inc_lo} of the seeded PCG64 bit generator
+ * (Generator.bit_generator.state["state"]). Ziggurat = numpy 2.3's own routine. */
+int ifx_noise_normal_f32(const uint64_t pcg_state[4], int64_t n, float* out, int threads);
+
 #ifdef __cplusplus
 }
 #endif

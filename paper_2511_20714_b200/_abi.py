@@ -41,6 +41,7 @@ EXPORTS = (
     "ifx_kv_append", "ifx_kv_gather",
     "ifx_attn_fwd", "ifx_attn_workspace_bytes",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_ulysses_pack", "ifx_ulysses_unpack",
+    "ifx_noise_normal_f32",
 )
 
 
@@ -101,6 +102,7 @@ def lib() -> ctypes.CDLL:
             L.ifx_rope_qk.argtypes = [P, I64, I64, I64, I64, I64, I64, I64, P, P, I64, P]
             L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]
             L.ifx_ulysses_unpack.argtypes = [P, I64, I64, I64, I64, ctypes.c_int, P, I64, P]
+            L.ifx_noise_normal_f32.argtypes = [ctypes.POINTER(ctypes.c_uint64), I64, P, ctypes.c_int]
             _lib = L
     return _lib
 

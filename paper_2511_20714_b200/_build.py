@@ -17,7 +17,16 @@ OUT = os.path.join(PKG, "libinferix_b200.so")
 OBJ = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["attn_fwd_sm100.cu", "kv_ops.cu", "abi.cpp", "pagetable.cpp"]
+SOURCES = ["attn_fwd_sm100.cu", "kv_ops.cu", "abi.cpp", "pagetable.cpp", "noise_host.cpp"]
+
+
+def _npyrandom() -> str:
+    """numpy's static distributions library (ziggurat normal), linked for bit-exact noise."""
+    import numpy.random
+    path = os.path.join(os.path.dirname(numpy.random.__file__), "lib", "libnpyrandom.a")
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} missing (numpy 2.3 wheel layout expected)")
+    return path
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", *os.environ.get("IFX_NVCC_EXTRA", "").split(), "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-I", os.path.join(ROOT, "include")]
 
@@ -46,8 +55,8 @@ def build(verbose: bool = False) -> str:
         objs = list(ex.map(_compile, SOURCES))
     if os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(o) for o in objs):
         return OUT
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-lcuda" if False else "-lcudart_static",
-           "-Xcompiler", "-fPIC"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, _npyrandom(), "-lcudart_static", "-Xlinker", "--exclude-libs,ALL",
+           "-lm", "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

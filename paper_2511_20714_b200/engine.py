@@ -20,8 +20,10 @@ K2 page write on the clean pass, fp32 residual stream (GEMMs with fp32 output).
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 import math
+import os
 import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -30,6 +32,7 @@ from typing import Callable
 import numpy as np
 import torch
 
+from . import _abi
 from ._device import attn_fwd, require_cuda, rms_bf16, rope_qk
 from .errors import ConfigError, DimensionError
 from .kvcache import CROSS_ATTN, SELF_ATTN, KvCache, KvConfig
@@ -273,8 +276,25 @@ def _init_noise_pinned(cfg: ModelConfig, seed: int, chunk_index: int) -> torch.T
     """_init_noise into pinned host memory (async H2D). Same float64 draw + fp32 cast as
     engine.py:280-282, so the values are bit-identical."""
     out = torch.empty((cfg.block_len, cfg.model_dim), dtype=torch.float32, pin_memory=True)
-    rng = np.random.default_rng([seed, chunk_index])
-    np.copyto(out.numpy(), rng.standard_normal((cfg.block_len, cfg.model_dim)), casting="same_kind")
+    host_normal_f32(np.random.default_rng([seed, chunk_index]), out)
+    return out
+
+
+def host_normal_f32(rng: np.random.Generator, out: torch.Tensor, threads: int | None = None) -> torch.Tensor:
+    """out[:] = rng.standard_normal(out.shape).astype(float32), bit for bit, on all host
+    cores (csrc/noise_host.cpp: parallel parse of the PCG64 stream with numpy's own
+    ziggurat). `rng` must be freshly seeded; its state is not advanced."""
+    st = rng.bit_generator.state
+    if st["bit_generator"] != "PCG64" or st["has_uint32"]:
+        raise ConfigError("host_normal_f32 needs a freshly seeded PCG64 generator")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    m = (1 << 64) - 1
+    words = (ctypes.c_uint64 * 4)(s >> 64, s & m, inc >> 64, inc & m)
+    if threads is None:
+        threads = max(1, (os.cpu_count() or 2) - 1)  # leave a core to the launching thread
+    if out.dtype != torch.float32 or not out.is_contiguous() or out.is_cuda:
+        raise DimensionError("host_normal_f32 writes a contiguous host float32 tensor")
+    _abi.check(_abi.lib().ifx_noise_normal_f32(words, out.numel(), out.data_ptr(), threads), "noise")
     return out
 
 
