@@ -46,9 +46,8 @@ int ifx_version(void);
 
 /* =====================================================================================
  * Page table: bit-exact bookkeeping of KvCache (kvcache.py:105-404), host C++.
- * Data lives in caller-owned device slabs addressed by stream position;
- * the page table decides ids, tiers, LRU, eviction and block entries exactly as the
- * reference does.
+ * It decides ids, tiers, LRU, eviction and block entries exactly as the reference does,
+ * and the physical slot of every page in the device / pinned-host pools (below).
  * ===================================================================================*/
 typedef struct ifx_pagetable ifx_pagetable;
 
@@ -87,20 +86,58 @@ int ifx_pt_stats(const ifx_pagetable* pt, int64_t* out, int64_t out_cap);
  * *out_len receives the needed length; call with out=NULL to size. */
 int ifx_pt_snapshot(const ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* out_len);
 
+/* ---- physical placement (B200): every page owns a slot of page_len rows in the device
+ * pool (tier device) or the mapped pinned host pool (tier host) of its kind. Tier changes
+ * made by a call (restore-on-read, LRU demotion, offload) are logged as page moves. */
+
+/* Drain the logged page moves as records of 5 int64 (epoch, kind, dir, device slot, host
+ * slot); dir 0 = device -> host, 1 = host -> device. Records are in execution order: per
+ * logging call, all dir-0 moves then all dir-1 moves (each group is hazard-free, so it is
+ * one ifx_kv_move_pages launch). out == NULL: only *n_records is set, nothing drained. */
+int ifx_pt_drain_moves(ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* n_records);
+/* slots ever used per pool: out4[kind*2 + tier] (tier 0 device, 1 host) */
+int ifx_pt_pool_extent(const ifx_pagetable* pt, int64_t* out4);
+/* Slot codes of the pages covering tokens [start, end) of a stream (within its stored
+ * pages, which may begin below the addressable base after window eviction), in order:
+ * code >= 0 = device slot, code < 0 = host slot -1-code. *first_token = start token of the
+ * first page (page k covers [first_token + k*page_len, ...)); out == NULL sizes *n. */
+int ifx_pt_slots(ifx_pagetable* pt, int64_t layer, int kind, int64_t start, int64_t end,
+                 int32_t* out, int64_t cap, int64_t* first_token, int64_t* n);
+
 /* =====================================================================================
- * KV data kernels (HBM-bound)
+ * KV data kernels (HBM-bound) over the two pools
  * ===================================================================================*/
-/* K2 — page write for KvCache.append_block (kvcache.py:215-218): copy t rows of K and V
- * (src row stride in elements) into slab rows [dst_row, dst_row + t). 128-bit vectorised.
- * src/dst types: F32->F32, F32->BF16, BF16->BF16. */
+typedef struct ifx_kv_pool {
+  void* dev_k;    /* device pool [device slots * page_len, width] */
+  void* dev_v;
+  void* host_k;   /* mapped pinned host pool [host slots * page_len, width] (ifx_host_alloc) */
+  void* host_v;
+  int64_t width;  /* elements per row */
+  int64_t page_len;
+  int type;       /* IFX_F32 or IFX_BF16 */
+} ifx_kv_pool;
+
+/* K2 — page write for KvCache.append_block (kvcache.py:215-218): rows [0, t) of K and V
+ * (src row stride in elements) are tokens [token0, token0 + t) of a stream whose pages,
+ * starting at first_token, have the slot codes `slots` (device int32 array, ifx_pt_slots).
+ * 128-bit vectorised; src/pool types F32->F32, F32->BF16, BF16->BF16. */
 int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_type,
-                  void* k_slab, void* v_slab, int64_t slab_ld, int slab_type, int64_t dst_row,
-                  int64_t t, int64_t width, void* stream);
-/* K7 — gather for fetch_range / fetch_indices (kvcache.py:303-353): out[i] =
- * slab[rows[i]] (rows==NULL: rows are first_row + i). Same dtype in and out. */
-int ifx_kv_gather(const void* k_slab, const void* v_slab, int64_t slab_ld, int type,
-                  const int64_t* rows, int64_t first_row, int64_t n, int64_t width,
-                  void* k_out, void* v_out, void* stream);
+                  const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
+                  int64_t token0, int64_t t, void* stream);
+/* K7 — gather for fetch_range / fetch_indices (kvcache.py:303-353): out row i = token
+ * tokens[i] (device int64 array) or, tokens == NULL, token0 + i. Same dtype as the pool. */
+int ifx_kv_gather(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
+                  const int64_t* tokens, int64_t token0, int64_t n, void* k_out, void* v_out,
+                  void* stream);
+/* K6 — whole-page copies between the pools (tier moves of ifx_pt_drain_moves, staging of
+ * host pages for attention): moves = device int64 [n][2] (device slot, host slot);
+ * dir 0 device -> host, 1 host -> device. */
+int ifx_kv_move_pages(const ifx_kv_pool* pool, const int64_t* moves, int64_t n, int dir,
+                      void* stream);
+/* pinned host memory mapped into the device address space (cudaHostAllocMapped; under UVA
+ * the device address equals the host address) for the host pools */
+int ifx_host_alloc(int64_t bytes, void** out);
+int ifx_host_free(void* p);
 
 /* =====================================================================================
  * K1 — fused attention of a block's queries over [cached context ∥ the block's own K/V]
@@ -139,6 +176,19 @@ typedef struct ifx_attn_params {
    * the denominator relative to it, so callers can merge partials (attention.py:157-173) */
   float* row_max;
   float* row_sum;
+  /* paged context: when ctx_slots != NULL, k_ctx/v_ctx are device pools [ctx_rows, width]
+   * of ctx_page_len-row slots (ifx_kv_pool.dev_k/dev_v) and the context is tokens
+   * [ctx_row0, ctx_row0 + n_ctx) of a stream whose pages, from ctx_first_token on, are in
+   * slots ctx_slots[] (device int32): code c >= 0 is slot c of the pool, c < 0 is slot
+   * -1-c of the staging pool k_stage/v_stage [stage_rows, width] (same row stride), where
+   * the caller copied host-tier pages (ifx_kv_move_pages). ctx_page_len must divide 128
+   * and be a multiple of 8 (whole 1 KB swizzle atoms per TMA box). */
+  const int32_t* ctx_slots;
+  int64_t ctx_page_len;
+  int64_t ctx_first_token;
+  const void* k_stage;
+  const void* v_stage;
+  int64_t stage_rows;
   /* optional device scratch for split-KV (size from ifx_attn_workspace_bytes). When given
    * and (query tiles x heads) would leave the SMs under-filled (e.g. a Ulysses rank holding
    * few heads), the key range is split across CTAs and merged by a combine kernel

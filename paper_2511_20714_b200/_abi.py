@@ -37,12 +37,22 @@ EXPORTS = (
     "ifx_last_error", "ifx_version",
     "ifx_pt_create", "ifx_pt_destroy", "ifx_pt_append", "ifx_pt_offload", "ifx_pt_evict_window",
     "ifx_pt_clear_cross", "ifx_pt_touch_range", "ifx_pt_touch_indices", "ifx_pt_range",
-    "ifx_pt_stats", "ifx_pt_snapshot",
-    "ifx_kv_append", "ifx_kv_gather",
+    "ifx_pt_stats", "ifx_pt_snapshot", "ifx_pt_drain_moves", "ifx_pt_pool_extent", "ifx_pt_slots",
+    "ifx_kv_append", "ifx_kv_gather", "ifx_kv_move_pages", "ifx_host_alloc", "ifx_host_free",
     "ifx_attn_fwd", "ifx_attn_workspace_bytes",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_ulysses_pack", "ifx_ulysses_unpack",
     "ifx_noise_normal_f32",
 )
+
+
+class KvPool(ctypes.Structure):
+    """Mirror of `ifx_kv_pool` (include/ifx_abi.h)."""
+
+    _fields_ = [
+        ("dev_k", ctypes.c_void_p), ("dev_v", ctypes.c_void_p),
+        ("host_k", ctypes.c_void_p), ("host_v", ctypes.c_void_p),
+        ("width", ctypes.c_int64), ("page_len", ctypes.c_int64), ("type", ctypes.c_int),
+    ]
 
 
 class AttnParams(ctypes.Structure):
@@ -58,6 +68,9 @@ class AttnParams(ctypes.Structure):
         ("heads", ctypes.c_int64), ("head_dim", ctypes.c_int64), ("scale", ctypes.c_float),
         ("mask", ctypes.c_void_p), ("mask_ld", ctypes.c_int64),
         ("row_max", ctypes.c_void_p), ("row_sum", ctypes.c_void_p),
+        ("ctx_slots", ctypes.c_void_p), ("ctx_page_len", ctypes.c_int64),
+        ("ctx_first_token", ctypes.c_int64),
+        ("k_stage", ctypes.c_void_p), ("v_stage", ctypes.c_void_p), ("stage_rows", ctypes.c_int64),
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_int64),
     ]
 
@@ -94,8 +107,15 @@ def lib() -> ctypes.CDLL:
             L.ifx_pt_range.argtypes = [P, I64, ctypes.c_int, PI64, PI64]
             L.ifx_pt_stats.argtypes = [P, PI64, I64]
             L.ifx_pt_snapshot.argtypes = [P, PI64, I64, PI64]
-            L.ifx_kv_append.argtypes = [P, P, I64, ctypes.c_int, P, P, I64, ctypes.c_int, I64, I64, I64, P]
-            L.ifx_kv_gather.argtypes = [P, P, I64, ctypes.c_int, P, I64, I64, I64, P, P, P]
+            L.ifx_pt_drain_moves.argtypes = [P, PI64, I64, PI64]
+            L.ifx_pt_pool_extent.argtypes = [P, PI64]
+            L.ifx_pt_slots.argtypes = [P, I64, ctypes.c_int, I64, I64, P, I64, PI64, PI64]
+            PPOOL = ctypes.POINTER(KvPool)
+            L.ifx_kv_append.argtypes = [P, P, I64, ctypes.c_int, PPOOL, P, I64, I64, I64, P]
+            L.ifx_kv_gather.argtypes = [PPOOL, P, I64, P, I64, I64, P, P, P]
+            L.ifx_kv_move_pages.argtypes = [PPOOL, P, I64, ctypes.c_int, P]
+            L.ifx_host_alloc.argtypes = [I64, ctypes.POINTER(P)]
+            L.ifx_host_free.argtypes = [P]
             L.ifx_attn_fwd.argtypes = [ctypes.POINTER(AttnParams), P]
             L.ifx_attn_workspace_bytes.argtypes = [ctypes.POINTER(AttnParams), PI64]
             L.ifx_rms_bf16.argtypes = [P, I64, I64, P, ctypes.c_float, P, P, P]

@@ -73,11 +73,16 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
              cur_k: torch.Tensor | None = None, cur_v: torch.Tensor | None = None,
              scale: float | None = None, mask: torch.Tensor | None = None,
              row_max: torch.Tensor | None = None, row_sum: torch.Tensor | None = None,
-             split_kv: bool = True, stream=None) -> torch.Tensor:
+             split_kv: bool = True, stream=None, ctx_slots: torch.Tensor | None = None,
+             page_len: int = 0, first_token: int = 0, stage_k: torch.Tensor | None = None,
+             stage_v: torch.Tensor | None = None) -> torch.Tensor:
     """Enqueue K1 (attn_fwd_sm100.cu): out = softmax(q [ctx∥cur]^T * scale) [ctx∥cur].
 
-    q/out: [n_q, heads*head_dim] bf16 (row-strided views allowed). ctx_*: slabs whose rows
-    [ctx_row0, ctx_row0+n_ctx) are the cached keys. cur_*: [n_cur, heads*head_dim] views.
+    q/out: [n_q, heads*head_dim] bf16 (row-strided views allowed). cur_*: [n_cur,
+    heads*head_dim] views. Context, contiguous: rows [ctx_row0, ctx_row0+n_ctx) of ctx_k/v.
+    Paged (ctx_slots given): ctx_k/v are the KV pool, the context is tokens [ctx_row0,
+    ctx_row0+n_ctx) whose pages from first_token on sit in slot codes ctx_slots (int32
+    device tensor; codes < 0 address stage_k/v).
     """
     p = _abi.AttnParams()
     p.q, p.q_ld, p.n_q = q.data_ptr(), row_ld(q), q.shape[0]
@@ -85,6 +90,10 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
         p.k_ctx, p.v_ctx = ctx_k.data_ptr(), ctx_v.data_ptr()
         p.ctx_ld, p.ctx_rows = row_ld(ctx_k), ctx_k.shape[0]
         p.ctx_row0, p.n_ctx = ctx_row0, n_ctx
+        if ctx_slots is not None:
+            p.ctx_slots, p.ctx_page_len, p.ctx_first_token = ctx_slots.data_ptr(), page_len, first_token
+            if stage_k is not None:
+                p.k_stage, p.v_stage, p.stage_rows = stage_k.data_ptr(), stage_v.data_ptr(), stage_k.shape[0]
     if cur_k is not None and cur_k.shape[0] > 0:
         p.k_cur, p.v_cur = cur_k.data_ptr(), cur_v.data_ptr()
         p.cur_ld, p.n_cur = row_ld(cur_k), cur_k.shape[0]

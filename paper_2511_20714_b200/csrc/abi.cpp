@@ -42,8 +42,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// bf16 matrix [rows, cols] with row stride ld (elements); box = 64 cols x 128 rows, SW128.
-static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+// bf16 matrix [rows, cols] with row stride ld (elements); box = 64 cols x box_rows, SW128.
+static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                    int box_rows = 128) {
   std::memset(m, 0, sizeof(*m));
   if (base == nullptr || rows <= 0) return IFX_OK;  // unused segment
   auto fn = encode_fn();
@@ -52,7 +53,7 @@ static int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols
     return fail(IFX_EDIM, "TMA operands need 16-byte aligned base and row stride");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -72,8 +73,17 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
     return fail(IFX_EDIM, "bad attention sizes");
   if (p->n_ctx + p->n_cur == 0 && p->n_q > 0) return fail(IFX_EMASK, "query row with no allowed key");
   if (p->n_q == 0) return IFX_OK;
-  if (p->n_ctx > 0 && p->ctx_row0 + p->n_ctx > p->ctx_rows)
+  const bool paged = p->ctx_slots != nullptr && p->n_ctx > 0;
+  if (paged) {
+    const int64_t pl = p->ctx_page_len;
+    if (pl < 8 || pl > 128 || 128 % pl || pl % 8)
+      return fail(IFX_EUNSUPPORTED, "paged attention needs page_len in {8, 16, 32, 64, 128}");
+    if (p->ctx_row0 < p->ctx_first_token) return fail(IFX_ERANGE, "context before its first page");
+    if (p->mask != nullptr) return fail(IFX_EUNSUPPORTED, "dense masks need a contiguous context");
+    if (p->ctx_rows % pl) return fail(IFX_EDIM, "pool rows must be whole slots");
+  } else if (p->n_ctx > 0 && p->ctx_row0 + p->n_ctx > p->ctx_rows) {
     return fail(IFX_ERANGE, "context rows outside the slab");
+  }
   const int64_t width = p->heads * p->head_dim;
   if (p->n_q > INT32_MAX || p->ctx_rows > INT32_MAX || p->n_cur > INT32_MAX)
     return fail(IFX_EDIM, "attention extents must fit int32");
@@ -82,8 +92,14 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   int rc;
   if ((rc = make_map(&a.tm_q, p->q, p->n_q, width, p->q_ld))) return rc;
   if (p->n_ctx > 0) {
-    if ((rc = make_map(&a.tm_kc, p->k_ctx, p->ctx_rows, width, p->ctx_ld))) return rc;
-    if ((rc = make_map(&a.tm_vc, p->v_ctx, p->ctx_rows, width, p->ctx_ld))) return rc;
+    const int box = paged ? (int)p->ctx_page_len : 128;
+    if ((rc = make_map(&a.tm_kc, p->k_ctx, p->ctx_rows, width, p->ctx_ld, box))) return rc;
+    if ((rc = make_map(&a.tm_vc, p->v_ctx, p->ctx_rows, width, p->ctx_ld, box))) return rc;
+    if (paged && p->k_stage != nullptr && p->stage_rows > 0) {
+      if (p->stage_rows % p->ctx_page_len) return fail(IFX_EDIM, "staging rows must be whole slots");
+      if ((rc = make_map(&a.tm_ks, p->k_stage, p->stage_rows, width, p->ctx_ld, box))) return rc;
+      if ((rc = make_map(&a.tm_vs, p->v_stage, p->stage_rows, width, p->ctx_ld, box))) return rc;
+    }
   }
   if (p->n_cur > 0) {
     if ((rc = make_map(&a.tm_kn, p->k_cur, p->n_cur, width, p->cur_ld))) return rc;
@@ -93,6 +109,15 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   a.n_ctx = (int)p->n_ctx;
   a.n_cur = (int)p->n_cur;
   a.ctx_row0 = (int)p->ctx_row0;
+  if (paged) {
+    const int64_t lo = p->ctx_row0 - p->ctx_first_token;
+    if (lo + p->n_ctx > INT32_MAX) return fail(IFX_EDIM, "attention extents must fit int32");
+    a.ctx_slots = p->ctx_slots;
+    a.ctx_page_len = (int)p->ctx_page_len;
+    a.ctx_lo = (int)lo;
+    a.n_ctx = (int)(lo + p->n_ctx);  // rows from the first page's start
+    a.ctx_row0 = 0;
+  }
   a.scale_log2 = p->scale * 1.4426950408889634f;
   a.o = static_cast<__nv_bfloat16*>(p->o);
   a.o_ld = p->o_ld;
@@ -138,7 +163,8 @@ int choose_splits(const ifx_attn_params* p) {
   const int sms = num_sms();
   const int64_t ctas = ((p->n_q + 127) / 128) * p->heads;
   if (ctas >= 3 * sms) return 1;
-  const int64_t tiles = (p->n_ctx + 127) / 128 + (p->n_cur + 127) / 128;
+  const int64_t lo = p->ctx_slots != nullptr ? p->ctx_row0 - p->ctx_first_token : 0;
+  const int64_t tiles = (lo + p->n_ctx + 127) / 128 + (p->n_cur + 127) / 128;
   auto eff = [&](int s) {
     const double w = (double)(ctas * s) / sms;
     return w / std::ceil(w);
@@ -169,38 +195,80 @@ int ifx_attn_workspace_bytes(const ifx_attn_params* p, int64_t* bytes) {
   return IFX_OK;
 }
 
-int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_type, void* k_slab,
-                  void* v_slab, int64_t slab_ld, int slab_type, int64_t dst_row, int64_t t,
-                  int64_t width, void* stream) {
-  if (t < 0 || width <= 0) return ifx::fail(IFX_EDIM, "bad append sizes");
+static int check_pool(const ifx_kv_pool* p) {
+  if (p == nullptr || p->width <= 0 || p->page_len <= 0) return ifx::fail(IFX_EDIM, "bad pool");
+  const int esz = p->type == IFX_BF16 ? 2 : 4;
+  if ((p->width * esz) % 16) return ifx::fail(IFX_EDIM, "row width must be a multiple of 16 bytes");
+  if ((reinterpret_cast<uintptr_t>(p->dev_k) | reinterpret_cast<uintptr_t>(p->dev_v) |
+       reinterpret_cast<uintptr_t>(p->host_k) | reinterpret_cast<uintptr_t>(p->host_v)) & 15)
+    return ifx::fail(IFX_EDIM, "pools must be 16-byte aligned");
+  return IFX_OK;
+}
+
+int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_type,
+                  const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
+                  int64_t token0, int64_t t, void* stream) {
+  if (int rc = check_pool(pool)) return rc;
+  if (t < 0 || token0 < first_token) return ifx::fail(IFX_EDIM, "bad append sizes");
   if (t == 0) return IFX_OK;
-  if (src_type == IFX_BF16 && slab_type == IFX_F32)
+  if (src_type == IFX_BF16 && pool->type == IFX_F32)
     return ifx::fail(IFX_EUNSUPPORTED, "bf16 -> fp32 append not supported");
-  const int esz = slab_type == IFX_BF16 ? 2 : 4;
-  if ((width * esz) % 16 || (src_type == IFX_F32 && slab_type == IFX_BF16 && width % 8))
-    return ifx::fail(IFX_EDIM, "row width must be a multiple of 16 bytes");
   const int ssz = src_type == IFX_BF16 ? 2 : 4;
-  if ((reinterpret_cast<uintptr_t>(k_src) | reinterpret_cast<uintptr_t>(v_src) |
-       reinterpret_cast<uintptr_t>(k_slab) | reinterpret_cast<uintptr_t>(v_slab)) & 15 ||
-      (src_ld * ssz) % 16 || (slab_ld * esz) % 16)
+  if ((reinterpret_cast<uintptr_t>(k_src) | reinterpret_cast<uintptr_t>(v_src)) & 15 ||
+      (src_ld * ssz) % 16)
     return ifx::fail(IFX_EDIM, "append operands must be 16-byte aligned");
-  int e = ifx::kv_append_launch(k_src, v_src, src_ld, src_type == IFX_BF16, k_slab, v_slab,
-                                slab_ld, slab_type == IFX_BF16, dst_row, t, width,
+  int e = ifx::kv_append_launch(k_src, v_src, src_ld, src_type == IFX_BF16, pool->dev_k,
+                                pool->dev_v, pool->host_k, pool->host_v, pool->type == IFX_BF16,
+                                pool->width, pool->page_len, slots, token0 - first_token, t,
                                 static_cast<cudaStream_t>(stream));
   return ifx::cuda_fail(e, "kv_append launch");
 }
 
-int ifx_kv_gather(const void* k_slab, const void* v_slab, int64_t slab_ld, int type,
-                  const int64_t* rows, int64_t first_row, int64_t n, int64_t width, void* k_out,
-                  void* v_out, void* stream) {
-  if (n < 0 || width <= 0) return ifx::fail(IFX_EDIM, "bad gather sizes");
+int ifx_kv_gather(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
+                  const int64_t* tokens, int64_t token0, int64_t n, void* k_out, void* v_out,
+                  void* stream) {
+  if (int rc = check_pool(pool)) return rc;
+  if (n < 0) return ifx::fail(IFX_EDIM, "bad gather sizes");
   if (n == 0) return IFX_OK;
-  const int esz = type == IFX_BF16 ? 2 : 4;
-  if ((width * esz) % 16 || (slab_ld * esz) % 16)
-    return ifx::fail(IFX_EDIM, "row width must be a multiple of 16 bytes");
-  int e = ifx::kv_gather_launch(k_slab, v_slab, slab_ld, esz, rows, first_row, n, width, k_out,
-                                v_out, static_cast<cudaStream_t>(stream));
+  const int esz = pool->type == IFX_BF16 ? 2 : 4;
+  int e = ifx::kv_gather_launch(pool->dev_k, pool->dev_v, pool->host_k, pool->host_v, esz,
+                                pool->width, pool->page_len, slots, tokens,
+                                tokens ? first_token : token0 - first_token, n, k_out, v_out,
+                                static_cast<cudaStream_t>(stream));
   return ifx::cuda_fail(e, "kv_gather launch");
+}
+
+int ifx_kv_move_pages(const ifx_kv_pool* pool, const int64_t* moves, int64_t n, int dir,
+                      void* stream) {
+  if (int rc = check_pool(pool)) return rc;
+  if (n < 0 || (dir != 0 && dir != 1)) return ifx::fail(IFX_EDIM, "bad page move batch");
+  if (n == 0) return IFX_OK;
+  const int esz = pool->type == IFX_BF16 ? 2 : 4;
+  int e = ifx::kv_move_launch(pool->dev_k, pool->dev_v, pool->host_k, pool->host_v, esz,
+                              pool->width, pool->page_len, moves, n, dir,
+                              static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "kv_move_pages launch");
+}
+
+int ifx_host_alloc(int64_t bytes, void** out) {
+  *out = nullptr;
+  if (bytes <= 0) return IFX_OK;
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+  if (e != cudaSuccess) return ifx::cuda_fail((int)e, "cudaHostAlloc");
+  void* d = nullptr;
+  e = cudaHostGetDevicePointer(&d, p, 0);
+  if (e != cudaSuccess || d != p) {  // UVA: the mapped device address is the host address
+    cudaFreeHost(p);
+    return ifx::fail(IFX_ECUDA, "pinned host pool is not mapped at its host address (no UVA?)");
+  }
+  *out = p;
+  return IFX_OK;
+}
+
+int ifx_host_free(void* p) {
+  if (p == nullptr) return IFX_OK;
+  return ifx::cuda_fail((int)cudaFreeHost(p), "cudaFreeHost");
 }
 
 int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec, float t,

@@ -106,23 +106,33 @@ struct Layout {
 };
 
 struct Tile {
-  int seg, row, kv0, valid;
+  int seg, row, kv0, lo, valid;  // keys [lo, valid) of the tile are visible
 };
 
 __device__ __forceinline__ Tile tile_of(const AttnKernelArgs& a, int j, int n0) {
   Tile t;
   if (j < n0) {
     t.seg = 0;
-    t.row = a.ctx_row0 + j * BN;
+    t.row = a.ctx_row0 + j * BN;  // paged: row relative to the first page (ctx_row0 = 0)
     t.kv0 = j * BN;
+    t.lo = j == 0 ? a.ctx_lo : 0;
     t.valid = min(BN, a.n_ctx - j * BN);
   } else {
     t.seg = 1;
     t.row = (j - n0) * BN;
     t.kv0 = a.n_ctx + (j - n0) * BN;
+    t.lo = 0;
     t.valid = min(BN, a.n_cur - (j - n0) * BN);
   }
   return t;
+}
+
+// paged context: slot of page `lane` of key tile j (clamped to the last page: rows past the
+// context are loaded from a finite page and masked)
+__device__ __forceinline__ int32_t tile_slot(const AttnKernelArgs& a, int j, int lane) {
+  const int n_pages = (a.n_ctx + a.ctx_page_len - 1) / a.ctx_page_len;
+  const int pg = min(j * (BN / a.ctx_page_len) + lane, n_pages - 1);
+  return __ldg(a.ctx_slots + pg);
 }
 
 template <int HD>
@@ -185,11 +195,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (warp == 0) {
     // ===================== TMA producer =====================
-    if (elect_one()) {
+    // lane 0 drives the ring; for a paged context tile, lanes 0..ppt-1 each fetch one page
+    // (a page_len-row box per 64-column chunk) from the slot the page table assigned
+    const bool paged = a.ctx_slots != nullptr;
+    const int ppt = paged ? BN / a.ctx_page_len : 1;
+    const int prow_b = paged ? a.ctx_page_len * 128 : 0;  // smem bytes of one page box
+    const bool leader = lane == 0;
+    if (leader) {
       tma_prefetch_desc(&a.tm_q);
       if (n0 > 0) {
         tma_prefetch_desc(&a.tm_kc);
         tma_prefetch_desc(&a.tm_vc);
+      }
+      if (n0 > 0 && paged) {
+        tma_prefetch_desc(&a.tm_ks);
+        tma_prefetch_desc(&a.tm_vs);
       }
       if (n_total > n0) {
         tma_prefetch_desc(&a.tm_kn);
@@ -198,19 +218,50 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_expect_tx(q_full, L::Q_BYTES);
       for (int c = 0; c < L::KCH; ++c)
         tma_load_2d(sQ + c * BM * 128, &a.tm_q, q_full, head * HD + c * 64, q0);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int s = j % NS;
-        const uint32_t ph = (j / NS) & 1;
-        const Tile t = tile_of(a, t0 + j, n0);
-        const CUtensorMap* mk = t.seg == 0 ? &a.tm_kc : &a.tm_kn;
-        const CUtensorMap* mv = t.seg == 0 ? &a.tm_vc : &a.tm_vn;
+    }
+    int32_t slot_next = (paged && n_tiles > 0 && t0 < n0 && lane < ppt) ? tile_slot(a, t0, lane) : 0;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j % NS;
+      const uint32_t ph = (j / NS) & 1;
+      const Tile t = tile_of(a, t0 + j, n0);
+      const int32_t slot = slot_next;
+      if (paged && j + 1 < n_tiles && t0 + j + 1 < n0 && lane < ppt)
+        slot_next = tile_slot(a, t0 + j + 1, lane);  // prefetch: hides the table load
+      const bool by_page = paged && t.seg == 0;
+      const CUtensorMap* mk = t.seg == 0 ? &a.tm_kc : &a.tm_kn;
+      const CUtensorMap* mv = t.seg == 0 ? &a.tm_vc : &a.tm_vn;
+      if (leader) {
         mbar_wait(k_empty + s, ph ^ 1);
         mbar_expect_tx(k_full + s, L::KV_BYTES);
+      }
+      __syncwarp();
+      if (by_page) {
+        if (lane < ppt) {
+          const CUtensorMap* m = slot >= 0 ? &a.tm_kc : &a.tm_ks;
+          const int r = (slot >= 0 ? slot : -1 - slot) * a.ctx_page_len;
+          for (int c = 0; c < L::KCH; ++c)
+            tma_load_2d(sK + s * L::KV_BYTES + c * BN * 128 + lane * prow_b, m, k_full + s,
+                        head * HD + c * 64, r);
+        }
+      } else if (leader) {
         for (int c = 0; c < L::KCH; ++c)
           tma_load_2d(sK + s * L::KV_BYTES + c * BN * 128, mk, k_full + s, head * HD + c * 64,
                       t.row);
+      }
+      if (leader) {
         mbar_wait(v_empty + s, ph ^ 1);
         mbar_expect_tx(v_full + s, L::KV_BYTES);
+      }
+      __syncwarp();
+      if (by_page) {
+        if (lane < ppt) {
+          const CUtensorMap* m = slot >= 0 ? &a.tm_vc : &a.tm_vs;
+          const int r = (slot >= 0 ? slot : -1 - slot) * a.ctx_page_len;
+          for (int c = 0; c < L::KCH; ++c)
+            tma_load_2d(sV + s * L::KV_BYTES + c * BN * 128 + lane * prow_b, m, v_full + s,
+                        head * HD + c * 64, r);
+        }
+      } else if (leader) {
         for (int c = 0; c < L::KCH; ++c)
           tma_load_2d(sV + s * L::KV_BYTES + c * BN * 128, mv, v_full + s, head * HD + c * 64,
                       t.row);
@@ -306,11 +357,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_before();
       mbar_arrive(s_empty + b);
 
-      const bool full = (t.valid == BN) && mrow == nullptr;
+      const bool full = (t.valid == BN) && t.lo == 0 && mrow == nullptr;
       if (!full) {
 #pragma unroll
         for (int i = 0; i < HALF; ++i) {
-          bool ok = c0 + i < t.valid;
+          bool ok = c0 + i < t.valid && c0 + i >= t.lo;
           if (ok && mrow != nullptr) ok = mrow[t.kv0 + c0 + i] != 0;
           if (!ok) sv[i] = -INFINITY;
         }

@@ -10,12 +10,21 @@ namespace ifx {
 
 struct AttnKernelArgs {
   CUtensorMap tm_q;   // Q       [n_q, H*dh]   box 64 x 128, SW128
-  CUtensorMap tm_kc;  // K slab  [rows, H*dh]
-  CUtensorMap tm_vc;  // V slab
+  CUtensorMap tm_kc;  // K context [rows, H*dh] (contiguous: box 128 rows; paged: box page_len)
+  CUtensorMap tm_vc;  // V context
+  CUtensorMap tm_ks;  // paged only: K staging pool (slot codes < 0), box page_len
+  CUtensorMap tm_vs;  // V staging pool
   CUtensorMap tm_kn;  // K of the current block [n_cur, H*dh]
   CUtensorMap tm_vn;  // V of the current block
   int n_q, n_ctx, n_cur, ctx_row0;
   float scale_log2;   // scale * log2(e)
+  // paged context (ctx_slots != nullptr): context rows [0, n_ctx) counted from the start of
+  // the first page; row r lives in slot code c = ctx_slots[r / page_len]: c >= 0 slot c of
+  // the pool (tm_kc/tm_vc), c < 0 slot -1-c of the staging pool (tm_ks/tm_vs); rows
+  // [0, ctx_lo) precede the addressable window and are masked
+  int ctx_lo;
+  const int32_t* ctx_slots;
+  int ctx_page_len;
   int pad_;
   __nv_bfloat16* o;
   int64_t o_ld;

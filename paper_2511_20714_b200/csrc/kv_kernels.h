@@ -5,12 +5,14 @@
 #include <cstdint>
 
 namespace ifx {
-int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf16, void* kd,
-                     void* vd, int64_t dst_ld, int dst_bf16, int64_t dst_row, int64_t t,
-                     int64_t width, cudaStream_t st);
-int kv_gather_launch(const void* ks, const void* vs, int64_t ld, int esz, const int64_t* rows,
-                     int64_t first_row, int64_t n, int64_t width, void* ko, void* vo,
-                     cudaStream_t st);
+int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf16, void* dk,
+                     void* dv, void* hk, void* hv, int pool_bf16, int64_t width, int64_t page_len,
+                     const int32_t* slots, int64_t rel0, int64_t t, cudaStream_t st);
+int kv_gather_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t width,
+                     int64_t page_len, const int32_t* slots, const int64_t* tokens, int64_t rel0,
+                     int64_t n, void* ko, void* vo, cudaStream_t st);
+int kv_move_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t width,
+                   int64_t page_len, const int64_t* moves, int64_t n, int dir, cudaStream_t st);
 int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
                float* x_out, void* y, cudaStream_t st);
 int rope_launch(void* qkv, int64_t rows, int64_t ld, int heads, int64_t head_stride, int pairs,

@@ -47,32 +47,56 @@ __device__ __forceinline__ void copy_row(const uint8_t* __restrict__ s, uint8_t*
   }
 }
 
-// same-type copy: rows [0, t) of K and V -> slab rows (dst already offset to the first row)
+// Pool addressing: a page slot code c >= 0 is device slot c, c < 0 is host slot -1-c; a
+// slot is page_len consecutive rows of `width` elements. Host pools are mapped pinned
+// memory, so the same kernels read and write both tiers (host traffic crosses PCIe).
+struct PoolPtrs {
+  uint8_t* dev_k;
+  uint8_t* dev_v;
+  uint8_t* host_k;
+  uint8_t* host_v;
+  int64_t row_b;  // bytes per row (= width * esz; rows are dense inside a slot)
+  int page_len;
+};
+
+__device__ __forceinline__ uint8_t* pool_row(const PoolPtrs& p, bool is_v, int32_t code,
+                                             int in_page) {
+  const int64_t r = (int64_t)(code >= 0 ? code : -1 - code) * p.page_len + in_page;
+  uint8_t* base = code >= 0 ? (is_v ? p.dev_v : p.dev_k) : (is_v ? p.host_v : p.host_k);
+  return base + r * p.row_b;
+}
+
+// K2 same-type: row r of K / V (token token0 + r) -> its page slot row
 __global__ void append_same(const uint8_t* __restrict__ ks, const uint8_t* __restrict__ vs,
-                            int64_t src_ld_b, uint8_t* __restrict__ kd, uint8_t* __restrict__ vd,
-                            int64_t dst_ld_b, int64_t t, int64_t row_vecs) {
+                            int64_t src_ld_b, PoolPtrs pool, const int32_t* __restrict__ slots,
+                            int64_t rel0, int64_t t, int64_t row_vecs) {
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * t;
        u += n_warps) {
     const bool is_v = u >= t;
     const int64_t r = is_v ? u - t : u;
-    copy_row<8>((is_v ? vs : ks) + r * src_ld_b, (is_v ? vd : kd) + r * dst_ld_b, row_vecs, lane);
+    const int64_t rel = rel0 + r;  // token - first page's start token
+    const int pg = (int)(rel / pool.page_len);
+    uint8_t* d = pool_row(pool, is_v, __ldg(slots + pg), (int)(rel - (int64_t)pg * pool.page_len));
+    copy_row<8>((is_v ? vs : ks) + r * src_ld_b, d, row_vecs, lane);
   }
 }
 // fp32 -> bf16: per 16-byte destination vector, 32 source bytes
 __global__ void append_f32_bf16(const float* __restrict__ ks, const float* __restrict__ vs,
-                                int64_t src_ld, __nv_bfloat16* __restrict__ kd,
-                                __nv_bfloat16* __restrict__ vd, int64_t dst_ld, int64_t t,
-                                int64_t row_vecs) {
+                                int64_t src_ld, PoolPtrs pool, const int32_t* __restrict__ slots,
+                                int64_t rel0, int64_t t, int64_t row_vecs) {
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * t;
        u += n_warps) {
     const bool is_v = u >= t;
     const int64_t r = is_v ? u - t : u;
+    const int64_t rel = rel0 + r;
+    const int pg = (int)(rel / pool.page_len);
     const float* srow = (is_v ? vs : ks) + r * src_ld;
-    __nv_bfloat16* drow = (is_v ? vd : kd) + r * dst_ld;
+    uint8_t* drow =
+        pool_row(pool, is_v, __ldg(slots + pg), (int)(rel - (int64_t)pg * pool.page_len));
     for (int64_t c = lane; c < row_vecs; c += 32) {
       const uint4 a = ld_nc(srow + c * 8), b = ld_nc(srow + c * 8 + 4);
       uint4 o;
@@ -80,24 +104,55 @@ __global__ void append_f32_bf16(const float* __restrict__ ks, const float* __res
       o.y = f2_to_bf2(__uint_as_float(a.z), __uint_as_float(a.w));
       o.z = f2_to_bf2(__uint_as_float(b.x), __uint_as_float(b.y));
       o.w = f2_to_bf2(__uint_as_float(b.z), __uint_as_float(b.w));
-      st_na(drow + c * 8, o);
+      st_na(drow + c * 16, o);
     }
   }
 }
 
-// K7: out[i] = slab[rows[i]] (rows == NULL: first_row + i), K and V
-__global__ void gather_rows(const uint8_t* __restrict__ ks, const uint8_t* __restrict__ vs,
-                            int64_t ld_b, const int64_t* __restrict__ rows, int64_t first_row,
-                            int64_t n, int64_t row_vecs, uint8_t* __restrict__ ko,
-                            uint8_t* __restrict__ vo, int64_t row_b) {
+// K7: out[i] = pool row of token tokens[i] (tokens == NULL: token0 + i), K and V; tokens
+// are given relative to the first page's start token
+__global__ void gather_rows(PoolPtrs pool, const int32_t* __restrict__ slots,
+                            const int64_t* __restrict__ tokens, int64_t rel0, int64_t n,
+                            int64_t row_vecs, uint8_t* __restrict__ ko, uint8_t* __restrict__ vo) {
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * n;
        u += n_warps) {
     const bool is_v = u >= n;
     const int64_t i = is_v ? u - n : u;
-    const int64_t src_r = rows ? rows[i] : first_row + i;
-    copy_row<8>((is_v ? vs : ks) + src_r * ld_b, (is_v ? vo : ko) + i * row_b, row_vecs, lane);
+    const int64_t rel = tokens ? tokens[i] - rel0 : rel0 + i;
+    const int pg = (int)(rel / pool.page_len);
+    const uint8_t* src =
+        pool_row(pool, is_v, __ldg(slots + pg), (int)(rel - (int64_t)pg * pool.page_len));
+    copy_row<8>(src, (is_v ? vo : ko) + i * pool.row_b, row_vecs, lane);
+  }
+}
+
+// K6: whole-page copies between the device and host pools (tier moves, staging). moves[i]
+// = (device slot, host slot); dir 0 device -> host, 1 host -> device. One warp per
+// (move, K|V, 4 KB piece) so a batch of large pages spreads over every SM.
+__global__ void move_pages(PoolPtrs pool, const int64_t* __restrict__ moves, int64_t n, int dir,
+                           int64_t page_vecs, int64_t piece_vecs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t pieces = (page_vecs + piece_vecs - 1) / piece_vecs;
+  const int64_t units = n * 2 * pieces;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t page_b = page_vecs * 16;
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < units;
+       u += n_warps) {
+    const int64_t piece = u % pieces;
+    const int64_t mv = u / pieces;
+    const int64_t m = mv >> 1;
+    const bool is_v = mv & 1;
+    const int64_t ds = moves[2 * m], hs = moves[2 * m + 1];
+    uint8_t* dev = (is_v ? pool.dev_v : pool.dev_k) + ds * page_b;
+    uint8_t* host = (is_v ? pool.host_v : pool.host_k) + hs * page_b;
+    const int64_t off = piece * piece_vecs * 16;
+    const int64_t nv = min(piece_vecs, page_vecs - piece * piece_vecs);
+    if (dir == 0)
+      copy_row<8>(dev + off, host + off, nv, lane);
+    else
+      copy_row<8>(host + off, dev + off, nv, lane);
   }
 }
 
@@ -197,36 +252,50 @@ int grid_for(int64_t work, int threads) {
 
 }  // namespace
 
-int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf16, void* kd,
-                     void* vd, int64_t dst_ld, int dst_bf16, int64_t dst_row, int64_t t,
-                     int64_t width, cudaStream_t st) {
+static PoolPtrs pool_ptrs(void* dk, void* dv, void* hk, void* hv, int64_t width, int esz,
+                          int64_t page_len) {
+  return PoolPtrs{static_cast<uint8_t*>(dk), static_cast<uint8_t*>(dv), static_cast<uint8_t*>(hk),
+                  static_cast<uint8_t*>(hv), width * esz, (int)page_len};
+}
+
+int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf16, void* dk,
+                     void* dv, void* hk, void* hv, int pool_bf16, int64_t width, int64_t page_len,
+                     const int32_t* slots, int64_t rel0, int64_t t, cudaStream_t st) {
   const int threads = 256;
-  if (!src_bf16 && dst_bf16) {
-    const int64_t rv = width / 8;
-    auto* k = static_cast<__nv_bfloat16*>(kd) + dst_row * dst_ld;
-    auto* v = static_cast<__nv_bfloat16*>(vd) + dst_row * dst_ld;
+  const PoolPtrs pool = pool_ptrs(dk, dv, hk, hv, width, pool_bf16 ? 2 : 4, page_len);
+  if (!src_bf16 && pool_bf16) {
     append_f32_bf16<<<grid_for(2 * t * 32, threads), threads, 0, st>>>(
-        static_cast<const float*>(ks), static_cast<const float*>(vs), src_ld, k, v, dst_ld, t, rv);
+        static_cast<const float*>(ks), static_cast<const float*>(vs), src_ld, pool, slots, rel0, t,
+        width / 8);
   } else {
-    const int esz = dst_bf16 ? 2 : 4;
-    const int64_t rv = width * esz / 16;
-    auto* k = static_cast<uint8_t*>(kd) + dst_row * dst_ld * esz;
-    auto* v = static_cast<uint8_t*>(vd) + dst_row * dst_ld * esz;
+    const int esz = pool_bf16 ? 2 : 4;
     append_same<<<grid_for(2 * t * 32, threads), threads, 0, st>>>(
-        static_cast<const uint8_t*>(ks), static_cast<const uint8_t*>(vs), src_ld * esz, k, v,
-        dst_ld * esz, t, rv);
+        static_cast<const uint8_t*>(ks), static_cast<const uint8_t*>(vs), src_ld * esz, pool, slots,
+        rel0, t, width * esz / 16);
   }
   return (int)cudaGetLastError();
 }
 
-int kv_gather_launch(const void* ks, const void* vs, int64_t ld, int esz, const int64_t* rows,
-                     int64_t first_row, int64_t n, int64_t width, void* ko, void* vo,
-                     cudaStream_t st) {
+int kv_gather_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t width,
+                     int64_t page_len, const int32_t* slots, const int64_t* tokens, int64_t rel0,
+                     int64_t n, void* ko, void* vo, cudaStream_t st) {
   const int threads = 256;
-  const int64_t rv = width * esz / 16;
+  const PoolPtrs pool = pool_ptrs(dk, dv, hk, hv, width, esz, page_len);
   gather_rows<<<grid_for(2 * n * 32, threads), threads, 0, st>>>(
-      static_cast<const uint8_t*>(ks), static_cast<const uint8_t*>(vs), ld * esz, rows, first_row,
-      n, rv, static_cast<uint8_t*>(ko), static_cast<uint8_t*>(vo), width * esz);
+      pool, slots, tokens, rel0, n, width * esz / 16, static_cast<uint8_t*>(ko),
+      static_cast<uint8_t*>(vo));
+  return (int)cudaGetLastError();
+}
+
+int kv_move_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t width,
+                   int64_t page_len, const int64_t* moves, int64_t n, int dir, cudaStream_t st) {
+  const int threads = 256;
+  const PoolPtrs pool = pool_ptrs(dk, dv, hk, hv, width, esz, page_len);
+  const int64_t page_vecs = page_len * width * esz / 16;
+  const int64_t piece = 256;  // 4 KB per warp task
+  const int64_t units = n * 2 * ((page_vecs + piece - 1) / piece);
+  move_pages<<<grid_for(units * 32, threads), threads, 0, st>>>(pool, moves, n, dir, page_vecs,
+                                                                piece);
   return (int)cudaGetLastError();
 }
 

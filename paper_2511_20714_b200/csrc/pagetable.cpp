@@ -20,6 +20,15 @@
 //   * The LRU index (ordered set keyed (last_access, stream, page id)) is only maintained
 //     while some page lives on the host tier; without host pages no restore can happen,
 //     so the common no-spill case touches pages in O(pages) with no tree updates.
+//   * Physical placement follows the tiers exactly: every page owns a SLOT in the device
+//     pool (tier 0) or the pinned host pool (tier 1) of its kind (self / cross; a slot is
+//     page_len rows). Tier changes inside one call (restore, demote) are logged as page
+//     moves and drained by the caller as two hazard-free batches executed in order: all
+//     device->host copies, then all host->device copies (K6, ifx_kv_move_pages). Within a
+//     call, host slots freed by a restore are only recycled at the drain (so no D2H of the
+//     batch overwrites a host page an H2D of the batch still has to read), and a page that
+//     is restored and demoted again (or the reverse) in the same call cancels its pending
+//     move instead of chaining a second one.
 //
 // Snapshot record (ifx_pt_snapshot), all int64:
 //   clock, next_page, next_block, device_used, host_used, n_streams,
@@ -27,6 +36,8 @@
 //               start_token, last_access
 //   n_blocks, per block (ascending id): id, layer, kind, start, end, chunk, n_pages, ids...
 
+#include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <cstring>
 #include <deque>
@@ -49,6 +60,55 @@ struct Page {
   int64_t start;
   int64_t last_access;
   int stream;
+  int64_t slot = -1;      // row block in the pool of (kind, tier)
+  int64_t pending = -1;   // index of this call's live move that brought it to its tier
+  int64_t prev_slot = -1; // the slot that move copies from (still holds the data)
+};
+
+// slot allocator of one (kind, tier) pool: LIFO free list + high-water mark; frees of
+// host slots made during a call are deferred to the drain (see header)
+struct SlotPool {
+  std::vector<int64_t> free_list;
+  std::vector<int64_t> deferred;
+  std::vector<char> is_deferred;
+  int64_t hwm = 0;
+  int64_t take() {
+    if (!free_list.empty()) {
+      int64_t s = free_list.back();
+      free_list.pop_back();
+      return s;
+    }
+    return hwm++;
+  }
+  void give(int64_t s) { free_list.push_back(s); }
+  void defer(int64_t s) {
+    if ((int64_t)is_deferred.size() <= s) is_deferred.resize(s + 1, 0);
+    is_deferred[s] = 1;
+    deferred.push_back(s);
+  }
+  bool reclaim(int64_t s) {  // take back a deferred slot (its data is still there)
+    if (s < (int64_t)is_deferred.size() && is_deferred[s]) {
+      is_deferred[s] = 0;
+      return true;
+    }
+    return false;
+  }
+  void flush() {
+    for (int64_t s : deferred)
+      if (s < (int64_t)is_deferred.size() && is_deferred[s]) {
+        is_deferred[s] = 0;
+        free_list.push_back(s);
+      }
+    deferred.clear();
+  }
+};
+
+struct Move {
+  int64_t epoch;  // the call that logged it: batches execute per call, in call order
+  int kind;
+  int dir;  // 0 device -> host (demote), 1 host -> device (restore)
+  int64_t dev_slot, host_slot;
+  bool live;
 };
 
 struct Stream {
@@ -76,7 +136,21 @@ struct ifx_pagetable {
   int64_t next_block = 0, next_page = 0, dev_used = 0, host_used = 0, clock = 0;
   bool lru_on = false;
   std::set<LruKey> lru;  // device pages, maintained only while host_used > 0
+  SlotPool pools[2][2];  // [kind][tier]
+  std::vector<Move> moves;
+  std::vector<Page*> pend_pages;  // pages with a move pending in the current call
+  int64_t epoch = 0;
   std::mutex mu;
+
+  // start of every mutating call: moves of earlier calls are final (they execute before
+  // this call's), host slots they freed may be recycled
+  void begin_call() {
+    epoch++;
+    for (Page* p : pend_pages) p->pending = -1;
+    pend_pages.clear();
+    for (auto& k : pools)
+      for (auto& t : k) t.flush();
+  }
 
   ~ifx_pagetable() {
     for (auto& kv : live) delete kv.second;
@@ -107,13 +181,15 @@ struct ifx_pagetable {
       return nullptr;
     }
     Page* p = new Page{next_page++, tier, 0, start, 0, s};
+    p->slot = pools[s & 1][tier].take();
     live[p->id] = p;
     if (tier == 0 && lru_on) lru.insert(key(p));
     lru_sync();
     return p;
   }
 
-  void release(Page* p) {
+  void release(Page* p) {  // no call leaves pending moves, so the slot is free at once
+    pools[p->stream & 1][p->tier].give(p->slot);
     if (p->tier == 0) {
       dev_used--;
       if (lru_on) lru.erase(key(p));
@@ -127,6 +203,22 @@ struct ifx_pagetable {
 
   void demote(Page* p) {  // device -> host
     if (lru_on) lru.erase(key(p));
+    const int k = p->stream & 1;
+    if (p->pending >= 0 && pools[k][1].reclaim(p->prev_slot)) {
+      // restored earlier in this call: its data never left the host slot it came from
+      moves[p->pending].live = false;
+      pools[k][0].give(p->slot);
+      p->slot = p->prev_slot;
+      p->pending = -1;
+    } else {
+      const int64_t hs = pools[k][1].take();
+      moves.push_back(Move{epoch, k, 0, p->slot, hs, true});
+      pools[k][0].give(p->slot);  // read by the D2H batch before any H2D may refill it
+      p->pending = (int64_t)moves.size() - 1;
+      p->prev_slot = p->slot;
+      p->slot = hs;
+      pend_pages.push_back(p);
+    }
     p->tier = 1;
     dev_used--;
     host_used++;
@@ -141,6 +233,22 @@ struct ifx_pagetable {
       Page* victim = live.at(std::get<2>(*lru.begin()));
       demote(victim);
     }
+    const int k = p->stream & 1;
+    const int64_t ds = pools[k][0].take();
+    if (p->pending >= 0 && ds == p->prev_slot) {
+      // demoted earlier in this call and its device slot is still unused: cancel the D2H
+      moves[p->pending].live = false;
+      pools[k][1].give(p->slot);
+      p->pending = -1;
+    } else {
+      // (a demotion earlier in this call, if any, stays live: D2H runs before H2D)
+      moves.push_back(Move{epoch, k, 1, ds, p->slot, true});
+      pools[k][1].defer(p->slot);
+      p->pending = (int64_t)moves.size() - 1;
+      p->prev_slot = p->slot;
+      pend_pages.push_back(p);
+    }
+    p->slot = ds;
     p->tier = 0;
     host_used--;
     dev_used++;
@@ -196,12 +304,14 @@ int ifx_pt_append(ifx_pagetable* pt, int64_t layer, int kind, int64_t t, int64_t
                   int64_t* out_block_id, int64_t* out_start, int64_t* out_written,
                   int64_t* out_pages, int64_t page_cap, int64_t* out_npages) {
   std::lock_guard<std::mutex> g(pt->mu);
+  pt->begin_call();
   *out_written = 0;
   if (t < 1) return ifx::fail(IFX_EDIM, "append needs at least one token");
   if (int rc = check_stream(pt, layer, kind)) return rc;
   const int s = (int)(layer * 2 + kind);
   Stream& st = pt->streams[s];
   const int64_t start = st.total;
+  *out_start = start;  // also on CapacityError: the caller copies the rows already packed
   std::vector<int64_t> ids;
   int64_t written = 0;
   while (written < t) {  // kvcache.py:210-223
@@ -233,6 +343,7 @@ int ifx_pt_append(ifx_pagetable* pt, int64_t layer, int kind, int64_t t, int64_t
 
 int ifx_pt_offload(ifx_pagetable* pt, const int64_t* block_ids, int64_t n, int64_t* out_moved) {
   std::lock_guard<std::mutex> g(pt->mu);
+  pt->begin_call();
   *out_moved = 0;
   std::vector<Page*> order;  // dict insertion order of kvcache.py:238-245
   std::set<int64_t> seen;
@@ -256,6 +367,7 @@ int ifx_pt_offload(ifx_pagetable* pt, const int64_t* block_ids, int64_t n, int64
 
 int ifx_pt_evict_window(ifx_pagetable* pt, int64_t keep, int64_t* out_freed) {
   std::lock_guard<std::mutex> g(pt->mu);
+  pt->begin_call();
   if (keep < 0) return ifx::fail(IFX_ECONFIG, "keep_last_n_tokens must be >= 0");
   int64_t freed = 0;
   for (int64_t l = 0; l < pt->num_layers; ++l) {  // kvcache.py:263-278
@@ -285,6 +397,7 @@ int ifx_pt_evict_window(ifx_pagetable* pt, int64_t keep, int64_t* out_freed) {
 
 int ifx_pt_clear_cross(ifx_pagetable* pt, int64_t* out_cleared) {
   std::lock_guard<std::mutex> g(pt->mu);
+  pt->begin_call();
   int64_t cleared = 0;
   for (auto it = pt->blocks.begin(); it != pt->blocks.end();) {
     if (it->second.kind == IFX_CROSS_ATTN) {
@@ -305,6 +418,7 @@ int ifx_pt_clear_cross(ifx_pagetable* pt, int64_t* out_cleared) {
 
 int ifx_pt_touch_range(ifx_pagetable* pt, int64_t layer, int kind, int64_t start, int64_t end) {
   std::lock_guard<std::mutex> g(pt->mu);
+  pt->begin_call();
   if (int rc = check_stream(pt, layer, kind)) return rc;
   Stream& st = pt->streams[layer * 2 + kind];
   if (start < st.base || end > st.total || start > end)
@@ -326,6 +440,7 @@ int ifx_pt_touch_range(ifx_pagetable* pt, int64_t layer, int kind, int64_t start
 int ifx_pt_touch_indices(ifx_pagetable* pt, int64_t layer, int kind, const int64_t* idx,
                          int64_t n) {
   std::lock_guard<std::mutex> g(pt->mu);
+  pt->begin_call();
   if (int rc = check_stream(pt, layer, kind)) return rc;
   Stream& st = pt->streams[layer * 2 + kind];
   for (int64_t i = 0; i < n; ++i)  // validation precedes any mutation (kvcache.py:346-349)
@@ -381,6 +496,61 @@ int ifx_pt_snapshot(const ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t*
   if (out == nullptr) return IFX_OK;
   if (cap < (int64_t)r.size()) return ifx::fail(IFX_EDIM, "snapshot buffer too small");
   std::memcpy(out, r.data(), r.size() * sizeof(int64_t));
+  return IFX_OK;
+}
+
+int ifx_pt_drain_moves(ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* n_records) {
+  std::lock_guard<std::mutex> g(pt->mu);
+  std::vector<const Move*> live;
+  for (const Move& m : pt->moves)
+    if (m.live) live.push_back(&m);
+  // execution order: per call (epoch), every device->host copy before any host->device one
+  std::stable_sort(live.begin(), live.end(), [](const Move* a, const Move* b) {
+    return a->epoch != b->epoch ? a->epoch < b->epoch : a->dir < b->dir;
+  });
+  *n_records = (int64_t)live.size();
+  if (out == nullptr) return IFX_OK;
+  if (cap < 5 * (int64_t)live.size()) return ifx::fail(IFX_EDIM, "move buffer too small");
+  for (size_t i = 0; i < live.size(); ++i) {
+    const Move& m = *live[i];
+    int64_t* r = out + 5 * i;
+    r[0] = m.epoch;
+    r[1] = m.kind;
+    r[2] = m.dir;
+    r[3] = m.dev_slot;
+    r[4] = m.host_slot;
+  }
+  pt->moves.clear();
+  return IFX_OK;
+}
+
+int ifx_pt_pool_extent(const ifx_pagetable* pt, int64_t* out4) {
+  for (int k = 0; k < 2; ++k)
+    for (int t = 0; t < 2; ++t) out4[k * 2 + t] = pt->pools[k][t].hwm;
+  return IFX_OK;
+}
+
+int ifx_pt_slots(ifx_pagetable* pt, int64_t layer, int kind, int64_t start, int64_t end,
+                 int32_t* out, int64_t cap, int64_t* first_token, int64_t* n) {
+  std::lock_guard<std::mutex> g(pt->mu);
+  if (int rc = check_stream(pt, layer, kind)) return rc;
+  Stream& st = pt->streams[layer * 2 + kind];
+  *n = 0;
+  *first_token = start;
+  if (start >= end) return IFX_OK;
+  if (st.pages.empty() || start < st.pages.front()->start || end > st.total)
+    return ifx::fail(IFX_ERANGE, "slot range outside the stored pages");
+  const int64_t s0 = st.pages.front()->start;
+  const int64_t k0 = (start - s0) / pt->page_len, k1 = (end - 1 - s0) / pt->page_len + 1;
+  *first_token = s0 + k0 * pt->page_len;
+  *n = k1 - k0;
+  if (out == nullptr) return IFX_OK;
+  if (cap < k1 - k0) return ifx::fail(IFX_EDIM, "slot buffer too small");
+  for (int64_t k = k0; k < k1; ++k) {
+    const Page* p = st.pages[k];
+    if (p->slot > INT32_MAX - 1) return ifx::fail(IFX_EDIM, "slot index exceeds int32");
+    out[k - k0] = p->tier == 0 ? (int32_t)p->slot : (int32_t)(-1 - p->slot);
+  }
   return IFX_OK;
 }
 

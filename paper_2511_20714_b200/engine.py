@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._device import attn_fwd, require_cuda, rms_bf16, rope_qk
+from ._device import attn_fwd, count_launch, require_cuda, rms_bf16, rope_qk
 from .errors import ConfigError, DimensionError
 from .kvcache import CROSS_ATTN, SELF_ATTN, KvCache, KvConfig
 
@@ -341,12 +341,13 @@ class BlockRunner:
         self.dev = require_cuda()
         self.ws = _Workspace(c.block_len, c.model_dim, model.attn_width, self.dev)
         self.attn_events = None
+        self.stager = _Stager(self.dev)
 
     def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
                 collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None,
                 rope=None):
-        """One pass. ctx[l] = (slab, base, total) or None; cross[l] = (k, v, row0, n) or None;
-        rope = (cos, sin) tables of this block (rope_tables) or None."""
+        """One pass. ctx: _KvContext of the block or None; cross[l] = (k, v, row0, n) or
+        None; rope = (cos, sin) tables of this block (rope_tables) or None."""
         m, ws = self.model, self.ws
         c = m.config
         H, dhp, Dp = m.heads_pad, m.dh_pad, m.attn_width
@@ -364,11 +365,8 @@ class BlockRunner:
             if ev is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-            slab_info = ctx[li] if ctx is not None else None
-            if slab_info is not None and slab_info[2] > slab_info[1]:
-                s, base, total = slab_info
-                attn_fwd(q, H, dhp, ws.attn, s.k, s.v, base - s.origin, total - base, kc, vc,
-                         scale=sc)
+            if ctx is not None:
+                ctx.attend(li, q, H, dhp, ws.attn, kc, vc, sc)
             else:
                 attn_fwd(q, H, dhp, ws.attn, cur_k=kc, cur_v=vc, scale=sc)
             if ev is not None:
@@ -405,22 +403,184 @@ class BlockRunner:
         return latent
 
 
-def _ctx_from_cache(model: ToyModel, cache: KvCache | None):
-    """engine.py:228-237 — bookkeeping of the context fetch (restore + access clock, in the
-    reference's call order) while the data stays in place for K1."""
+PAGED_K1_PAGE_LENS = (8, 16, 32, 64, 128)  # page boxes that tile K1's 128-key tiles
+
+
+class _Stager:
+    """HBM staging pool for host-tier context pages (one per runner, reused by blocks).
+
+    K1 cannot stream pages out of host memory at tensor-core speed (every key tile is read
+    by all query tiles), so before a layer's attention its host pages are copied H2D (K6,
+    PCIe) into staging slots, on a side stream, one attention call ahead: the copy for the
+    next layer overlaps this layer's attention. If every layer's host pages fit the budget
+    they are staged once per block (the data is constant within a block); otherwise 2
+    buffers rotate between consecutive layers (3 for an odd layer count)."""
+
+    def __init__(self, dev, budget_bytes: int | None = None):
+        self.dev = dev
+        self.copy = torch.cuda.Stream(dev)
+        self.k = self.v = None
+        self.budget = budget_bytes if budget_bytes is not None else int(
+            os.environ.get("IFX_STAGE_BUDGET_MB", "8192")) << 20
+        self.staged_pages = 0  # pages copied H2D for attention (all blocks)
+
+    def ensure(self, slots: int, page_len: int, width: int, dtype) -> None:
+        rows = slots * page_len
+        if self.k is not None and self.k.shape[0] >= rows and self.k.shape[1] == width \
+                and self.k.dtype == dtype:
+            return
+        self.copy.synchronize()  # no staging copy may still write the old buffers
+        rows = max(rows, 2 * (self.k.shape[0] if self.k is not None else 0))
+        self.k = torch.zeros(rows, width, device=self.dev, dtype=dtype)
+        self.v = torch.zeros_like(self.k)
+
+
+class _KvContext:
+    """Attention view of the self-attention cache for one block (engine.py:228-237).
+
+    Built once per block after the context fetch's bookkeeping (restore-on-read + clock,
+    whose tier moves the cache executes). K1 reads device-tier pages IN PLACE from the pool
+    through a per-layer slot table; host-tier pages come from the staging pool (_Stager).
+    Page lengths K1 cannot box (not in PAGED_K1_PAGE_LENS) fall back to a K7 gather of the
+    context into a contiguous scratch per call."""
+
+    def __init__(self, model, cache: KvCache, stager: _Stager, passes: int):
+        self.cache = cache
+        cfg = cache.config
+        L = model.config.layers
+        self.L, self.P = L, cfg.page_len
+        self.pool = cache.pool(SELF_ATTN)
+        self.paged = cfg.page_len in PAGED_K1_PAGE_LENS
+        self.stager = stager
+        self.calls = 0
+        self.n_calls = passes * L
+        self.ranges = []
+        for li in range(L):  # the reference's fetch order: layer 0..L-1 (engine.py:228-237)
+            lo, hi = cache.addressable_range(li, SELF_ATTN)
+            if hi > lo:
+                cache.touch_range(li, (lo, hi), SELF_ATTN)
+            self.ranges.append((lo, hi))
+        self.first = [0] * L
+        self.host_moves = [None] * L
+        self.buf_of = [0] * L
+        if not self.paged:
+            return
+        tables, host = [], []
+        for li, (lo, hi) in enumerate(self.ranges):
+            codes, first = cache.slot_table(li, SELF_ATTN, lo, hi) if hi > lo else (np.zeros(0, np.int32), lo)
+            self.first[li] = first
+            tables.append(codes)
+            host.append(np.flatnonzero(codes < 0))
+        per_layer = max((len(h) for h in host), default=0)
+        W = self.pool.width
+        if per_layer:
+            slot_b = self.P * W * self.pool.esz
+            total = sum(len(h) for h in host)
+            if total * slot_b <= stager.budget or L == 1:
+                nbuf, self.buf_of = L, list(range(L))   # stage once per block
+                offs = np.cumsum([0] + [len(h) for h in host])
+            else:
+                nbuf = 2 if L % 2 == 0 else 3
+                self.buf_of = [li % 2 for li in range(L)]
+                if L % 2:
+                    self.buf_of[L - 1] = 2
+                offs = [self.buf_of[li] * per_layer for li in range(L)]
+            self.once = nbuf == L
+            stager.ensure(int(offs[-1]) if self.once else nbuf * per_layer, self.P, W, self.pool.dtype)
+            for li, h in enumerate(host):
+                if len(h):
+                    hs = -1 - tables[li][h].astype(np.int64)
+                    st = int(offs[li]) + np.arange(len(h), dtype=np.int64)
+                    tables[li] = tables[li].copy()
+                    tables[li][h] = (-1 - st).astype(np.int32)
+                    self.host_moves[li] = np.stack([st, hs], axis=1)
+        dev = require_cuda()
+        flat = np.concatenate(tables) if tables else np.zeros(0, np.int32)
+        allt = torch.from_numpy(flat).to(dev, non_blocking=True)
+        lens = np.cumsum([0] + [len(t) for t in tables])
+        self.tables = [allt[lens[i]:lens[i + 1]] for i in range(L)]
+        mv = [m for m in self.host_moves if m is not None]
+        self.moves_dev = None
+        if mv:
+            allm = torch.from_numpy(np.concatenate(mv)).to(dev, non_blocking=True)
+            self.moves_dev, o = [None] * L, 0
+            for li, m in enumerate(self.host_moves):
+                if m is not None:
+                    self.moves_dev[li] = allm[o:o + len(m)]
+                    o += len(m)
+            self.staged = {}
+            self.consumed = {}
+            start = torch.cuda.Event()
+            start.record()  # tier moves + table uploads of this block are enqueued before it
+            stager.copy.wait_event(start)
+            if self.once:
+                for li in range(L):
+                    self._stage(li, li)
+            else:
+                self._stage(0, 0)
+
+    def _stage(self, call: int, li: int) -> None:
+        """Enqueue the H2D copy of layer li's host pages for attention call `call`."""
+        if self.moves_dev is None or self.moves_dev[li] is None:
+            return
+        st = self.stager
+        buf = self.buf_of[li]
+        if buf in self.consumed:
+            st.copy.wait_event(self.consumed[buf])
+        p = _abi.KvPool()
+        pool = self.pool
+        p.dev_k, p.dev_v = st.k.data_ptr(), st.v.data_ptr()
+        p.host_k, p.host_v = pool.host_k.ptr, pool.host_v.ptr
+        p.width, p.page_len, p.type = pool.width, pool.page_len, _abi.BF16 if pool.dtype == torch.bfloat16 else _abi.F32
+        m = self.moves_dev[li]
+        _abi.check(_abi.lib().ifx_kv_move_pages(ctypes.byref(p), m.data_ptr(), m.shape[0], 1,
+                                               st.copy.cuda_stream), "stage")
+        count_launch()
+        st.staged_pages += m.shape[0]
+        ev = torch.cuda.Event()
+        ev.record(st.copy)
+        self.staged[call if not self.once else li] = ev
+
+    def attend(self, li: int, q, heads: int, dhp: int, out, cur_k, cur_v, scale: float, attn=None):
+        """K1 for layer li: q over [this layer's cached context ∥ the block's own K/V]."""
+        attn = attn or attn_fwd
+        lo, hi = self.ranges[li]
+        call = self.calls
+        self.calls += 1
+        if hi <= lo:
+            return attn(q, heads, dhp, out, cur_k=cur_k, cur_v=cur_v, scale=scale)
+        if not self.paged:  # K7 gather of the context (host pages read over PCIe in place)
+            k, v = self.cache._gather(li, SELF_ATTN, None, lo, hi - lo, lo, hi, raw=True)
+            return attn(q, heads, dhp, out, k, v, 0, hi - lo, cur_k, cur_v, scale=scale)
+        staged = self.moves_dev is not None and self.moves_dev[li] is not None
+        if staged:
+            torch.cuda.current_stream().wait_event(self.staged[li if self.once else call])
+        pool, st = self.pool, self.stager
+        attn(q, heads, dhp, out, pool.dev_k, pool.dev_v, lo, hi - lo, cur_k, cur_v, scale=scale,
+             ctx_slots=self.tables[li], page_len=self.P, first_token=self.first[li],
+             stage_k=st.k if staged else None, stage_v=st.v if staged else None)
+        if self.moves_dev is not None and not self.once:
+            if staged:
+                ev = torch.cuda.Event()
+                ev.record()
+                self.consumed[self.buf_of[li]] = ev
+            if call + 1 < self.n_calls:
+                self._stage(call + 1, (li + 1) % self.L)
+        return out
+
+
+def _ctx_from_cache(model: ToyModel, cache: KvCache | None, stager: _Stager | None = None,
+                    passes: int = 1):
+    """engine.py:228-237 — the context fetch's bookkeeping (restore + access clock, in the
+    reference's call order, with the tier moves it implies) and K1's paged view."""
     if cache is None:
         return None
-    out = []
-    for li in range(model.config.layers):
-        lo, hi = cache.addressable_range(li, SELF_ATTN)
-        if hi > lo:
-            cache.touch_range(li, (lo, hi), SELF_ATTN)
-        out.append((cache.slab(li, SELF_ATTN), lo, hi))
-    return out
+    return _KvContext(model, cache, stager or _Stager(require_cuda()), passes)
 
 
 def _cross_from_cache(model: ToyModel, cache: KvCache | None, prompt_ctx):
-    """engine.py:240-250."""
+    """engine.py:240-250 — per layer the prompt K/V rows, gathered (K7) into a contiguous
+    bf16 buffer once per block (a few rows; pages may sit on either tier)."""
     if cache is not None:
         lo, hi = cache.addressable_range(0, CROSS_ATTN)
         if hi > lo:
@@ -428,8 +588,8 @@ def _cross_from_cache(model: ToyModel, cache: KvCache | None, prompt_ctx):
             for li in range(model.config.layers):
                 a, b = cache.addressable_range(li, CROSS_ATTN)
                 cache.touch_range(li, (a, b), CROSS_ATTN)
-                s = cache.slab(li, CROSS_ATTN)
-                out.append((s.k, s.v, a - s.origin, b - a))
+                k, v = cache._gather(li, CROSS_ATTN, None, a, b - a, a, b, raw=True)
+                out.append((k, v, 0, b - a))
             return out
     if prompt_ctx is None:
         return None
@@ -463,7 +623,8 @@ def denoise_step(model: ToyModel, latent, t: float, step_scale: float, cache: Kv
         r.__init__(model)
         r.ws = _Workspace(lat.shape[0], c.model_dim, model.attn_width, r.dev)
     eps = torch.empty_like(lat)
-    r.forward(lat, float(t), _ctx_from_cache(model, cache), _cross_from_cache(model, cache, prompt_ctx),
+    r.forward(lat, float(t), _ctx_from_cache(model, cache, getattr(r, "stager", None)),
+              _cross_from_cache(model, cache, prompt_ctx),
               cache, eps_out=eps, rope=rope_tables(c, 0, lat.device) if lat.shape[0] == c.block_len
               else None)
     return lat.sub_(eps, alpha=float(step_scale))
@@ -510,9 +671,10 @@ def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSche
     src = noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)
     lat = torch.empty(src.shape, device=require_cuda(), dtype=torch.float32)
     lat.copy_(src, non_blocking=True)  # async H2D when the noise lives in pinned memory
-    ctx = _ctx_from_cache(model, cache)
+    runner = _runner(model)
+    ctx = _ctx_from_cache(model, cache, runner.stager, passes=len(schedule.steps) + 1)
     cross = _cross_from_cache(model, cache, prompt_ctx)
-    _runner(model).denoise(lat, schedule, ctx, cross, cache, chunk_index)
+    runner.denoise(lat, schedule, ctx, cross, cache, chunk_index)
     if not to_host:
         return GeneratedBlock(chunk_index, lat, [], prompt_text)
     # frames decoded on device; latent + frames land in pinned host buffers (one sync)

@@ -6,10 +6,13 @@ Split of responsibilities:
   * bookkeeping (page ids, tiers, LRU, access clock, eviction, block entries) is the
     native page table in libinferix_b200.so (csrc/pagetable.cpp), bit-exact with the
     reference (tests/test_pagetable.py replays the reference's full state);
-  * data lives in HBM: one K slab and one V slab per (layer, kind), rows addressed by
-    stream position (token id - origin), written by K2 (`ifx_kv_append`, 128-bit stores)
-    and read either in place by the attention kernel K1 or through K7 (`ifx_kv_gather`)
-    for `fetch_range` / `fetch_indices`.
+  * data placement follows the tiers exactly: every page owns a slot (page_len rows) in
+    the HBM pool (tier device) or in the mapped pinned-host pool (tier host) of its kind;
+    the tier moves a call makes (restore-on-read with LRU demotion, offload) are drained
+    from the page table and executed as whole-page copies (K6 `ifx_kv_move_pages`);
+  * K2 (`ifx_kv_append`) writes appended rows straight into their pages' slots (device
+    or host), K7 (`ifx_kv_gather`) serves fetch_range / fetch_indices, and the attention
+    kernel K1 reads device pages in place through the slot table (engine.py).
 
 Storage dtype is fp32 (bit-exact API parity, the default) or bf16 (the engine's choice:
 K1 reads bf16 tiles). Returned fetches are new CUDA tensors.
@@ -94,44 +97,86 @@ class KvStats:
     bytes_logical: int
 
 
-class _Slab:
-    """Device K/V rows of one (layer, kind) stream: row = token - origin.
+class _HostBuf:
+    """Pinned host memory mapped into the device address space (ifx_host_alloc): K2/K6/K7
+    address it directly (UVA). Zero-filled so partially filled pages stay finite."""
 
-    Grows geometrically; when it must grow and tokens below the stream base are dead
-    (window eviction), live rows are compacted to the front instead (origin moves)."""
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _abi.check(_abi.lib().ifx_host_alloc(int(nbytes), ctypes.byref(p)), "host_alloc")
+        self.ptr, self.nbytes = p.value or 0, int(nbytes)
+        if self.ptr:
+            self.bytes_view().zero_()
 
-    def __init__(self, width: int, dtype: torch.dtype, rows: int):
-        self.width, self.dtype = width, dtype
-        self.origin = 0
-        rows = max(16, rows)
-        dev = require_cuda()
-        self.k = torch.zeros(rows, width, device=dev, dtype=dtype)
-        self.v = torch.zeros(rows, width, device=dev, dtype=dtype)
+    def bytes_view(self) -> torch.Tensor:
+        """CPU uint8 tensor aliasing the buffer (valid while self is alive)."""
+        return torch.frombuffer((ctypes.c_uint8 * self.nbytes).from_address(self.ptr),
+                                dtype=torch.uint8)
 
-    def reset(self):
-        self.origin = 0
+    def __del__(self):
+        if getattr(self, "ptr", 0):
+            try:
+                _abi.lib().ifx_host_free(ctypes.c_void_p(self.ptr))
+            except Exception:  # interpreter shutdown
+                pass
+            self.ptr = 0
 
-    def ensure(self, base: int, end: int, page_len: int):
-        """Make rows for tokens [base, end) addressable. Rows from the start of the page
-        holding `base` are kept (a partially evicted page stays readable for dump())."""
-        need = end - self.origin
-        if need <= self.k.shape[0]:
-            return
-        keep = base - base % page_len
-        if end - keep <= self.k.shape[0] // 2 and keep > self.origin:  # compact in place
-            live0 = keep - self.origin
-            n = max(0, min(self.k.shape[0], end - self.origin) - live0)
-            if n:
-                self.k[:n].copy_(self.k[live0:live0 + n].clone())
-                self.v[:n].copy_(self.v[live0:live0 + n].clone())
-            self.origin = keep
-            return
-        rows = max(need, 2 * self.k.shape[0])
-        k = torch.zeros(rows, self.width, device=self.k.device, dtype=self.dtype)
-        v = torch.zeros_like(k)
-        k[:self.k.shape[0]].copy_(self.k)
-        v[:self.v.shape[0]].copy_(self.v)
-        self.k, self.v = k, v
+
+class _Pool:
+    """Slot pools of one kind (self / cross): HBM [slots * page_len, width] K and V, and
+    the pinned host tier alike. Grown geometrically as the page table's high-water marks
+    rise (device growth is a stream-ordered copy; host growth synchronises first)."""
+
+    def __init__(self, width: int, dtype: torch.dtype, page_len: int):
+        self.width, self.dtype, self.page_len = width, dtype, page_len
+        self.esz = torch.finfo(dtype).bits // 8
+        self.dev_slots = self.host_slots = 0
+        self.dev_k = self.dev_v = None
+        self.host_k = self.host_v = None
+        self._abi = None
+
+    @property
+    def slot_bytes(self) -> int:
+        return self.page_len * self.width * self.esz
+
+    def ensure(self, dev_slots: int, host_slots: int) -> None:
+        P, W = self.page_len, self.width
+        if dev_slots > self.dev_slots:
+            n = max(dev_slots, 2 * self.dev_slots, 4)
+            dev = require_cuda()
+            k = torch.zeros(n * P, W, device=dev, dtype=self.dtype)
+            v = torch.zeros_like(k)
+            if self.dev_slots:
+                k[:self.dev_slots * P].copy_(self.dev_k)
+                v[:self.dev_slots * P].copy_(self.dev_v)
+            self.dev_k, self.dev_v, self.dev_slots = k, v, n
+            self._abi = None
+        if host_slots > self.host_slots:
+            n = max(host_slots, 2 * self.host_slots, 4)
+            k, v = _HostBuf(n * self.slot_bytes), _HostBuf(n * self.slot_bytes)
+            if self.host_slots:
+                torch.cuda.synchronize()  # no kernel may still address the old buffers
+                used = self.host_slots * self.slot_bytes
+                k.bytes_view()[:used].copy_(self.host_k.bytes_view()[:used])
+                v.bytes_view()[:used].copy_(self.host_v.bytes_view()[:used])
+            self.host_k, self.host_v, self.host_slots = k, v, n
+            self._abi = None
+
+    def abi(self) -> _abi.KvPool:
+        if self._abi is None:
+            p = _abi.KvPool()
+            p.dev_k = self.dev_k.data_ptr() if self.dev_k is not None else None
+            p.dev_v = self.dev_v.data_ptr() if self.dev_v is not None else None
+            p.host_k = self.host_k.ptr if self.host_k is not None else None
+            p.host_v = self.host_v.ptr if self.host_v is not None else None
+            p.width, p.page_len, p.type = self.width, self.page_len, dtype_code(self.dtype)
+            self._abi = p
+        return self._abi
+
+    def host_rows(self, which: str) -> torch.Tensor:
+        """CPU [host_slots * page_len, width] view of the host tier (tests, dump)."""
+        buf = self.host_k if which == "k" else self.host_v
+        return buf.bytes_view().view(self.dtype).view(-1, self.width)
 
 
 class PageTable:
@@ -203,6 +248,39 @@ class PageTable:
                                            ctypes.byref(base), ctypes.byref(total)))
         return base.value, total.value
 
+    def drain_moves(self) -> np.ndarray:
+        """Logged tier moves as int64 [n, 5] (epoch, kind, dir, device slot, host slot), in
+        execution order."""
+        n = ctypes.c_int64()
+        L = _abi.lib()
+        _abi.check(L.ifx_pt_drain_moves(self._h, None, 0, ctypes.byref(n)))
+        if n.value == 0:
+            return np.zeros((0, 5), np.int64)
+        out = np.empty((n.value, 5), np.int64)
+        _abi.check(L.ifx_pt_drain_moves(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                        out.size, ctypes.byref(n)))
+        return out
+
+    def pool_extent(self) -> list:
+        """Slots ever used: [self device, self host, cross device, cross host]."""
+        out = (ctypes.c_int64 * 4)()
+        _abi.check(_abi.lib().ifx_pt_pool_extent(self._h, out))
+        return list(out)
+
+    def slots(self, layer: int, kind: str, start: int, end: int):
+        """(int32 slot codes of the pages covering [start, end), first page's start token);
+        code >= 0 device slot, < 0 host slot -1-code."""
+        n, first = ctypes.c_int64(), ctypes.c_int64()
+        L = _abi.lib()
+        k = self.kind_code(kind)
+        _abi.check(L.ifx_pt_slots(self._h, layer, k, start, end, None, 0, ctypes.byref(first),
+                                  ctypes.byref(n)))
+        out = np.empty(n.value, np.int32)
+        if n.value:
+            _abi.check(L.ifx_pt_slots(self._h, layer, k, start, end, out.ctypes.data, n.value,
+                                      ctypes.byref(first), ctypes.byref(n)))
+        return out, first.value
+
     def stats(self) -> list:
         L = self.config.num_layers
         out = (ctypes.c_int64 * (3 + L))()
@@ -235,11 +313,11 @@ class PageTable:
 class KvCache:
     """Drop-in for `inferix.kvcache.KvCache` (kvcache.py:105-404); create via create_cache().
 
-    Extra keyword arguments (B200 only): `dtype` of the device slabs (torch.float32 for
-    bit-exact API parity, torch.bfloat16 for the engine), `reserve_tokens` rows to
-    pre-allocate per self-attention stream, `row_width` of the device rows when it
-    differs from head_dim (the engine stores per-head zero-padded rows; a Ulysses rank
-    stores only its heads), `cross_row_width` likewise for the cross-attention streams."""
+    Extra keyword arguments (B200 only): `dtype` of the pools (torch.float32 for bit-exact
+    API parity, torch.bfloat16 for the engine), `reserve_tokens` per self-attention stream
+    to pre-size the HBM pool for, `row_width` of the pool rows when it differs from
+    head_dim (the engine stores per-head zero-padded rows; a Ulysses rank stores only its
+    heads), `cross_row_width` likewise for the cross-attention streams."""
 
     def __init__(self, config: KvConfig, dtype: torch.dtype = torch.float32,
                  reserve_tokens: int = 0, row_width: int | None = None,
@@ -254,10 +332,13 @@ class KvCache:
         w = row_width or config.stored_width
         wc = cross_row_width or w
         self._row_width = {SELF_ATTN: w, CROSS_ATTN: wc}
-        self._slabs = {}
-        for layer in range(config.num_layers):
-            self._slabs[(layer, SELF_ATTN)] = _Slab(w, dtype, reserve_tokens)
-            self._slabs[(layer, CROSS_ATTN)] = _Slab(wc, dtype, 64)
+        self._pools = {SELF_ATTN: _Pool(w, dtype, config.page_len),
+                       CROSS_ATTN: _Pool(wc, dtype, config.page_len)}
+        self.moved_pages = [0, 0]  # pages copied device->host, host->device (tier moves)
+        if reserve_tokens:
+            per_layer = -(-reserve_tokens // config.page_len) + 1
+            self._pools[SELF_ATTN].ensure(min(config.capacity_pages_device,
+                                              per_layer * config.num_layers), 0)
         self._latent_down = self._latent_up = None
         if config.latent is not None:
             dev = require_cuda()
@@ -268,9 +349,9 @@ class KvCache:
     def page_table(self) -> PageTable:
         return self._pt
 
-    def slab(self, layer: int, kind: str = SELF_ATTN) -> _Slab:
-        """Device rows of a stream (the engine's K1 reads them in place)."""
-        return self._slabs[(layer, kind)]
+    def pool(self, kind: str = SELF_ATTN) -> _Pool:
+        """Slot pools of a kind (the engine's K1 reads device pages in place)."""
+        return self._pools[kind]
 
     @staticmethod
     def _as_rows(x) -> torch.Tensor:
@@ -280,6 +361,34 @@ class KvCache:
         a = np.asarray(x, dtype=np.float32)
         t = torch.from_numpy(np.ascontiguousarray(a))
         return t.to(require_cuda()) if a.ndim == 2 else t
+
+    # -- physical placement ---------------------------------------------------------------
+    def _sync(self, stream=None) -> None:
+        """Grow the pools to the page table's slot high-water marks, then execute the tier
+        moves its last call logged (K6: device->host batch, then host->device batch)."""
+        ext = self._pt.pool_extent()
+        self._pools[SELF_ATTN].ensure(ext[0], ext[1])
+        self._pools[CROSS_ATTN].ensure(ext[2], ext[3])
+        mv = self._pt.drain_moves()
+        if not len(mv):
+            return
+        dev = require_cuda()
+        pairs = torch.from_numpy(np.ascontiguousarray(mv[:, 3:5])).to(dev, non_blocking=True)
+        # consecutive records with the same (epoch, dir, kind) form one hazard-free launch
+        key = mv[:, 0] * 4 + mv[:, 2] * 2 + mv[:, 1]
+        cuts = np.flatnonzero(np.diff(key)) + 1
+        for lo, hi in zip(np.r_[0, cuts], np.r_[cuts, len(mv)]):
+            kind = _KIND_NAME[int(mv[lo, 1])]
+            d = int(mv[lo, 2])
+            p = self._pools[kind]
+            _abi.check(_abi.lib().ifx_kv_move_pages(ctypes.byref(p.abi()), pairs[lo].data_ptr(),
+                                                   int(hi - lo), d, stream_ptr(stream)), "kv_move_pages")
+            count_launch()
+            self.moved_pages[d] += int(hi - lo)
+
+    def slot_table(self, layer: int, kind: str, start: int, end: int):
+        """(int32 slot codes of the pages covering tokens [start, end), first page's start)."""
+        return self._pt.slots(layer, kind, start, end)
 
     # -- mutations ------------------------------------------------------------------------
     def append_block(self, layer: int, k, v, kind: str = SELF_ATTN, chunk_index: int = 0,
@@ -304,56 +413,65 @@ class KvCache:
             k, v = k.contiguous(), v.contiguous()
         with self._lock:
             rc, bid, start, written, pages = self._pt.append(layer, kind, t, chunk_index)
+            self._sync(stream)
             if written > 0:  # rows already packed even if allocation then failed (kvcache.py:210-223)
-                base, total = self._pt.range(layer, kind)
-                s = self._slabs[(layer, kind)]
-                s.ensure(base, total, cfg.page_len)
+                codes, first = self._pt.slots(layer, kind, start, start + written)
+                slots = torch.from_numpy(codes).to(k.device, non_blocking=True)
+                p = self._pools[kind]
                 _abi.check(_abi.lib().ifx_kv_append(
-                    k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype),
-                    s.k.data_ptr(), s.v.data_ptr(), s.width, dtype_code(s.dtype),
-                    total - written - s.origin, written, s.width, stream_ptr(stream)), "kv_append")
+                    k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype), ctypes.byref(p.abi()),
+                    slots.data_ptr(), first, start, written, stream_ptr(stream)), "kv_append")
                 count_launch()
             _abi.check(rc, "append_block")
             return BlockEntry(bid, layer, (start, start + t), pages, kind, chunk_index)
 
     def offload_blocks(self, block_ids) -> int:
-        """kvcache.py:236-256 (tier bookkeeping; data stays resident in HBM)."""
+        """kvcache.py:236-256: demote the blocks' device pages; their data moves to the
+        pinned host pool (K6) even when a later block id fails (partial, like the
+        reference)."""
         with self._lock:
-            return self._pt.offload(block_ids)
+            try:
+                return self._pt.offload(block_ids)
+            finally:
+                self._sync()
 
     def evict_window(self, keep_last_n_tokens: int) -> int:
-        """kvcache.py:258-285."""
+        """kvcache.py:258-285 (freed pages return their slots to the pools)."""
         with self._lock:
             return self._pt.evict_window(keep_last_n_tokens)
 
     def clear_cross_attention(self) -> int:
         """kvcache.py:287-299."""
         with self._lock:
-            n = self._pt.clear_cross()
-            for layer in range(self.config.num_layers):
-                self._slabs[(layer, CROSS_ATTN)].reset()
-            return n
+            return self._pt.clear_cross()
 
     # -- reads ----------------------------------------------------------------------------
-    def touch_range(self, layer: int, token_range, kind: str = SELF_ATTN) -> None:
+    def touch_range(self, layer: int, token_range, kind: str = SELF_ATTN, stream=None) -> None:
         """Bookkeeping half of fetch_range (restore-on-read + per-token access clock,
-        kvcache.py:303-339) without moving data — what the engine calls before K1 reads
-        the slab in place."""
+        kvcache.py:303-339) with the data moves it implies, without gathering — what the
+        engine calls before K1 reads the pages in place."""
         a, b = token_range
         with self._lock:
-            self._pt.touch_range(layer, kind, a, b)
+            try:
+                self._pt.touch_range(layer, kind, a, b)
+            finally:
+                self._sync(stream)
 
-    def _gather(self, layer, kind, rows: torch.Tensor | None, first: int, n: int):
-        s = self._slabs[(layer, kind)]
-        ko = torch.empty(n, s.width, device=s.k.device, dtype=s.dtype)
+    def _gather(self, layer, kind, tokens: torch.Tensor | None, first: int, n: int, lo: int, hi: int,
+                raw: bool = False):
+        p = self._pools[kind]
+        dev = require_cuda()
+        ko = torch.empty(n, p.width, device=dev, dtype=p.dtype)
         vo = torch.empty_like(ko)
         if n:
+            codes, first_tok = self._pt.slots(layer, kind, lo, hi)
+            slots = torch.from_numpy(codes).to(dev, non_blocking=True)
             _abi.check(_abi.lib().ifx_kv_gather(
-                s.k.data_ptr(), s.v.data_ptr(), s.width, dtype_code(s.dtype),
-                None if rows is None else rows.data_ptr(), first - s.origin, n, s.width,
+                ctypes.byref(p.abi()), slots.data_ptr(), first_tok,
+                None if tokens is None else tokens.data_ptr(), first, n,
                 ko.data_ptr(), vo.data_ptr(), stream_ptr()), "kv_gather")
             count_launch()
-        if self._latent_up is not None:
+        if self._latent_up is not None and not raw:
             ko, vo = ko.float() @ self._latent_up, vo.float() @ self._latent_up
         return ko, vo
 
@@ -363,8 +481,8 @@ class KvCache:
         if not 0 <= layer < self.config.num_layers:
             raise OutOfRangeError(f"layer {layer} out of range")
         with self._lock:
-            self._pt.touch_range(layer, kind, a, b)
-            return self._gather(layer, kind, None, a, b - a)
+            self.touch_range(layer, (a, b), kind)
+            return self._gather(layer, kind, None, a, b - a, a, b)
 
     def fetch_indices(self, layer: int, indices, kind: str = SELF_ATTN):
         """kvcache.py:341-353 (order and duplicates preserved; empty -> (0, head_dim))."""
@@ -372,13 +490,15 @@ class KvCache:
         if not 0 <= layer < self.config.num_layers:
             raise OutOfRangeError(f"layer {layer} out of range")
         with self._lock:
-            self._pt.touch_indices(layer, kind, idx)
+            try:
+                self._pt.touch_indices(layer, kind, idx)
+            finally:
+                self._sync()
             if not idx:
                 w, dev = self.config.head_dim, require_cuda()
                 return (torch.empty(0, w, device=dev), torch.empty(0, w, device=dev))
-            s = self._slabs[(layer, kind)]
-            rows = torch.tensor(idx, dtype=torch.int64).to(s.k.device) - s.origin
-            return self._gather(layer, kind, rows, 0, len(idx))
+            toks = torch.tensor(idx, dtype=torch.int64).to(require_cuda(), non_blocking=True)
+            return self._gather(layer, kind, toks, 0, len(idx), min(idx), max(idx) + 1)
 
     def addressable_range(self, layer: int, kind: str = SELF_ATTN):
         """kvcache.py:355-357."""
@@ -402,10 +522,16 @@ class KvCache:
         return [BlockEntry(b[0], b[1], (b[3], b[4]), b[5], b[2], b[6]) for b in self.state()["blocks"]]
 
     def dump(self, path) -> None:
-        """kvcache.py:380-404 — INFKV1 snapshot (fp32 rows, pages sorted by id)."""
+        """kvcache.py:380-404 — INFKV1 snapshot (fp32 rows, pages sorted by id). Reads every
+        page where it lives (device or host pool) without touching the access clock."""
         cfg = self.config
-        pages = []
-        for layer, kind, _base, _total, pgs in self.state()["streams"]:
+        pages, rows = [], {}
+        for layer, kind, _base, total, pgs in self.state()["streams"]:
+            if not pgs:
+                continue
+            s0 = pgs[0][3]
+            k, v = self._gather(layer, kind, None, s0, total - s0, s0, total, raw=True)
+            rows[(layer, kind)] = (s0, k.float().cpu().numpy(), v.float().cpu().numpy())
             for pid, tier, filled, start, _la in pgs:
                 pages.append((pid, tier, filled, start, layer, kind))
         pages.sort()
@@ -416,10 +542,9 @@ class KvCache:
             f.write(struct.pack("<I", len(pages)))
             for pid, tier, filled, start, layer, kind in pages:
                 f.write(struct.pack("<IBII", pid, tier, filled, start))
-                s = self._slabs[(layer, kind)]
-                r0 = start - s.origin
-                f.write(s.k[r0:r0 + filled].float().cpu().numpy().tobytes())
-                f.write(s.v[r0:r0 + filled].float().cpu().numpy().tobytes())
+                s0, k, v = rows[(layer, kind)]
+                f.write(k[start - s0:start - s0 + filled].tobytes())
+                f.write(v[start - s0:start - s0 + filled].tobytes())
 
 
 def create_cache(config: KvConfig, **kw) -> KvCache:

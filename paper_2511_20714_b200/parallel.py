@@ -302,6 +302,8 @@ class UlyssesRunner:
         self.eps = torch.empty(n, D, device=dev)
         self.zero_bias = torch.zeros(2 * D, device=dev, dtype=torch.bfloat16)
         self.attn_events = None
+        from .engine import _Stager
+        self.stager = _Stager(dev)
 
     def _rms(self, x, out, tvec=None, t=0.0, x_out=None):
         from ._device import rms_bf16
@@ -331,12 +333,7 @@ class UlyssesRunner:
             if ev is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-            s, base, total = ctx[li]
-            if total > base:
-                self._attn(q, self.hl, dhp, self.attn_h, s.k, s.v, base - s.origin, total - base,
-                           kc, vc, scale=sc)
-            else:
-                self._attn(q, self.hl, dhp, self.attn_h, cur_k=kc, cur_v=vc, scale=sc)
+            ctx.attend(li, q, self.hl, dhp, self.attn_h, kc, vc, sc, attn=self._attn)
             if ev is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record()
@@ -405,7 +402,7 @@ class UlyssesEngine:
             noise = make_noise(chunk)
             full = noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)
             lat = full[rank * n:(rank + 1) * n].to(m.time_vec.device, torch.float32).clone()
-            ctx = _ctx_from_cache(m, self.cache)
+            ctx = _ctx_from_cache(m, self.cache, r.stager, passes=len(request.schedule.steps) + 1)
             cross = _cross_from_cache(m, self.cache, None)
             r.denoise(lat, request.schedule, ctx, cross, self.cache, chunk)
             if request.kv_window is not None:

@@ -92,33 +92,130 @@ def test_attention_large_scores_and_masks():
     assert (out.float() - ref).abs().max().item() < 3e-2
 
 
-def test_kv_append_and_gather_bit_exact():
+def _pool(kd, vd, hk, hv, w, page_len, dt):
+    from paper_2511_20714_b200 import _abi
+    p = _abi.KvPool()
+    p.dev_k, p.dev_v = kd.data_ptr(), vd.data_ptr()
+    p.host_k, p.host_v = hk, hv
+    p.width, p.page_len = w, page_len
+    p.type = _abi.BF16 if dt == torch.bfloat16 else _abi.F32
+    return p
+
+
+def test_kv_append_gather_move_bit_exact():
+    """K2 / K7 / K6 over a device pool + a mapped pinned host pool, scattered slots."""
+    import ctypes
+
     from paper_2511_20714_b200 import _abi
     from paper_2511_20714_b200._device import stream_ptr
+    from paper_2511_20714_b200.kvcache import _HostBuf
 
     L = _abi.lib()
     g = torch.Generator(device="cuda").manual_seed(1)
+    code = lambda dt: _abi.BF16 if dt == torch.bfloat16 else _abi.F32  # noqa: E731
     for src_dt, dst_dt in [(torch.float32, torch.float32), (torch.float32, torch.bfloat16),
                            (torch.bfloat16, torch.bfloat16)]:
-        t, w = 37, 256
+        t, w, P = 37, 256, 8
+        esz = 2 if dst_dt == torch.bfloat16 else 4
         src = torch.randn(t, 3 * w, device="cuda", generator=g).to(src_dt)
         ks, vs = src[:, w:2 * w], src[:, 2 * w:]
-        kd = torch.zeros(100, w, device="cuda", dtype=dst_dt)
-        vd = torch.zeros(100, w, device="cuda", dtype=dst_dt)
-        code = lambda dt: _abi.BF16 if dt == torch.bfloat16 else _abi.F32
-        _abi.check(L.ifx_kv_append(ks.data_ptr(), vs.data_ptr(), 3 * w, code(src_dt), kd.data_ptr(),
-                                   vd.data_ptr(), w, code(dst_dt), 11, t, w, stream_ptr()))
+        kd = torch.zeros(10 * P, w, device="cuda", dtype=dst_dt)
+        vd = torch.zeros_like(kd)
+        hk, hv = _HostBuf(6 * P * w * esz), _HostBuf(6 * P * w * esz)
+        pool = _pool(kd, vd, hk.ptr, hv.ptr, w, P, dst_dt)
+        # stream tokens [first, ...): token0 = first + 3 sits mid-page; pages on both tiers
+        slots_np = [7, -1 - 4, 2, -1 - 0, 9, 5]
+        slots = torch.tensor(slots_np, device="cuda", dtype=torch.int32)
+        first, token0 = 32, 35
+        _abi.check(L.ifx_kv_append(ks.data_ptr(), vs.data_ptr(), 3 * w, code(src_dt), ctypes.byref(pool),
+                                   slots.data_ptr(), first, token0, t, stream_ptr()))
         torch.cuda.synchronize()
-        assert torch.equal(kd[11:11 + t], ks.to(dst_dt))
-        assert torch.equal(vd[11:11 + t], vs.to(dst_dt))
-        assert kd[:11].abs().sum() == 0 and kd[11 + t:].abs().sum() == 0
-        rows = torch.tensor([12, 11, 40, 12], device="cuda", dtype=torch.int64)
-        ko = torch.empty(4, w, device="cuda", dtype=dst_dt)
+        hk_t = hk.bytes_view().view(dst_dt).view(-1, w)
+        for r in range(t):
+            rel = token0 + r - first
+            c = slots_np[rel // P]
+            row = (c if c >= 0 else -1 - c) * P + rel % P
+            got = kd[row].cpu() if c >= 0 else hk_t[row]
+            assert torch.equal(got, ks[r].to(dst_dt).cpu()), (r, c)
+        toks = torch.tensor([36, 35, 70, 36, 60], device="cuda", dtype=torch.int64)
+        ko = torch.empty(5, w, device="cuda", dtype=dst_dt)
         vo = torch.empty_like(ko)
-        _abi.check(L.ifx_kv_gather(kd.data_ptr(), vd.data_ptr(), w, code(dst_dt), rows.data_ptr(),
-                                   0, 4, w, ko.data_ptr(), vo.data_ptr(), stream_ptr()))
+        _abi.check(L.ifx_kv_gather(ctypes.byref(pool), slots.data_ptr(), first, toks.data_ptr(), 0, 5,
+                                   ko.data_ptr(), vo.data_ptr(), stream_ptr()))
         torch.cuda.synchronize()
-        assert torch.equal(ko, kd[rows]) and torch.equal(vo, vd[rows])
+        idx = (toks - token0).long()
+        assert torch.equal(ko, ks.to(dst_dt)[idx]) and torch.equal(vo, vs.to(dst_dt)[idx])
+        ko2 = torch.empty(t, w, device="cuda", dtype=dst_dt)
+        vo2 = torch.empty_like(ko2)
+        _abi.check(L.ifx_kv_gather(ctypes.byref(pool), slots.data_ptr(), first, None, token0, t,
+                                   ko2.data_ptr(), vo2.data_ptr(), stream_ptr()))
+        torch.cuda.synchronize()
+        assert torch.equal(ko2, ks.to(dst_dt)) and torch.equal(vo2, vs.to(dst_dt))
+        # K6: device slot 7 -> host slot 5, host slot 4 -> device slot 0 (whole pages)
+        before_d7, before_h4 = kd[7 * P:8 * P].cpu().clone(), hk_t[4 * P:5 * P].clone()
+        for d, pairs in ((0, [[7, 5]]), (1, [[0, 4]])):
+            mv = torch.tensor(pairs, device="cuda", dtype=torch.int64)
+            _abi.check(L.ifx_kv_move_pages(ctypes.byref(pool), mv.data_ptr(), 1, d, stream_ptr()))
+        torch.cuda.synchronize()
+        assert torch.equal(hk_t[5 * P:6 * P], before_d7)
+        assert torch.equal(kd[0:P].cpu(), before_h4)
+
+
+PAGED = [
+    # heads, head_dim, page_len, n_ctx, lo (window start inside the first page), n_cur, staged
+    (12, 128, 16, 9360, 0, 4680, False),
+    (2, 128, 16, 5000, 5, 300, True),
+    (3, 64, 8, 2600, 3, 257, True),
+    (2, 128, 32, 1000, 31, 0, False),
+    (1, 128, 128, 700, 100, 64, True),
+    (4, 64, 64, 37, 0, 128, True),
+]
+
+
+@pytest.mark.parametrize("case", PAGED)
+def test_paged_attention_matches_torch(case):
+    """K1 paged mode: context pages scattered over the pool (and the staging pool for
+    negative codes), window start inside the first page."""
+    from paper_2511_20714_b200._device import attn_fwd
+
+    heads, hd, P, n_ctx, lo, n_cur, staged = case
+    d = heads * hd
+    g = torch.Generator(device="cuda").manual_seed(hash(case) % 2**31)
+    n_q = 300
+    rows = lo + n_ctx
+    n_pages = -(-rows // P)
+    k_log = torch.randn(n_pages * P, d, device="cuda", generator=g).bfloat16()
+    v_log = torch.randn(n_pages * P, d, device="cuda", generator=g).bfloat16()
+    perm = torch.randperm(n_pages + 5, generator=torch.Generator().manual_seed(3))[:n_pages]
+    pool_k = torch.zeros((n_pages + 5) * P, d, device="cuda", dtype=torch.bfloat16)
+    pool_v = torch.zeros_like(pool_k)
+    stage_k = torch.zeros(n_pages * P, d, device="cuda", dtype=torch.bfloat16)
+    stage_v = torch.zeros_like(stage_k)
+    codes = []
+    for i in range(n_pages):
+        src = slice(i * P, (i + 1) * P)
+        if staged and i % 3 == 1:
+            stage_k[i * P:(i + 1) * P], stage_v[i * P:(i + 1) * P] = k_log[src], v_log[src]
+            codes.append(-1 - i)
+        else:
+            s = int(perm[i])
+            pool_k[s * P:(s + 1) * P], pool_v[s * P:(s + 1) * P] = k_log[src], v_log[src]
+            codes.append(s)
+    slots = torch.tensor(codes, device="cuda", dtype=torch.int32)
+    q = torch.randn(n_q, d, device="cuda", generator=g).bfloat16()
+    qkv = torch.randn(max(n_cur, 1), 3 * d, device="cuda", generator=g).bfloat16()[:n_cur]
+    kc, vc = qkv[:, d:2 * d], qkv[:, 2 * d:]
+    out = torch.empty(n_q, d, device="cuda", dtype=torch.bfloat16)
+    first = 1000 * P
+    attn_fwd(q, heads, hd, out, pool_k, pool_v, first + lo, n_ctx, kc if n_cur else None,
+             vc if n_cur else None, ctx_slots=slots, page_len=P, first_token=first,
+             stage_k=stage_k if staged else None, stage_v=stage_v if staged else None)
+    torch.cuda.synchronize()
+    k = torch.cat([k_log[lo:lo + n_ctx], kc])
+    v = torch.cat([v_log[lo:lo + n_ctx], vc])
+    ref = _ref_attn(q, k, v, heads)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
 
 
 def test_rms_matches_torch():

@@ -1,0 +1,112 @@
+"""CPU check of the physical tier logic in the native page table (csrc/pagetable.cpp):
+slot assignment and the drained page-move batches.
+
+A Python model of the two pools stands in for HBM / pinned host memory: each page's
+payload is written into its slot on append (as K2 does), each drained batch is executed
+as K6 would (every move of a batch concurrently), and after every call every live page's
+payload must sit in the slot of the tier the page table reports. Each batch must also be
+hazard-free (no slot both read and written, no slot written twice), which is what lets K6
+run a batch as one launch."""
+
+import numpy as np
+import pytest
+
+from paper_2511_20714_b200.kvcache import KvConfig, PageTable
+
+
+def _check_batches(mv):
+    for key in np.unique(mv[:, 0] * 4 + mv[:, 2] * 2 + mv[:, 1]):
+        b = mv[mv[:, 0] * 4 + mv[:, 2] * 2 + mv[:, 1] == key]
+        d = int(b[0, 2])
+        src = b[:, 4] if d == 1 else b[:, 3]
+        dst = b[:, 3] if d == 1 else b[:, 4]
+        assert len(set(dst.tolist())) == len(dst), "slot written twice in one batch"
+        # reads and writes of one batch are on different tiers, so they cannot collide;
+        # the sources must be distinct pages too
+        assert len(set(src.tolist())) == len(src)
+
+
+def _run(seed):
+    rng = np.random.default_rng(seed)
+    P = int(rng.integers(1, 6))
+    cfg = KvConfig(num_layers=2, head_dim=4, page_len=P,
+                   capacity_pages_device=int(rng.integers(0, 7)), capacity_pages_host=60)
+    pt = PageTable(cfg)
+    pools = {(k, t): {} for k in (0, 1) for t in (0, 1)}  # (kind, tier) -> slot -> payload
+    payload = {}  # page id -> token-start tag (what its rows hold)
+    kinds = ("self_attn", "cross_attn")
+
+    def execute():
+        mv = pt.drain_moves()
+        if len(mv):
+            _check_batches(mv)
+            key = mv[:, 0] * 4 + mv[:, 2] * 2 + mv[:, 1]
+            cuts = np.flatnonzero(np.diff(key)) + 1
+            for lo, hi in zip(np.r_[0, cuts], np.r_[cuts, len(mv)]):
+                b = mv[lo:hi]
+                kind, d = int(b[0, 1]), int(b[0, 2])
+                srct, dstt = (0, 1) if d == 0 else (1, 0)
+                vals = [pools[(kind, srct)].get(int(r[3] if d == 0 else r[4])) for r in b]
+                for r, val in zip(b, vals):
+                    pools[(kind, dstt)][int(r[4] if d == 0 else r[3])] = val
+
+    def verify():
+        st = pt.state()
+        for layer, kind, base, total, pages in st["streams"]:
+            if not pages:
+                continue
+            k = 0 if kind == "self_attn" else 1
+            codes, first = pt.slots(layer, kind, pages[0][3], total)
+            assert len(codes) == len(pages)
+            for (pid, tier, filled, start, _la), c in zip(pages, codes):
+                assert (c < 0) == (tier == 1)
+                slot = int(c) if c >= 0 else -1 - int(c)
+                assert pools[(k, tier)].get(slot) == payload[pid], (seed, pid)
+        ext = pt.pool_extent()
+        n_dev = sum(1 for s in st["streams"] for p in s[4] if p[1] == 0)
+        assert ext[0] + ext[2] <= max(cfg.capacity_pages_device, 0) + 2 * n_dev + 8
+
+    for _ in range(40):
+        op = rng.integers(0, 10)
+        layer, kind = int(rng.integers(0, 2)), kinds[int(rng.random() < 0.25)]
+        if op < 4:
+            rc, bid, start, written, pages = pt.append(layer, kind, int(rng.integers(1, 12)), 0)
+            if written:  # also after a CapacityError: rows already packed are written
+                k = 0 if kind == "self_attn" else 1
+                codes_all, first = pt.slots(layer, kind, start, start + written)
+                ids = [s for s in pt.state()["streams"] if s[0] == layer and s[1] == kind][0][4]
+                for p in ids:
+                    if p[0] not in payload:
+                        payload[p[0]] = (p[0], p[3])
+                for p, c in zip([p for p in ids if p[3] >= first], codes_all):
+                    tier = 0 if c >= 0 else 1
+                    slot = int(c) if c >= 0 else -1 - int(c)
+                    pools[(k, tier)][slot] = payload[p[0]]  # K2 writes the page's rows
+            execute()
+        elif op < 8:
+            base, total = pt.range(layer, kind)
+            if total > base:
+                if op == 7:
+                    pt.touch_indices(layer, kind, [int(x) for x in rng.integers(base, total, size=6)])
+                else:
+                    a = int(rng.integers(base, total))
+                    pt.touch_range(layer, kind, a, int(rng.integers(a, total + 1)))
+            execute()
+        elif op == 8:
+            st = pt.state()
+            ids = [b[0] for b in st["blocks"]]
+            if ids:
+                try:
+                    pt.offload([int(x) for x in rng.choice(ids, size=min(3, len(ids)), replace=False)])
+                except Exception:
+                    pass
+            execute()
+        else:
+            pt.evict_window(int(rng.integers(0, 25)))
+            execute()
+        verify()
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_tier_moves_keep_every_page_in_its_slot(seed):
+    _run(seed)
