@@ -304,8 +304,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (reference-seeded noise, PCG64 random-init weights)",
         "config": {"workload": c["desc"], "layers": mc.layers, "heads": mc.heads,
                    "head_dim": mc.head_dim, "tokens_per_block": T, "blocks": nb,
-                   "denoise_steps": len(STEPS), "kv_cache": "bf16 paged (page_len 16), HBM slabs",
-                   "l2": "inputs larger than L2 (weights 1.4 GB, KV slabs up to 6 GB)",
+                   "denoise_steps": len(STEPS), "kv_cache": "bf16 paged (page_len 16): HBM slot pool + pinned host tier",
+                   "l2": "inputs larger than L2 (weights 1.4 GB, KV pool up to 6 GB)",
                    "parallelism": "single GPU"},
         "attention_tflops": achieved,
         "attention_frac_of_peak": achieved / peak,

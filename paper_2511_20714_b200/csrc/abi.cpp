@@ -95,10 +95,16 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
     const int box = paged ? (int)p->ctx_page_len : 128;
     if ((rc = make_map(&a.tm_kc, p->k_ctx, p->ctx_rows, width, p->ctx_ld, box))) return rc;
     if ((rc = make_map(&a.tm_vc, p->v_ctx, p->ctx_rows, width, p->ctx_ld, box))) return rc;
+    if (paged) {
+      if ((rc = make_map(&a.tm_kc_run, p->k_ctx, p->ctx_rows, width, p->ctx_ld))) return rc;
+      if ((rc = make_map(&a.tm_vc_run, p->v_ctx, p->ctx_rows, width, p->ctx_ld))) return rc;
+    }
     if (paged && p->k_stage != nullptr && p->stage_rows > 0) {
       if (p->stage_rows % p->ctx_page_len) return fail(IFX_EDIM, "staging rows must be whole slots");
       if ((rc = make_map(&a.tm_ks, p->k_stage, p->stage_rows, width, p->ctx_ld, box))) return rc;
       if ((rc = make_map(&a.tm_vs, p->v_stage, p->stage_rows, width, p->ctx_ld, box))) return rc;
+      if ((rc = make_map(&a.tm_ks_run, p->k_stage, p->stage_rows, width, p->ctx_ld))) return rc;
+      if ((rc = make_map(&a.tm_vs_run, p->v_stage, p->stage_rows, width, p->ctx_ld))) return rc;
     }
   }
   if (p->n_cur > 0) {

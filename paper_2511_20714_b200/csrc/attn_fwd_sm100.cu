@@ -127,15 +127,7 @@ __device__ __forceinline__ Tile tile_of(const AttnKernelArgs& a, int j, int n0) 
   return t;
 }
 
-// paged context: slot of page `lane` of key tile j (clamped to the last page: rows past the
-// context are loaded from a finite page and masked)
-__device__ __forceinline__ int32_t tile_slot(const AttnKernelArgs& a, int j, int lane) {
-  const int n_pages = (a.n_ctx + a.ctx_page_len - 1) / a.ctx_page_len;
-  const int pg = min(j * (BN / a.ctx_page_len) + lane, n_pages - 1);
-  return __ldg(a.ctx_slots + pg);
-}
-
-template <int HD>
+template <int HD, bool PAGED>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ AttnKernelArgs a) {
   using L = Layout<HD>;
@@ -193,23 +185,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ===================== TMA producer =====================
-    // lane 0 drives the ring; for a paged context tile, lanes 0..ppt-1 each fetch one page
-    // (a page_len-row box per 64-column chunk) from the slot the page table assigned
-    const bool paged = a.ctx_slots != nullptr;
-    const int ppt = paged ? BN / a.ctx_page_len : 1;
-    const int prow_b = paged ? a.ctx_page_len * 128 : 0;  // smem bytes of one page box
-    const bool leader = lane == 0;
-    if (leader) {
+  if (warp == 0 && !PAGED) {
+    // ===================== TMA producer (contiguous context) =====================
+    if (elect_one()) {
       tma_prefetch_desc(&a.tm_q);
       if (n0 > 0) {
         tma_prefetch_desc(&a.tm_kc);
         tma_prefetch_desc(&a.tm_vc);
-      }
-      if (n0 > 0 && paged) {
-        tma_prefetch_desc(&a.tm_ks);
-        tma_prefetch_desc(&a.tm_vs);
       }
       if (n_total > n0) {
         tma_prefetch_desc(&a.tm_kn);
@@ -218,53 +200,99 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_expect_tx(q_full, L::Q_BYTES);
       for (int c = 0; c < L::KCH; ++c)
         tma_load_2d(sQ + c * BM * 128, &a.tm_q, q_full, head * HD + c * 64, q0);
-    }
-    int32_t slot_next = (paged && n_tiles > 0 && t0 < n0 && lane < ppt) ? tile_slot(a, t0, lane) : 0;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int s = j % NS;
-      const uint32_t ph = (j / NS) & 1;
-      const Tile t = tile_of(a, t0 + j, n0);
-      const int32_t slot = slot_next;
-      if (paged && j + 1 < n_tiles && t0 + j + 1 < n0 && lane < ppt)
-        slot_next = tile_slot(a, t0 + j + 1, lane);  // prefetch: hides the table load
-      const bool by_page = paged && t.seg == 0;
-      const CUtensorMap* mk = t.seg == 0 ? &a.tm_kc : &a.tm_kn;
-      const CUtensorMap* mv = t.seg == 0 ? &a.tm_vc : &a.tm_vn;
-      if (leader) {
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % NS;
+        const uint32_t ph = (j / NS) & 1;
+        const Tile t = tile_of(a, t0 + j, n0);
+        const CUtensorMap* mk = t.seg == 0 ? &a.tm_kc : &a.tm_kn;
+        const CUtensorMap* mv = t.seg == 0 ? &a.tm_vc : &a.tm_vn;
         mbar_wait(k_empty + s, ph ^ 1);
         mbar_expect_tx(k_full + s, L::KV_BYTES);
-      }
-      __syncwarp();
-      if (by_page) {
-        if (lane < ppt) {
-          const CUtensorMap* m = slot >= 0 ? &a.tm_kc : &a.tm_ks;
-          const int r = (slot >= 0 ? slot : -1 - slot) * a.ctx_page_len;
-          for (int c = 0; c < L::KCH; ++c)
-            tma_load_2d(sK + s * L::KV_BYTES + c * BN * 128 + lane * prow_b, m, k_full + s,
-                        head * HD + c * 64, r);
-        }
-      } else if (leader) {
         for (int c = 0; c < L::KCH; ++c)
           tma_load_2d(sK + s * L::KV_BYTES + c * BN * 128, mk, k_full + s, head * HD + c * 64,
                       t.row);
-      }
-      if (leader) {
         mbar_wait(v_empty + s, ph ^ 1);
         mbar_expect_tx(v_full + s, L::KV_BYTES);
-      }
-      __syncwarp();
-      if (by_page) {
-        if (lane < ppt) {
-          const CUtensorMap* m = slot >= 0 ? &a.tm_vc : &a.tm_vs;
-          const int r = (slot >= 0 ? slot : -1 - slot) * a.ctx_page_len;
-          for (int c = 0; c < L::KCH; ++c)
-            tma_load_2d(sV + s * L::KV_BYTES + c * BN * 128 + lane * prow_b, m, v_full + s,
-                        head * HD + c * 64, r);
-        }
-      } else if (leader) {
         for (int c = 0; c < L::KCH; ++c)
           tma_load_2d(sV + s * L::KV_BYTES + c * BN * 128, mv, v_full + s, head * HD + c * 64,
                       t.row);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 0) {
+    // ===================== TMA producer (paged context) =====================
+    // One elected thread, like the contiguous path. A context tile whose ppt pages sit in
+    // consecutive slots of one pool (the common case: a block's appends take consecutive
+    // slots) is one 128-row box per 64-column chunk; otherwise every page is its own
+    // page_len-row box from the slot the page table assigned. The slot codes of tile j+1
+    // are loaded at the end of iteration j, so the table reads hide behind the ring waits.
+    if (elect_one()) {
+      constexpr int MAXP = BN / 8;  // pages per tile at the smallest page_len
+      const int ppt = BN / a.ctx_page_len;
+      const int prow_b = a.ctx_page_len * 128;  // smem bytes of one page box
+      const int n_pages = (a.n_ctx + a.ctx_page_len - 1) / a.ctx_page_len;
+      tma_prefetch_desc(&a.tm_q);
+      if (n0 > 0) {
+        tma_prefetch_desc(&a.tm_kc);
+        tma_prefetch_desc(&a.tm_vc);
+        tma_prefetch_desc(&a.tm_kc_run);
+        tma_prefetch_desc(&a.tm_vc_run);
+      }
+      if (n_total > n0) {
+        tma_prefetch_desc(&a.tm_kn);
+        tma_prefetch_desc(&a.tm_vn);
+      }
+      mbar_expect_tx(q_full, L::Q_BYTES);
+      for (int c = 0; c < L::KCH; ++c)
+        tma_load_2d(sQ + c * BM * 128, &a.tm_q, q_full, head * HD + c * 64, q0);
+      int32_t sl[MAXP];
+      auto load_slots = [&](int tile) {
+#pragma unroll
+        for (int i = 0; i < MAXP; ++i)
+          if (i < ppt) sl[i] = __ldg(a.ctx_slots + min(tile * ppt + i, n_pages - 1));
+      };
+      if (n_tiles > 0 && t0 < n0) load_slots(t0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % NS;
+        const uint32_t ph = (j / NS) & 1;
+        const Tile t = tile_of(a, t0 + j, n0);
+        const bool ctx = t.seg == 0;
+        bool run = ctx;
+#pragma unroll
+        for (int i = 1; i < MAXP; ++i)
+          if (i < ppt) run = run && sl[i] == sl[0] + (sl[0] >= 0 ? i : -i);
+        const int32_t phys0 = sl[0] >= 0 ? sl[0] : -1 - sl[0];
+        for (int kv = 0; kv < 2; ++kv) {
+          uint64_t* full = (kv == 0 ? k_full : v_full) + s;
+          uint64_t* empty = (kv == 0 ? k_empty : v_empty) + s;
+          uint8_t* dst = (kv == 0 ? sK : sV) + s * L::KV_BYTES;
+          mbar_wait(empty, ph ^ 1);
+          mbar_expect_tx(full, L::KV_BYTES);
+          if (!ctx) {
+            const CUtensorMap* m = kv == 0 ? &a.tm_kn : &a.tm_vn;
+            for (int c = 0; c < L::KCH; ++c)
+              tma_load_2d(dst + c * BN * 128, m, full, head * HD + c * 64, t.row);
+          } else if (run) {
+            const CUtensorMap* m = sl[0] >= 0 ? (kv == 0 ? &a.tm_kc_run : &a.tm_vc_run)
+                                              : (kv == 0 ? &a.tm_ks_run : &a.tm_vs_run);
+            for (int c = 0; c < L::KCH; ++c)
+              tma_load_2d(dst + c * BN * 128, m, full, head * HD + c * 64,
+                          phys0 * a.ctx_page_len);
+          } else {
+#pragma unroll
+            for (int i = 0; i < MAXP; ++i) {
+              if (i < ppt) {
+                const int32_t c0 = sl[i];
+                const CUtensorMap* m = c0 >= 0 ? (kv == 0 ? &a.tm_kc : &a.tm_vc)
+                                               : (kv == 0 ? &a.tm_ks : &a.tm_vs);
+                const int row = (c0 >= 0 ? c0 : -1 - c0) * a.ctx_page_len;
+                for (int c = 0; c < L::KCH; ++c)
+                  tma_load_2d(dst + c * BN * 128 + i * prow_b, m, full, head * HD + c * 64, row);
+              }
+            }
+          }
+        }
+        if (j + 1 < n_tiles && t0 + j + 1 < n0) load_slots(t0 + j + 1);
       }
     }
     __syncwarp();
@@ -564,11 +592,13 @@ __global__ void attn_combine_kernel(const AttnKernelArgs a) {
 template <int HD>
 int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
   using L = Layout<HD>;
-  auto* fn = attn_fwd_kernel<HD>;
+  auto* fn = a.ctx_slots != nullptr ? attn_fwd_kernel<HD, true> : attn_fwd_kernel<HD, false>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-    if (e != cudaSuccess) return (int)e;
+    for (auto* f : {attn_fwd_kernel<HD, true>, attn_fwd_kernel<HD, false>}) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+      if (e != cudaSuccess) return (int)e;
+    }
     attr_set = true;
   }
   dim3 grid((n_q + BM - 1) / BM, heads, a.n_splits);

@@ -14,6 +14,10 @@ struct AttnKernelArgs {
   CUtensorMap tm_vc;  // V context
   CUtensorMap tm_ks;  // paged only: K staging pool (slot codes < 0), box page_len
   CUtensorMap tm_vs;  // V staging pool
+  CUtensorMap tm_kc_run;  // paged only: the pools again with 128-row boxes, for tiles whose
+  CUtensorMap tm_vc_run;  // pages are one consecutive run of slots
+  CUtensorMap tm_ks_run;
+  CUtensorMap tm_vs_run;
   CUtensorMap tm_kn;  // K of the current block [n_cur, H*dh]
   CUtensorMap tm_vn;  // V of the current block
   int n_q, n_ctx, n_cur, ctx_row0;

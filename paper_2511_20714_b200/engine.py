@@ -460,9 +460,20 @@ class _KvContext:
             if hi > lo:
                 cache.touch_range(li, (lo, hi), SELF_ATTN)
             self.ranges.append((lo, hi))
+        self.prepared = False
+
+    def prepare(self) -> None:
+        """Slot tables + staging of the block, once every fetch of the block is done (the
+        cross-attention fetch that follows the context fetch, engine.py:297-298, may still
+        demote context pages to the host tier)."""
+        if self.prepared:
+            return
+        self.prepared = True
+        cache, stager, L = self.cache, self.stager, self.L
         self.first = [0] * L
         self.host_moves = [None] * L
         self.buf_of = [0] * L
+        self.moves_dev = None
         if not self.paged:
             return
         tables, host = [], []
@@ -476,17 +487,17 @@ class _KvContext:
         if per_layer:
             slot_b = self.P * W * self.pool.esz
             total = sum(len(h) for h in host)
-            if total * slot_b <= stager.budget or L == 1:
-                nbuf, self.buf_of = L, list(range(L))   # stage once per block
+            self.once = bool(total * slot_b <= stager.budget or L <= 3)
+            if self.once:  # every layer its own region: staged once per block
+                self.buf_of = list(range(L))
                 offs = np.cumsum([0] + [len(h) for h in host])
-            else:
-                nbuf = 2 if L % 2 == 0 else 3
+            else:          # 2 rotating buffers (3 for an odd layer count)
                 self.buf_of = [li % 2 for li in range(L)]
                 if L % 2:
                     self.buf_of[L - 1] = 2
                 offs = [self.buf_of[li] * per_layer for li in range(L)]
-            self.once = nbuf == L
-            stager.ensure(int(offs[-1]) if self.once else nbuf * per_layer, self.P, W, self.pool.dtype)
+            need = max(int(offs[li]) + len(h) for li, h in enumerate(host))
+            stager.ensure(need, self.P, W, self.pool.dtype)
             for li, h in enumerate(host):
                 if len(h):
                     hs = -1 - tables[li][h].astype(np.int64)
@@ -500,7 +511,6 @@ class _KvContext:
         lens = np.cumsum([0] + [len(t) for t in tables])
         self.tables = [allt[lens[i]:lens[i + 1]] for i in range(L)]
         mv = [m for m in self.host_moves if m is not None]
-        self.moves_dev = None
         if mv:
             allm = torch.from_numpy(np.concatenate(mv)).to(dev, non_blocking=True)
             self.moves_dev, o = [None] * L, 0
@@ -544,6 +554,7 @@ class _KvContext:
     def attend(self, li: int, q, heads: int, dhp: int, out, cur_k, cur_v, scale: float, attn=None):
         """K1 for layer li: q over [this layer's cached context ∥ the block's own K/V]."""
         attn = attn or attn_fwd
+        self.prepare()
         lo, hi = self.ranges[li]
         call = self.calls
         self.calls += 1
@@ -674,6 +685,8 @@ def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSche
     runner = _runner(model)
     ctx = _ctx_from_cache(model, cache, runner.stager, passes=len(schedule.steps) + 1)
     cross = _cross_from_cache(model, cache, prompt_ctx)
+    if ctx is not None:
+        ctx.prepare()
     runner.denoise(lat, schedule, ctx, cross, cache, chunk_index)
     if not to_host:
         return GeneratedBlock(chunk_index, lat, [], prompt_text)

@@ -404,6 +404,7 @@ class UlyssesEngine:
             lat = full[rank * n:(rank + 1) * n].to(m.time_vec.device, torch.float32).clone()
             ctx = _ctx_from_cache(m, self.cache, r.stager, passes=len(request.schedule.steps) + 1)
             cross = _cross_from_cache(m, self.cache, None)
+            ctx.prepare()  # slot tables once the block's fetches (self, then cross) are done
             r.denoise(lat, request.schedule, ctx, cross, self.cache, chunk)
             if request.kv_window is not None:
                 self.cache.evict_window(request.kv_window)

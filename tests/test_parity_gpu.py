@@ -349,9 +349,10 @@ def test_long_context_c3_bookkeeping_bit_exact():
 # ---------------------------------------------------------------- pinned-host tier
 @pytest.mark.parametrize("case", [
     # layers, page_len, device capacity (pages), stage budget (bytes), window
-    (3, 16, 10, 0, None),          # rotating 3-buffer staging (odd layer count)
-    (2, 16, 7, 0, None),           # rotating 2-buffer staging
+    (5, 16, 18, 0, None),          # rotating 3-buffer staging (odd layer count)
+    (4, 16, 14, 0, None),          # rotating 2-buffer staging
     (3, 16, 12, 1 << 30, None),    # every layer's host pages staged once per block
+    (2, 16, 7, 0, None),           # few layers: staged once per block regardless of budget
     (2, 8, 9, 0, 70),              # 8-row pages + window eviction
     (2, 12, 8, 0, None),           # page_len K1 cannot box: K7 gather fallback
 ])

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--heads", type=int, default=12)
     ap.add_argument("--no-split", action="store_true")
+    ap.add_argument("--paged", action="store_true", help="context through a page_len-16 slot table")
     args = ap.parse_args()
     T, H, dh = 4680, args.heads, 128
     D = H * dh
@@ -29,8 +30,16 @@ def main():
         ks = torch.randn(max(C, 1), D, device="cuda").bfloat16()
         vs = torch.randn(max(C, 1), D, device="cuda").bfloat16()
         out = torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
-        f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:],
-                             split_kv=not args.no_split)
+        kw = {}
+        if args.paged and C:  # engine layout: page k of the stream in slot k (appends are in order)
+            P = 16
+            n_pages = -(-C // P)
+            ks = torch.randn(n_pages * P, D, device="cuda").bfloat16()
+            vs = torch.randn(n_pages * P, D, device="cuda").bfloat16()
+            kw = dict(ctx_slots=torch.arange(n_pages, device="cuda", dtype=torch.int32), page_len=P,
+                      first_token=0)
+        f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:],  # noqa: E731
+                             split_kv=not args.no_split, **kw)
         for _ in range(3):
             f()
         torch.cuda.synchronize()

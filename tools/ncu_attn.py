@@ -1,17 +1,27 @@
-"""One K1 launch at the c2 shape with b cached blocks, for `ncu --set full` (-k regex:attn)."""
+"""One K1 launch at the c2 shape with b cached blocks, for `ncu --set full` (-k regex:attn).
+
+    python tools/ncu_attn.py [b] [--paged]
+
+--paged: the context comes through a page_len-16 slot table (engine layout, consecutive
+slots), i.e. the attn_fwd_kernel<128, true> variant."""
 import sys
 
 import torch
 
 from paper_2511_20714_b200._device import attn_fwd
 
-b = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-T, H, dh = 4680, 12, 128
+b = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 3
+paged = "--paged" in sys.argv
+T, H, dh, P = 4680, 12, 128, 16
 D = H * dh
+C = b * T
+rows = -(-max(C, 1) // P) * P
 qkv = torch.randn(T, 3 * D, device="cuda").bfloat16()
-ks = torch.randn(max(b * T, 1), D, device="cuda").bfloat16()
-vs = torch.randn(max(b * T, 1), D, device="cuda").bfloat16()
+ks = torch.randn(rows, D, device="cuda").bfloat16()
+vs = torch.randn(rows, D, device="cuda").bfloat16()
 out = torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
+kw = dict(ctx_slots=torch.arange(rows // P, device="cuda", dtype=torch.int32), page_len=P,
+          first_token=0) if paged and C else {}
 for _ in range(3):
-    attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, b * T, qkv[:, D:2 * D], qkv[:, 2 * D:])
+    attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:], **kw)
 torch.cuda.synchronize()
