@@ -59,6 +59,13 @@ CONFIGS = {
     "c4": dict(layers=40, heads=40, head_dim=128, block_len=4680, blocks=3, frame_shape=(16, 16),
                weights="device",
                desc="c4: Wan2.1-14B-shaped (40L, 40 heads x 128, dim 5120), 3 blocks, 4 steps"),
+    # c5 on ONE GPU: the cache of a minute-long rollout does not fit HBM, so the pinned host
+    # tier is live. Blocks [0, prefill) are appended from synthetic K/V (no denoising), then
+    # `blocks` more are generated through generate_block and timed.
+    "c5": dict(layers=40, heads=40, head_dim=128, block_len=4680, blocks=2, prefill=60,
+               device_blocks=36, frame_shape=(16, 16), weights="device",
+               desc="c5: Wan2.1-14B-shaped LV rollout on 1 GPU: 60 cached blocks (36 blocks of "
+                    "pages in HBM, the rest on the pinned host tier), blocks 61-62 timed"),
 }
 
 
@@ -222,6 +229,8 @@ def run_ours(args):
     c = CONFIGS[cfgname]
     if world > 1:
         return run_ulysses_bench(args, c, cfgname, world, rank, local)
+    if "prefill" in c:
+        return run_host_tier_bench(args, c, cfgname, local)
 
     from paper_2511_20714_b200 import _device
     from paper_2511_20714_b200 import engine as E
@@ -321,6 +330,99 @@ def run_ours(args):
         "host_enqueue_ms_per_step": host_ms,
         "clocks": clocks,
         "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_host_tier_bench(args, c, cfgname, local):
+    """c5: steady state of a rollout whose KV cache exceeds HBM (reference tier semantics:
+    device-first allocation with host spill, restore-on-fetch with LRU demotion,
+    kvcache.py:126-175). Prefill appends synthetic K/V for `prefill` blocks through the
+    cache API; then each timed step generates one block (engine.py:285-312) over the
+    whole cache: tier moves at the context fetch (K6), device pages read in place by K1,
+    host pages staged H2D on the side stream one layer ahead."""
+    import torch
+
+    from paper_2511_20714_b200 import _device
+    from paper_2511_20714_b200 import engine as E
+    from paper_2511_20714_b200.kvcache import CROSS_ATTN, SELF_ATTN, KvCache
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
+                       block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
+                       weight_seed=0)
+    model = E.build_model(mc, weights=c["weights"])
+    T, L, W = mc.block_len, mc.layers, model.attn_width
+    pages_blk = -(-T // 16)
+    nb_pre, nb = c["prefill"], max(c["blocks"], args.steps)
+    kvc = E.default_kv_config(mc, capacity_pages_device=c["device_blocks"] * L * pages_blk,
+                              capacity_pages_host=(nb_pre + nb + 2) * L * pages_blk)
+    cache = KvCache(kvc, dtype=torch.bfloat16, reserve_tokens=T * c["device_blocks"], row_width=W)
+    host_slots = (nb_pre + nb + 2 - c["device_blocks"]) * L * pages_blk
+    t0 = time.perf_counter()
+    cache.pool(SELF_ATTN).ensure(0, host_slots)  # pinned + mapped + zeroed once, up front
+    host_alloc_s = time.perf_counter() - t0
+    emb = E.embed_prompt(model, "a quiet scene")
+    for li, (kc, vc) in enumerate(E._cross_kv(model, emb)):
+        cache.append_block(li, kc, vc, kind=CROSS_ATTN, chunk_index=0)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    kv = [torch.randn(T, W, device="cuda", generator=g).bfloat16() for _ in range(2)]
+    t0 = time.perf_counter()
+    for b in range(nb_pre):
+        for li in range(L):
+            cache.append_block(li, kv[0], kv[1], kind=SELF_ATTN, chunk_index=b)
+    torch.cuda.synchronize()
+    prefill_s = time.perf_counter() - t0
+    sched = E.DenoiseSchedule(STEPS)
+    noise = torch.randn(T, mc.model_dim, device="cuda", generator=g)
+    runner = E._runner(model)
+
+    def block(ch):
+        return E.generate_block(model, cache, sched, None, ch, 0, noise=noise.clone(), to_host=False)
+
+    for w in range(min(args.warmup, 1)):  # one warm block (the cache keeps growing)
+        block(nb_pre + w)
+    torch.cuda.synchronize()
+    ch0 = nb_pre + min(args.warmup, 1)
+    runner.attn_events = []
+    mv0, st0 = list(cache.moved_pages), runner.stager.staged_pages
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.steps):
+            block(ch0 + i)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    attn_ms = sum(a.elapsed_time(b) for a, b in runner.attn_events) / args.steps
+    runner.attn_events = None
+    P = len(STEPS) + 1
+    flops = sum(4.0 * T * (b * T + T) * mc.model_dim * L * P for b in range(ch0, ch0 + args.steps)) / args.steps
+    peak, peak_src = load_peaks()
+    page_b = 2 * 16 * W * 2  # K + V bytes of one page
+    moved = [(a - b) * page_b / args.steps for a, b in zip(cache.moved_pages, mv0)]
+    staged = (runner.stager.staged_pages - st0) * page_b / args.steps
+    st = cache.memory_stats()
+    line = {
+        "metric": METRIC, "value": FRAMES_PER_BLOCK / (ms / 1e3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (prefill K/V and noise from torch.randn, random-init weights)",
+        "config": {"workload": c["desc"], "step": "one generated block (4 steps + clean pass)",
+                   "cached_blocks": [ch0, ch0 + args.steps - 1],
+                   "device_pages": st.device_pages_used, "host_pages": st.host_pages_used,
+                   "prefill_s": prefill_s, "host_pool_alloc_s": host_alloc_s,
+                   "host_pool_GB": host_slots * 2 * 16 * W * 2 / 1e9},
+        "roofline": {"bound": "tensor", "achieved": flops / (attn_ms / 1e3) / 1e12, "peak": peak,
+                     "unit": "TFLOP/s", "frac": flops / (attn_ms / 1e3) / 1e12 / peak,
+                     "traffic": None, "peak_source": peak_src, "kernel": "K1 (paged)",
+                     "kernel_ms_per_step": attn_ms, "share_of_step": attn_ms / ms},
+        "host_tier": {"d2h_bytes_per_step": moved[0], "h2d_bytes_per_step": moved[1],
+                      "staged_h2d_bytes_per_step": staged,
+                      "pcie_GBps_if_serial": (moved[0] + moved[1] + staged) / (ms / 1e3) / 1e9},
+        "gpu_launches": None, "clocks": clk.summary(), "cpu_baseline": None,
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -189,6 +189,11 @@ typedef struct ifx_attn_params {
   const void* k_stage;
   const void* v_stage;
   int64_t stage_rows;
+  /* optional (paged): per 128-key tile of the context, counted from ctx_first_token, the
+   * code of its first page when the tile's pages are consecutive slots of one pool (device
+   * codes ascending or staging codes descending), else INT32_MIN. Lets K1 load such a
+   * tile as one 128-row box with one table read; NULL = K1 checks the slots itself. */
+  const int32_t* ctx_tile_runs;
   /* optional device scratch for split-KV (size from ifx_attn_workspace_bytes). When given
    * and (query tiles x heads) would leave the SMs under-filled (e.g. a Ulysses rank holding
    * few heads), the key range is split across CTAs and merged by a combine kernel

@@ -71,6 +71,7 @@ class AttnParams(ctypes.Structure):
         ("ctx_slots", ctypes.c_void_p), ("ctx_page_len", ctypes.c_int64),
         ("ctx_first_token", ctypes.c_int64),
         ("k_stage", ctypes.c_void_p), ("v_stage", ctypes.c_void_p), ("stage_rows", ctypes.c_int64),
+        ("ctx_tile_runs", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_int64),
     ]
 

@@ -75,14 +75,14 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
              row_max: torch.Tensor | None = None, row_sum: torch.Tensor | None = None,
              split_kv: bool = True, stream=None, ctx_slots: torch.Tensor | None = None,
              page_len: int = 0, first_token: int = 0, stage_k: torch.Tensor | None = None,
-             stage_v: torch.Tensor | None = None) -> torch.Tensor:
+             stage_v: torch.Tensor | None = None, tile_runs: torch.Tensor | None = None) -> torch.Tensor:
     """Enqueue K1 (attn_fwd_sm100.cu): out = softmax(q [ctx∥cur]^T * scale) [ctx∥cur].
 
     q/out: [n_q, heads*head_dim] bf16 (row-strided views allowed). cur_*: [n_cur,
     heads*head_dim] views. Context, contiguous: rows [ctx_row0, ctx_row0+n_ctx) of ctx_k/v.
     Paged (ctx_slots given): ctx_k/v are the KV pool, the context is tokens [ctx_row0,
     ctx_row0+n_ctx) whose pages from first_token on sit in slot codes ctx_slots (int32
-    device tensor; codes < 0 address stage_k/v).
+    device tensor; codes < 0 address stage_k/v); tile_runs = tile_run_codes(codes, page_len).
     """
     p = _abi.AttnParams()
     p.q, p.q_ld, p.n_q = q.data_ptr(), row_ld(q), q.shape[0]
@@ -92,6 +92,8 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
         p.ctx_row0, p.n_ctx = ctx_row0, n_ctx
         if ctx_slots is not None:
             p.ctx_slots, p.ctx_page_len, p.ctx_first_token = ctx_slots.data_ptr(), page_len, first_token
+            if tile_runs is not None:
+                p.ctx_tile_runs = tile_runs.data_ptr()
             if stage_k is not None:
                 p.k_stage, p.v_stage, p.stage_rows = stage_k.data_ptr(), stage_v.data_ptr(), stage_k.shape[0]
     if cur_k is not None and cur_k.shape[0] > 0:
@@ -114,6 +116,22 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
     _abi.check(rc, "attn_fwd")
     LAUNCHES[0] += 1
     return out
+
+
+def tile_run_codes(codes: np.ndarray, page_len: int) -> np.ndarray:
+    """Per 128-key tile of a paged context (K1's ctx_tile_runs): the first page's slot code
+    when the tile's pages are one consecutive run of one pool, else INT32_MIN. The last
+    tile counts as a run only if it has all its pages (K1 then reads finite rows past the
+    context end and masks them)."""
+    ppt = 128 // page_len
+    n = len(codes)
+    n_tiles = -(-n // ppt)
+    pad = np.full(n_tiles * ppt, np.iinfo(np.int32).min, dtype=np.int64)
+    pad[:n] = codes
+    t = pad.reshape(n_tiles, ppt)
+    step = np.where(t[:, :1] >= 0, 1, -1)
+    run = (t == t[:, :1] + step * np.arange(ppt)[None, :]).all(axis=1) & (t[:, -1] != np.iinfo(np.int32).min)
+    return np.where(run, t[:, 0], np.iinfo(np.int32).min).astype(np.int32)
 
 
 def rms_bf16(x: torch.Tensor, out: torch.Tensor, tvec: torch.Tensor | None = None,

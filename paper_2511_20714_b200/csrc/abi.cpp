@@ -119,6 +119,7 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
     const int64_t lo = p->ctx_row0 - p->ctx_first_token;
     if (lo + p->n_ctx > INT32_MAX) return fail(IFX_EDIM, "attention extents must fit int32");
     a.ctx_slots = p->ctx_slots;
+    a.ctx_tile_runs = p->ctx_tile_runs;
     a.ctx_page_len = (int)p->ctx_page_len;
     a.ctx_lo = (int)lo;
     a.n_ctx = (int)(lo + p->n_ctx);  // rows from the first page's start

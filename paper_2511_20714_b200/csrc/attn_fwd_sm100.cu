@@ -31,6 +31,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 
 #include "attn_kernel.h"
@@ -221,20 +222,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncwarp();
   } else if (warp == 0) {
     // ===================== TMA producer (paged context) =====================
-    // One elected thread, like the contiguous path. A context tile whose ppt pages sit in
+    // One elected thread, like the contiguous path (its instructions share sub-partition 0
+    // with two softmax warps, so it is kept lean). A context tile whose pages sit in
     // consecutive slots of one pool (the common case: a block's appends take consecutive
     // slots) is one 128-row box per 64-column chunk; otherwise every page is its own
-    // page_len-row box from the slot the page table assigned. The slot codes of tile j+1
-    // are loaded at the end of iteration j, so the table reads hide behind the ring waits.
+    // page_len-row box from its slot. The caller's per-tile run codes (ctx_tile_runs)
+    // make the common case one table load per tile, prefetched a tile ahead; without
+    // them the tile's page slots are loaded and compared here.
     if (elect_one()) {
       constexpr int MAXP = BN / 8;  // pages per tile at the smallest page_len
+      constexpr int32_t kNoRun = INT32_MIN;
       const int ppt = BN / a.ctx_page_len;
       const int prow_b = a.ctx_page_len * 128;  // smem bytes of one page box
       const int n_pages = (a.n_ctx + a.ctx_page_len - 1) / a.ctx_page_len;
+      const int32_t* runs = a.ctx_tile_runs;
       tma_prefetch_desc(&a.tm_q);
       if (n0 > 0) {
-        tma_prefetch_desc(&a.tm_kc);
-        tma_prefetch_desc(&a.tm_vc);
         tma_prefetch_desc(&a.tm_kc_run);
         tma_prefetch_desc(&a.tm_vc_run);
       }
@@ -245,54 +248,69 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_expect_tx(q_full, L::Q_BYTES);
       for (int c = 0; c < L::KCH; ++c)
         tma_load_2d(sQ + c * BM * 128, &a.tm_q, q_full, head * HD + c * 64, q0);
-      int32_t sl[MAXP];
-      auto load_slots = [&](int tile) {
-#pragma unroll
-        for (int i = 0; i < MAXP; ++i)
-          if (i < ppt) sl[i] = __ldg(a.ctx_slots + min(tile * ppt + i, n_pages - 1));
-      };
-      if (n_tiles > 0 && t0 < n0) load_slots(t0);
+      int32_t rnext = (runs != nullptr && n_tiles > 0 && t0 < n0) ? __ldg(runs + t0) : kNoRun;
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % NS;
         const uint32_t ph = (j / NS) & 1;
         const Tile t = tile_of(a, t0 + j, n0);
-        const bool ctx = t.seg == 0;
-        bool run = ctx;
+        int32_t rc = rnext;
+        if (runs != nullptr && j + 1 < n_tiles && t0 + j + 1 < n0) rnext = __ldg(runs + t0 + j + 1);
+        int32_t sl[MAXP];
+        if (t.seg == 0 && rc == kNoRun) {  // page by page (or detect the run here)
 #pragma unroll
-        for (int i = 1; i < MAXP; ++i)
-          if (i < ppt) run = run && sl[i] == sl[0] + (sl[0] >= 0 ? i : -i);
-        const int32_t phys0 = sl[0] >= 0 ? sl[0] : -1 - sl[0];
-        for (int kv = 0; kv < 2; ++kv) {
-          uint64_t* full = (kv == 0 ? k_full : v_full) + s;
-          uint64_t* empty = (kv == 0 ? k_empty : v_empty) + s;
-          uint8_t* dst = (kv == 0 ? sK : sV) + s * L::KV_BYTES;
-          mbar_wait(empty, ph ^ 1);
-          mbar_expect_tx(full, L::KV_BYTES);
-          if (!ctx) {
-            const CUtensorMap* m = kv == 0 ? &a.tm_kn : &a.tm_vn;
-            for (int c = 0; c < L::KCH; ++c)
-              tma_load_2d(dst + c * BN * 128, m, full, head * HD + c * 64, t.row);
-          } else if (run) {
-            const CUtensorMap* m = sl[0] >= 0 ? (kv == 0 ? &a.tm_kc_run : &a.tm_vc_run)
-                                              : (kv == 0 ? &a.tm_ks_run : &a.tm_vs_run);
-            for (int c = 0; c < L::KCH; ++c)
-              tma_load_2d(dst + c * BN * 128, m, full, head * HD + c * 64,
-                          phys0 * a.ctx_page_len);
-          } else {
+          for (int i = 0; i < MAXP; ++i)
+            if (i < ppt) sl[i] = __ldg(a.ctx_slots + min((t0 + j) * ppt + i, n_pages - 1));
+          if (runs == nullptr) {
+            bool run = true;
+#pragma unroll
+            for (int i = 1; i < MAXP; ++i)
+              if (i < ppt) run = run && sl[i] == sl[0] + (sl[0] >= 0 ? i : -i);
+            if (run) rc = sl[0];
+          }
+        }
+        if (t.seg != 0) {
+          mbar_wait(k_empty + s, ph ^ 1);
+          mbar_expect_tx(k_full + s, L::KV_BYTES);
+          for (int c = 0; c < L::KCH; ++c)
+            tma_load_2d(sK + s * L::KV_BYTES + c * BN * 128, &a.tm_kn, k_full + s,
+                        head * HD + c * 64, t.row);
+          mbar_wait(v_empty + s, ph ^ 1);
+          mbar_expect_tx(v_full + s, L::KV_BYTES);
+          for (int c = 0; c < L::KCH; ++c)
+            tma_load_2d(sV + s * L::KV_BYTES + c * BN * 128, &a.tm_vn, v_full + s,
+                        head * HD + c * 64, t.row);
+        } else if (rc != kNoRun) {
+          const bool dev = rc >= 0;
+          const int row = (dev ? rc : -1 - rc) * a.ctx_page_len;
+          mbar_wait(k_empty + s, ph ^ 1);
+          mbar_expect_tx(k_full + s, L::KV_BYTES);
+          for (int c = 0; c < L::KCH; ++c)
+            tma_load_2d(sK + s * L::KV_BYTES + c * BN * 128, dev ? &a.tm_kc_run : &a.tm_ks_run,
+                        k_full + s, head * HD + c * 64, row);
+          mbar_wait(v_empty + s, ph ^ 1);
+          mbar_expect_tx(v_full + s, L::KV_BYTES);
+          for (int c = 0; c < L::KCH; ++c)
+            tma_load_2d(sV + s * L::KV_BYTES + c * BN * 128, dev ? &a.tm_vc_run : &a.tm_vs_run,
+                        v_full + s, head * HD + c * 64, row);
+        } else {
+          for (int kv = 0; kv < 2; ++kv) {
+            uint64_t* full = (kv == 0 ? k_full : v_full) + s;
+            uint8_t* dst = (kv == 0 ? sK : sV) + s * L::KV_BYTES;
+            mbar_wait((kv == 0 ? k_empty : v_empty) + s, ph ^ 1);
+            mbar_expect_tx(full, L::KV_BYTES);
 #pragma unroll
             for (int i = 0; i < MAXP; ++i) {
               if (i < ppt) {
-                const int32_t c0 = sl[i];
-                const CUtensorMap* m = c0 >= 0 ? (kv == 0 ? &a.tm_kc : &a.tm_vc)
-                                               : (kv == 0 ? &a.tm_ks : &a.tm_vs);
-                const int row = (c0 >= 0 ? c0 : -1 - c0) * a.ctx_page_len;
+                const bool dev = sl[i] >= 0;
+                const CUtensorMap* m = dev ? (kv == 0 ? &a.tm_kc : &a.tm_vc)
+                                           : (kv == 0 ? &a.tm_ks : &a.tm_vs);
+                const int row = (dev ? sl[i] : -1 - sl[i]) * a.ctx_page_len;
                 for (int c = 0; c < L::KCH; ++c)
                   tma_load_2d(dst + c * BN * 128 + i * prow_b, m, full, head * HD + c * 64, row);
               }
             }
           }
         }
-        if (j + 1 < n_tiles && t0 + j + 1 < n0) load_slots(t0 + j + 1);
       }
     }
     __syncwarp();

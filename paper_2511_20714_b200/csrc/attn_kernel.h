@@ -28,6 +28,7 @@ struct AttnKernelArgs {
   // [0, ctx_lo) precede the addressable window and are masked
   int ctx_lo;
   const int32_t* ctx_slots;
+  const int32_t* ctx_tile_runs;  // optional: per 128-key tile, run start code or INT32_MIN
   int ctx_page_len;
   int pad_;
   __nv_bfloat16* o;

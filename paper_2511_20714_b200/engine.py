@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._device import attn_fwd, count_launch, require_cuda, rms_bf16, rope_qk
+from ._device import attn_fwd, count_launch, require_cuda, rms_bf16, rope_qk, tile_run_codes
 from .errors import ConfigError, DimensionError
 from .kvcache import CROSS_ATTN, SELF_ATTN, KvCache, KvConfig
 
@@ -506,10 +506,12 @@ class _KvContext:
                     tables[li][h] = (-1 - st).astype(np.int32)
                     self.host_moves[li] = np.stack([st, hs], axis=1)
         dev = require_cuda()
-        flat = np.concatenate(tables) if tables else np.zeros(0, np.int32)
+        runs = [tile_run_codes(t, self.P) for t in tables]
+        flat = np.concatenate(tables + runs)
         allt = torch.from_numpy(flat).to(dev, non_blocking=True)
-        lens = np.cumsum([0] + [len(t) for t in tables])
+        lens = np.cumsum([0] + [len(t) for t in tables + runs])
         self.tables = [allt[lens[i]:lens[i + 1]] for i in range(L)]
+        self.runs = [allt[lens[L + i]:lens[L + i + 1]] for i in range(L)]
         mv = [m for m in self.host_moves if m is not None]
         if mv:
             allm = torch.from_numpy(np.concatenate(mv)).to(dev, non_blocking=True)
@@ -569,7 +571,8 @@ class _KvContext:
         pool, st = self.pool, self.stager
         attn(q, heads, dhp, out, pool.dev_k, pool.dev_v, lo, hi - lo, cur_k, cur_v, scale=scale,
              ctx_slots=self.tables[li], page_len=self.P, first_token=self.first[li],
-             stage_k=st.k if staged else None, stage_v=st.v if staged else None)
+             stage_k=st.k if staged else None, stage_v=st.v if staged else None,
+             tile_runs=self.runs[li])
         if self.moves_dev is not None and not self.once:
             if staged:
                 ev = torch.cuda.Event()

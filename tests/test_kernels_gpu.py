@@ -176,7 +176,9 @@ PAGED = [
 def test_paged_attention_matches_torch(case):
     """K1 paged mode: context pages scattered over the pool (and the staging pool for
     negative codes), window start inside the first page."""
-    from paper_2511_20714_b200._device import attn_fwd
+    import numpy as np
+
+    from paper_2511_20714_b200._device import attn_fwd, tile_run_codes
 
     heads, hd, P, n_ctx, lo, n_cur, staged = case
     d = heads * hd
@@ -207,15 +209,27 @@ def test_paged_attention_matches_torch(case):
     kc, vc = qkv[:, d:2 * d], qkv[:, 2 * d:]
     out = torch.empty(n_q, d, device="cuda", dtype=torch.bfloat16)
     first = 1000 * P
-    attn_fwd(q, heads, hd, out, pool_k, pool_v, first + lo, n_ctx, kc if n_cur else None,
-             vc if n_cur else None, ctx_slots=slots, page_len=P, first_token=first,
-             stage_k=stage_k if staged else None, stage_v=stage_v if staged else None)
-    torch.cuda.synchronize()
     k = torch.cat([k_log[lo:lo + n_ctx], kc])
     v = torch.cat([v_log[lo:lo + n_ctx], vc])
     ref = _ref_attn(q, k, v, heads)
-    err = (out.float() - ref).abs().max().item()
-    assert err < 2e-2, err
+    # with and without the per-tile run table; a run table over consecutive slots too
+    runs = torch.from_numpy(tile_run_codes(np.array(codes, np.int32), P)).cuda()
+    for tr in (None, runs):
+        out.zero_()
+        attn_fwd(q, heads, hd, out, pool_k, pool_v, first + lo, n_ctx, kc if n_cur else None,
+                 vc if n_cur else None, ctx_slots=slots, page_len=P, first_token=first,
+                 stage_k=stage_k if staged else None, stage_v=stage_v if staged else None,
+                 tile_runs=tr)
+        torch.cuda.synchronize()
+        err = (out.float() - ref).abs().max().item()
+        assert err < 2e-2, err
+    # the same context laid out in consecutive slots: every full tile is a run
+    seq = torch.arange(n_pages, device="cuda", dtype=torch.int32)
+    runs = torch.from_numpy(tile_run_codes(np.arange(n_pages, dtype=np.int32), P)).cuda()
+    attn_fwd(q, heads, hd, out, k_log, v_log, first + lo, n_ctx, kc if n_cur else None,
+             vc if n_cur else None, ctx_slots=seq, page_len=P, first_token=first, tile_runs=runs)
+    torch.cuda.synchronize()
+    assert (out.float() - ref).abs().max().item() < 2e-2
 
 
 def test_rms_matches_torch():

@@ -110,3 +110,16 @@ def _run(seed):
 @pytest.mark.parametrize("seed", range(200))
 def test_tier_moves_keep_every_page_in_its_slot(seed):
     _run(seed)
+
+
+def test_tile_run_codes():
+    """K1's per-tile run table (_device.tile_run_codes): a tile is one TMA box iff its pages
+    are consecutive slots of one pool; partial last tiles never are."""
+    from paper_2511_20714_b200._device import tile_run_codes
+
+    NO = np.iinfo(np.int32).min
+    assert list(tile_run_codes(np.arange(20, dtype=np.int32), 16)) == [0, 8, NO]
+    codes = np.array([-1, -2, -3, -4, 5, 6, 7, 9, -5, -6, -7, -8, -9, -10, -11, -12], np.int32)
+    assert list(tile_run_codes(codes, 16)) == [NO, -5]
+    assert list(tile_run_codes(codes, 64)) == [-1, -3, 5, NO, -5, -7, -9, -11]
+    assert list(tile_run_codes(np.array([3], np.int32), 128)) == [3]

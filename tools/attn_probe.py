@@ -36,8 +36,12 @@ def main():
             n_pages = -(-C // P)
             ks = torch.randn(n_pages * P, D, device="cuda").bfloat16()
             vs = torch.randn(n_pages * P, D, device="cuda").bfloat16()
+            import numpy as np
+
+            from paper_2511_20714_b200._device import tile_run_codes
             kw = dict(ctx_slots=torch.arange(n_pages, device="cuda", dtype=torch.int32), page_len=P,
-                      first_token=0)
+                      first_token=0, tile_runs=torch.from_numpy(
+                          tile_run_codes(np.arange(n_pages, dtype=np.int32), P)).cuda())
         f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:],  # noqa: E731
                              split_kv=not args.no_split, **kw)
         for _ in range(3):

@@ -20,8 +20,14 @@ qkv = torch.randn(T, 3 * D, device="cuda").bfloat16()
 ks = torch.randn(rows, D, device="cuda").bfloat16()
 vs = torch.randn(rows, D, device="cuda").bfloat16()
 out = torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
-kw = dict(ctx_slots=torch.arange(rows // P, device="cuda", dtype=torch.int32), page_len=P,
-          first_token=0) if paged and C else {}
+kw = {}
+if paged and C:
+    import numpy as np
+
+    from paper_2511_20714_b200._device import tile_run_codes
+    kw = dict(ctx_slots=torch.arange(rows // P, device="cuda", dtype=torch.int32), page_len=P,
+              first_token=0, tile_runs=torch.from_numpy(
+                  tile_run_codes(np.arange(rows // P, dtype=np.int32), P)).cuda())
 for _ in range(3):
     attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:], **kw)
 torch.cuda.synchronize()
