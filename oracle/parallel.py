@@ -1,7 +1,7 @@
 """Oracle: Ulysses head<->sequence re-shard and its communication model.
 
 Test infrastructure only (see oracle/__init__.py). Restates
-`/root/reference/pkg/src/inferix/parallel.py:38-169,312-364` without the
+`/root/reference/pkg/src/inferix/parallel.py:38-298,312-364` without the
 simulated queue fabric: the all-to-all is a transpose of the send matrix and the
 trace is the list of (sender, receiver, bytes) it implies.
 """
@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .attention import multi_head
+from .attention import attention_partial, empty_partial, finalize_partial, merge_partials, multi_head
 from .errors import DimensionError
 
 FLOAT_BYTES = 4  # parallel.py:38
@@ -98,3 +98,63 @@ def choose_strategy(seq_len, heads, world, cost_per_message=1e-6, cost_per_byte=
         if best is None or c < best[1]:
             best = (s, c, m, b)
     return {"strategy": best[0], "cost": best[1], "messages": best[2], "bytes": best[3]}
+
+
+def _offsets(shards) -> list:
+    """parallel.py:114-118."""
+    return [0] + list(np.cumsum([s.shape[0] for s in shards]))
+
+
+def _pbytes(p) -> int:
+    """parallel.py:41-49 for an AttentionPartial: acc + row_max + denom elements."""
+    return (p.acc.size + p.row_max.size + p.denom.size) * FLOAT_BYTES
+
+
+def ring_attention_pass_kv(q_shards, k_shards, v_shards, mask, heads=1):
+    """parallel.py:172-244 (lockstep schedule) — K/V rotate W-1 steps; each rank merges a
+    partial per head over every visiting shard. Returns (outputs, trace)."""
+    w = len(q_shards)
+    dh = q_shards[0].shape[1] // heads
+    qo, ko = _offsets(q_shards), _offsets(k_shards)
+    parts = [[empty_partial(q_shards[i].shape[0], dh) for _ in range(heads)] for i in range(w)]
+    cur = [(k_shards[i], v_shards[i], i) for i in range(w)]
+    trace = []
+    for step in range(w):
+        for i in range(w):
+            k, v, o = cur[i]
+            m = mask[qo[i]:qo[i + 1], ko[o]:ko[o + 1]]
+            for h in range(heads):
+                sl = slice(h * dh, (h + 1) * dh)
+                parts[i][h] = merge_partials(parts[i][h], attention_partial(q_shards[i][:, sl], k[:, sl], v[:, sl], m))
+        if step < w - 1:
+            trace += [(i, (i + 1) % w, _nbytes((cur[i][0], cur[i][1]))) for i in range(w)]
+            cur = [(cur[(i - 1) % w][0], cur[(i - 1) % w][1], cur[(i - 1) % w][2]) for i in range(w)]
+    return [np.concatenate([finalize_partial(p) for p in parts[i]], axis=1) for i in range(w)], trace
+
+
+def ring_attention_pass_q(q_shards, k_shards, v_shards, mask, heads=1):
+    """parallel.py:247-298 — Q and its partials rotate, K/V stay, then a gather to the
+    owners. Returns (outputs, trace)."""
+    w = len(q_shards)
+    dh = q_shards[0].shape[1] // heads
+    qo, ko = _offsets(q_shards), _offsets(k_shards)
+    trav = [(q_shards[i], [empty_partial(q_shards[i].shape[0], dh) for _ in range(heads)], i)
+            for i in range(w)]
+    trace = []
+    for step in range(w):
+        for i in range(w):
+            q, parts, o = trav[i]
+            m = mask[qo[o]:qo[o + 1], ko[i]:ko[i + 1]]
+            for h in range(heads):
+                sl = slice(h * dh, (h + 1) * dh)
+                parts[h] = merge_partials(parts[h], attention_partial(q[:, sl], k_shards[i][:, sl], v_shards[i][:, sl], m))
+        if step < w - 1:
+            trace += [(i, (i + 1) % w, trav[i][0].size * FLOAT_BYTES + sum(_pbytes(p) for p in trav[i][1]))
+                      for i in range(w)]
+            trav = [trav[(i - 1) % w] for i in range(w)]
+    out = [None] * w
+    for i in range(w):
+        q, parts, o = trav[i]
+        out[o] = np.concatenate([finalize_partial(p) for p in parts], axis=1)
+        trace.append((i, o, sum(_pbytes(p) for p in parts)))
+    return out, trace

@@ -27,7 +27,8 @@ import numpy as np
 import torch
 
 from . import _abi
-from .attention import scaled_dot_attention
+from .attention import (AttentionPartial, attention_partial, empty_partial, finalize_partial, merge_partials,
+                        scaled_dot_attention)
 from .errors import DimensionError
 
 FLOAT_BYTES = 4  # parallel.py:38 — the reference's cost model counts fp32 elements
@@ -38,6 +39,8 @@ def _payload_bytes(payload) -> int:
     """parallel.py:41-49."""
     if isinstance(payload, (np.ndarray, torch.Tensor)):
         return int(np.prod(tuple(payload.shape))) * FLOAT_BYTES
+    if isinstance(payload, AttentionPartial):
+        return sum(_payload_bytes(t) for t in (payload.acc, payload.row_max, payload.denom))
     if isinstance(payload, (tuple, list)):
         return sum(_payload_bytes(p) for p in payload)
     raise DimensionError(f"untraceable payload type {type(payload)!r}")
@@ -160,6 +163,86 @@ def ulysses_attention(group: WorkerGroup, q_shards, k_shards, v_shards, heads, m
     back = [[outs[j][cuts[i]:cuts[i + 1]] for i in range(w)] for j in range(w)]
     recv_back = all_to_all(group, back)
     return [torch.cat(recv_back[i], dim=1) for i in range(w)]
+
+
+def _shard_offsets(shards) -> list:
+    """parallel.py:114-118 — cumulative row offsets of a shard list."""
+    return [0] + list(np.cumsum([s.shape[0] for s in shards]))
+
+
+def _heads_partial(q, k, v, heads: int, m, parts):
+    """Merge one key shard into every head's running partial (attention.py:127-173): one
+    K1 launch per head with partial statistics, merged on device."""
+    dh = q.shape[1] // heads
+    for h in range(heads):
+        sl = slice(h * dh, (h + 1) * dh)
+        parts[h] = merge_partials(parts[h], attention_partial(q[:, sl], k[:, sl], v[:, sl], m))
+    return parts
+
+
+def ring_attention_pass_kv(group: WorkerGroup, q_shards, k_shards, v_shards, mask, heads: int = 1,
+                           threads: bool = False):
+    """parallel.py:172-244 — K/V shards rotate around the ring (W-1 steps, one 'kv' message
+    per rank per step), every rank merges partials over each visiting shard. The
+    lockstep schedule is used for either `threads` value: the result and the trace are
+    the same as the reference's (deterministic rotation), only the scheduling differs."""
+    w = group.world_size
+    qs, ks, vs = ([_dev(s) for s in x] for x in (q_shards, k_shards, v_shards))
+    m = _dev_mask(mask)
+    dh = qs[0].shape[1] // heads
+    q_off, kv_off = _shard_offsets(qs), _shard_offsets(ks)
+    parts = [[empty_partial(qs[i].shape[0], dh) for _ in range(heads)] for i in range(w)]
+    cur = [(ks[i], vs[i], i) for i in range(w)]
+    for step in range(w):
+        for i in range(w):
+            k, v, owner = cur[i]
+            _heads_partial(qs[i], k, v, heads,
+                           m[q_off[i]:q_off[i + 1], kv_off[owner]:kv_off[owner + 1]], parts[i])
+        if step < w - 1:
+            owners = [c[2] for c in cur]
+            for i in range(w):
+                group.send(i, (i + 1) % w, (cur[i][0], cur[i][1]), tag="kv")
+            cur = [(*group.recv((i - 1) % w, i), owners[(i - 1) % w]) for i in range(w)]
+            group.advance_step()
+    return [torch.cat([finalize_partial(p) for p in parts[i]], dim=1) for i in range(w)]
+
+
+def ring_attention_pass_q(group: WorkerGroup, q_shards, k_shards, v_shards, mask, heads: int = 1):
+    """parallel.py:247-298 — Q and its per-head partials rotate while K/V stay; after W
+    steps the finished partials are sent to their owners ('gather')."""
+    w = group.world_size
+    qs, ks, vs = ([_dev(s) for s in x] for x in (q_shards, k_shards, v_shards))
+    m = _dev_mask(mask)
+    dh = qs[0].shape[1] // heads
+    q_off, kv_off = _shard_offsets(qs), _shard_offsets(ks)
+    trav = [(qs[i], [empty_partial(qs[i].shape[0], dh) for _ in range(heads)], i) for i in range(w)]
+    for step in range(w):
+        for i in range(w):
+            q, parts, owner = trav[i]
+            _heads_partial(q, ks[i], vs[i], heads,
+                           m[q_off[owner]:q_off[owner + 1], kv_off[i]:kv_off[i + 1]], parts)
+        if step < w - 1:
+            for i in range(w):
+                q, parts, _ = trav[i]
+                group.send(i, (i + 1) % w, (q, *parts), tag="q")
+            nxt = []
+            for i in range(w):
+                payload = group.recv((i - 1) % w, i)
+                nxt.append((payload[0], list(payload[1:]), trav[(i - 1) % w][2]))
+            trav = nxt
+            group.advance_step()
+    out = [None] * w
+    for i in range(w):
+        q, parts, owner = trav[i]
+        if owner == i:
+            out[i] = torch.cat([finalize_partial(p) for p in parts], dim=1)
+        else:
+            group.send(i, owner, tuple(parts), tag="gather")
+    for i in range(w):
+        if out[i] is None:
+            holder = next(j for j in range(w) if trav[j][2] == i)
+            out[i] = torch.cat([finalize_partial(p) for p in group.recv(holder, i)], dim=1)
+    return out
 
 
 @dataclass

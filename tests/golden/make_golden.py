@@ -239,6 +239,12 @@ def gen_parallel():
                         RP.ulysses_attention(grp, qs, ks, vs, heads, mask))
                     traced = [t for t in grp.trace if t.sender != t.receiver]
                     out[f"trace_{tag}"] = np.array([len(traced), sum(t.bytes for t in traced)])
+                for name, fn in (("ringkv", RP.ring_attention_pass_kv),
+                                 ("ringq", RP.ring_attention_pass_q)):
+                    grp = RP.WorkerGroup(world)
+                    out[f"{name}_{tag}"] = np.concatenate(fn(grp, qs, ks, vs, mask, heads=heads))
+                    traced = [t for t in grp.trace if t.sender != t.receiver]
+                    out[f"{name}trace_{tag}"] = np.array([len(traced), sum(t.bytes for t in traced)])
                 for s in RP.STRATEGIES:
                     if s == "ulysses" and heads % world:
                         continue

@@ -141,6 +141,11 @@ def test_parallel_matches_reference():
                 else:
                     with pytest.raises(DimensionError):
                         OP.ulysses_attention(qs, ks, vs, heads, mask)
+                for name, fn in (("ringkv", OP.ring_attention_pass_kv), ("ringq", OP.ring_attention_pass_q)):
+                    out, trace = fn(qs, ks, vs, mask, heads)
+                    np.testing.assert_allclose(np.concatenate(out), g[f"{name}_{tag}"], atol=1e-6)
+                    off = [t for t in trace if t[0] != t[1]]
+                    assert [len(off), sum(t[2] for t in off)] == g[f"{name}trace_{tag}"].tolist()
 
 
 def test_comm_predictions_match_reference():

@@ -15,7 +15,7 @@ from conftest import GOLDEN
 pytestmark = pytest.mark.gpu
 
 
-def test_reference_api_ulysses_vs_golden():
+def test_reference_api_ulysses_and_ring_vs_golden():
     from paper_2511_20714_b200 import parallel as P
     from paper_2511_20714_b200.attention import block_causal_mask
 
@@ -41,6 +41,15 @@ def test_reference_api_ulysses_vs_golden():
                     assert [len(traced), sum(t.bytes for t in traced)] == g[f"trace_{tag}"].tolist()
                     assert P.predict_communication("ulysses", lens, heads, 4, world) == \
                         (len(traced), sum(t.bytes for t in traced))
+                for name, fn, strat in (("ringkv", P.ring_attention_pass_kv, "ring_pass_kv"),
+                                        ("ringq", P.ring_attention_pass_q, "ring_pass_q")):
+                    grp = P.WorkerGroup(world)
+                    out = torch.cat(fn(grp, qs, ks, vs, mask, heads=heads)).cpu().numpy()
+                    assert np.abs(out - g[f"{name}_{tag}"]).max() <= 2e-2, (name, tag)
+                    traced = [t for t in grp.trace if t.sender != t.receiver]
+                    got = [len(traced), sum(t.bytes for t in traced)]
+                    assert got == g[f"{name}trace_{tag}"].tolist(), (name, tag)
+                    assert P.predict_communication(strat, lens, heads, 4, world) == tuple(got)
 
 
 def _free_port():
@@ -55,7 +64,7 @@ CFG = dict(layers=2, heads=4, head_dim=64, block_len=256, frame_shape=(8, 8), pr
 REQ = dict(num_blocks=3, seed=0, prompt_schedule=[(0, "a quiet scene"), (2, "rain")])
 
 
-def _rank(rank, world, port, q, cfg=None):
+def _rank(rank, world, port, q, cfg=None, kvc=None):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -65,7 +74,7 @@ def _rank(rank, world, port, q, cfg=None):
         from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
 
         model = E.ToyModel(E.ModelConfig(**(cfg or CFG)), head_multiple=world)
-        eng = UlyssesEngine(model, UlyssesComm())
+        eng = UlyssesEngine(model, UlyssesComm(), E.KvConfig(**kvc) if kvc else None)
         lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
         q.put((rank, [l.cpu().numpy() for l in lats], eng.cache.state(), eng.comm.bytes))
     finally:
@@ -75,17 +84,23 @@ def _rank(rank, world, port, q, cfg=None):
 CFG_ROPE = dict(CFG, rope_grid=(1, 16, 16), heads=3)  # 3 heads on 2 ranks: dummy-head padding
 
 
-@pytest.mark.parametrize("world,cfg", [(2, CFG), (2, CFG_ROPE)])
-def test_ulysses_engine_matches_single_gpu(world, cfg):
+# device capacity below the working set: each rank's head shard spills to its own pinned
+# host pool, restores / demotions move data per rank, host pages are staged for K1
+KV_SPILL = dict(num_layers=2, head_dim=256, page_len=16, capacity_pages_device=40,
+                capacity_pages_host=10**4)
+
+
+@pytest.mark.parametrize("world,cfg,kvc", [(2, CFG, None), (2, CFG_ROPE, None), (2, CFG, KV_SPILL)])
+def test_ulysses_engine_matches_single_gpu(world, cfg, kvc):
     from paper_2511_20714_b200 import engine as E
 
     ref_model = E.build_model(E.ModelConfig(**cfg))
-    ref_eng = E.Engine(ref_model)
+    ref_eng = E.Engine(ref_model, E.KvConfig(**kvc) if kvc else None)
     ref = ref_eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, q, cfg)) for r in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, cfg, kvc)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
@@ -98,3 +113,5 @@ def test_ulysses_engine_matches_single_gpu(world, cfg):
         # replicated page table == single-GPU page table == reference semantics
         assert state == ref_eng.cache.state()
         assert nbytes > 0
+    if kvc:
+        assert ref_eng.cache.memory_stats().host_pages_used > 0
