@@ -63,9 +63,9 @@ CONFIGS = {
     # tier is live. Blocks [0, prefill) are appended from synthetic K/V (no denoising), then
     # `blocks` more are generated through generate_block and timed.
     "c5": dict(layers=40, heads=40, head_dim=128, block_len=4680, blocks=2, prefill=60,
-               device_blocks=36, frame_shape=(16, 16), weights="device",
-               desc="c5: Wan2.1-14B-shaped LV rollout on 1 GPU: 60 cached blocks (36 blocks of "
-                    "pages in HBM, the rest on the pinned host tier), blocks 61-62 timed"),
+               device_blocks=30, frame_shape=(16, 16), weights="device",
+               desc="c5: Wan2.1-14B-shaped LV rollout on 1 GPU: 60+ cached blocks (30 blocks of "
+                    "pages = 115 GB in HBM, the rest on the pinned host tier), 2 blocks timed"),
 }
 
 
@@ -358,7 +358,7 @@ def run_host_tier_bench(args, c, cfgname, local):
     nb_pre, nb = c["prefill"], max(c["blocks"], args.steps)
     kvc = E.default_kv_config(mc, capacity_pages_device=c["device_blocks"] * L * pages_blk,
                               capacity_pages_host=(nb_pre + nb + 2) * L * pages_blk)
-    cache = KvCache(kvc, dtype=torch.bfloat16, reserve_tokens=T * c["device_blocks"], row_width=W)
+    cache = KvCache(kvc, dtype=torch.bfloat16, reserve_tokens=T * (c["device_blocks"] + 1), row_width=W)
     host_slots = (nb_pre + nb + 2 - c["device_blocks"]) * L * pages_blk
     t0 = time.perf_counter()
     cache.pool(SELF_ATTN).ensure(0, host_slots)  # pinned + mapped + zeroed once, up front

@@ -127,8 +127,9 @@ class _Pool:
     the pinned host tier alike. Grown geometrically as the page table's high-water marks
     rise (device growth is a stream-ordered copy; host growth synchronises first)."""
 
-    def __init__(self, width: int, dtype: torch.dtype, page_len: int):
+    def __init__(self, width: int, dtype: torch.dtype, page_len: int, max_dev: int, max_host: int):
         self.width, self.dtype, self.page_len = width, dtype, page_len
+        self.max_dev, self.max_host = max(4, max_dev), max(4, max_host)  # tier capacities
         self.esz = torch.finfo(dtype).bits // 8
         self.dev_slots = self.host_slots = 0
         self.dev_k = self.dev_v = None
@@ -141,8 +142,8 @@ class _Pool:
 
     def ensure(self, dev_slots: int, host_slots: int) -> None:
         P, W = self.page_len, self.width
-        if dev_slots > self.dev_slots:
-            n = max(dev_slots, 2 * self.dev_slots, 4)
+        if dev_slots > self.dev_slots:  # geometric growth, never past the tier's capacity
+            n = max(dev_slots, min(2 * self.dev_slots, self.max_dev), 4)
             dev = require_cuda()
             k = torch.zeros(n * P, W, device=dev, dtype=self.dtype)
             v = torch.zeros_like(k)
@@ -152,7 +153,7 @@ class _Pool:
             self.dev_k, self.dev_v, self.dev_slots = k, v, n
             self._abi = None
         if host_slots > self.host_slots:
-            n = max(host_slots, 2 * self.host_slots, 4)
+            n = max(host_slots, min(2 * self.host_slots, self.max_host), 4)
             k, v = _HostBuf(n * self.slot_bytes), _HostBuf(n * self.slot_bytes)
             if self.host_slots:
                 torch.cuda.synchronize()  # no kernel may still address the old buffers
@@ -332,8 +333,9 @@ class KvCache:
         w = row_width or config.stored_width
         wc = cross_row_width or w
         self._row_width = {SELF_ATTN: w, CROSS_ATTN: wc}
-        self._pools = {SELF_ATTN: _Pool(w, dtype, config.page_len),
-                       CROSS_ATTN: _Pool(wc, dtype, config.page_len)}
+        cd, ch = config.capacity_pages_device, config.capacity_pages_host
+        self._pools = {SELF_ATTN: _Pool(w, dtype, config.page_len, cd, ch),
+                       CROSS_ATTN: _Pool(wc, dtype, config.page_len, cd, ch)}
         self.moved_pages = [0, 0]  # pages copied device->host, host->device (tier moves)
         if reserve_tokens:
             per_layer = -(-reserve_tokens // config.page_len) + 1
