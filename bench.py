@@ -196,7 +196,7 @@ def run_reference(args):
               f"to the {c['blocks']}-block rollout ({secs:.0f}s/rollout)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded numpy)",
             "config": {"workload": c["desc"], "extrapolated": True},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
@@ -309,7 +309,7 @@ def run_ours(args):
                             f"{t_rec['source']}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (reference-seeded noise, PCG64 random-init weights)",
         "config": {"workload": c["desc"], "layers": mc.layers, "heads": mc.heads,
                    "head_dim": mc.head_dim, "tokens_per_block": T, "blocks": nb,

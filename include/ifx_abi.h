@@ -95,6 +95,12 @@ int ifx_pt_snapshot(const ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t*
  * logging call, all dir-0 moves then all dir-1 moves (each group is hazard-free, so it is
  * one ifx_kv_move_pages launch). out == NULL: only *n_records is set, nothing drained. */
 int ifx_pt_drain_moves(ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* n_records);
+/* Group the following calls into one move batch (one epoch): a page restored by one call
+ * and demoted again by a later one before the drain (the LRU churn of fetching a whole
+ * context that exceeds the device tier) cancels instead of moving twice. Batches nest;
+ * drain after the outermost end, before reading the data. */
+int ifx_pt_batch_begin(ifx_pagetable* pt);
+int ifx_pt_batch_end(ifx_pagetable* pt);
 /* slots ever used per pool: out4[kind*2 + tier] (tier 0 device, 1 host) */
 int ifx_pt_pool_extent(const ifx_pagetable* pt, int64_t* out4);
 /* Slot codes of the pages covering tokens [start, end) of a stream (within its stored

@@ -68,19 +68,41 @@ struct Page {
 // slot allocator of one (kind, tier) pool: LIFO free list + high-water mark; frees of
 // host slots made during a call are deferred to the drain (see header)
 struct SlotPool {
-  std::vector<int64_t> free_list;
+  std::vector<int64_t> free_list;  // LIFO; may hold stale entries (is_free decides)
+  std::vector<char> is_free;
+  std::vector<Page*> holder;       // page in each slot (device pools)
   std::vector<int64_t> deferred;
   std::vector<char> is_deferred;
   int64_t hwm = 0;
+  void grow(int64_t s) {
+    if ((int64_t)is_free.size() <= s) {
+      is_free.resize(s + 1, 0);
+      holder.resize(s + 1, nullptr);
+    }
+  }
   int64_t take() {
-    if (!free_list.empty()) {
+    while (!free_list.empty()) {
       int64_t s = free_list.back();
       free_list.pop_back();
-      return s;
+      if (is_free[s]) {
+        is_free[s] = 0;
+        return s;
+      }
     }
+    grow(hwm);
     return hwm++;
   }
-  void give(int64_t s) { free_list.push_back(s); }
+  bool take_specific(int64_t s) {  // the entry left on the stack becomes stale
+    if (s >= (int64_t)is_free.size() || !is_free[s]) return false;
+    is_free[s] = 0;
+    return true;
+  }
+  void give(int64_t s) {
+    grow(s);
+    is_free[s] = 1;
+    holder[s] = nullptr;
+    free_list.push_back(s);
+  }
   void defer(int64_t s) {
     if ((int64_t)is_deferred.size() <= s) is_deferred.resize(s + 1, 0);
     is_deferred[s] = 1;
@@ -97,7 +119,7 @@ struct SlotPool {
     for (int64_t s : deferred)
       if (s < (int64_t)is_deferred.size() && is_deferred[s]) {
         is_deferred[s] = 0;
-        free_list.push_back(s);
+        give(s);
       }
     deferred.clear();
   }
@@ -140,11 +162,15 @@ struct ifx_pagetable {
   std::vector<Move> moves;
   std::vector<Page*> pend_pages;  // pages with a move pending in the current call
   int64_t epoch = 0;
+  int batch_depth = 0;  // > 0: calls share one epoch (ifx_pt_batch_begin / _end)
   std::mutex mu;
 
   // start of every mutating call: moves of earlier calls are final (they execute before
-  // this call's), host slots they freed may be recycled
+  // this call's), host slots they freed may be recycled. Inside a batch every call belongs
+  // to the batch's epoch, so a page restored by one call and demoted again by a later one
+  // (the LRU churn of a whole-context fetch) cancels instead of moving twice.
   void begin_call() {
+    if (batch_depth > 0) return;
     epoch++;
     for (Page* p : pend_pages) p->pending = -1;
     pend_pages.clear();
@@ -182,6 +208,7 @@ struct ifx_pagetable {
     }
     Page* p = new Page{next_page++, tier, 0, start, 0, s};
     p->slot = pools[s & 1][tier].take();
+    if (tier == 0) pools[s & 1][0].holder[p->slot] = p;
     live[p->id] = p;
     if (tier == 0 && lru_on) lru.insert(key(p));
     lru_sync();
@@ -199,6 +226,22 @@ struct ifx_pagetable {
     live.erase(p->id);
     delete p;
     lru_sync();
+  }
+
+  // Make device slot s available to a page being restored in the epoch that demoted it:
+  // free -> take it; held by a page whose H2D into s is still pending -> retarget that H2D.
+  bool reclaim_device_slot(SlotPool& dp, int64_t s) {
+    if (dp.take_specific(s)) return true;
+    if (s >= (int64_t)dp.holder.size()) return false;
+    Page* h = dp.holder[s];
+    if (h == nullptr || h->pending < 0 || moves[h->pending].dir != 1 || !moves[h->pending].live)
+      return false;
+    const int64_t ds = dp.take();
+    moves[h->pending].dev_slot = ds;
+    h->slot = ds;
+    dp.holder[ds] = h;
+    dp.holder[s] = nullptr;
+    return true;
   }
 
   void demote(Page* p) {  // device -> host
@@ -234,13 +277,26 @@ struct ifx_pagetable {
       demote(victim);
     }
     const int k = p->stream & 1;
-    const int64_t ds = pools[k][0].take();
-    if (p->pending >= 0 && ds == p->prev_slot) {
-      // demoted earlier in this call and its device slot is still unused: cancel the D2H
+    SlotPool& dp = pools[k][0];
+    if (p->pending >= 0 && reclaim_device_slot(dp, p->prev_slot)) {
+      // demoted earlier in this epoch: its data never left its device slot, which it gets
+      // back (a page restored into that slot meanwhile is pointed at another one before its
+      // H2D runs) -- the demotion's D2H is cancelled, nothing moves
       moves[p->pending].live = false;
-      pools[k][1].give(p->slot);
+      pools[k][1].give(p->slot);  // written only by the cancelled D2H
       p->pending = -1;
-    } else {
+      p->slot = p->prev_slot;
+      dp.holder[p->slot] = p;
+      p->tier = 0;
+      host_used--;
+      dev_used++;
+      if (lru_on) lru.insert(key(p));
+      lru_sync();
+      return;
+    }
+    const int64_t ds = dp.take();
+    dp.holder[ds] = p;
+    {
       // (a demotion earlier in this call, if any, stays live: D2H runs before H2D)
       moves.push_back(Move{epoch, k, 1, ds, p->slot, true});
       pools[k][1].defer(p->slot);
@@ -496,6 +552,20 @@ int ifx_pt_snapshot(const ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t*
   if (out == nullptr) return IFX_OK;
   if (cap < (int64_t)r.size()) return ifx::fail(IFX_EDIM, "snapshot buffer too small");
   std::memcpy(out, r.data(), r.size() * sizeof(int64_t));
+  return IFX_OK;
+}
+
+int ifx_pt_batch_begin(ifx_pagetable* pt) {
+  std::lock_guard<std::mutex> g(pt->mu);
+  if (pt->batch_depth == 0) pt->begin_call();
+  pt->batch_depth++;
+  return IFX_OK;
+}
+
+int ifx_pt_batch_end(ifx_pagetable* pt) {
+  std::lock_guard<std::mutex> g(pt->mu);
+  if (pt->batch_depth == 0) return ifx::fail(IFX_ECONFIG, "batch_end without batch_begin");
+  pt->batch_depth--;
   return IFX_OK;
 }
 

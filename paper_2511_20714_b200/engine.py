@@ -592,19 +592,52 @@ def _ctx_from_cache(model: ToyModel, cache: KvCache | None, stager: _Stager | No
     return _KvContext(model, cache, stager or _Stager(require_cuda()), passes)
 
 
+def _touch_cross(model: ToyModel, cache: KvCache | None):
+    """engine.py:240-246 — bookkeeping of the cross-attention fetch (if layer 0 has any)."""
+    if cache is None:
+        return None
+    lo, hi = cache.addressable_range(0, CROSS_ATTN)
+    if hi <= lo:
+        return None
+    rngs = []
+    for li in range(model.config.layers):
+        a, b = cache.addressable_range(li, CROSS_ATTN)
+        cache.touch_range(li, (a, b), CROSS_ATTN)
+        rngs.append((a, b))
+    return rngs
+
+
+def _gather_cross(cache: KvCache, rngs):
+    """Per layer the prompt K/V rows, gathered (K7) into a contiguous buffer (a few rows;
+    pages may sit on either tier)."""
+    out = []
+    for li, (a, b) in enumerate(rngs):
+        k, v = cache._gather(li, CROSS_ATTN, None, a, b - a, a, b, raw=True)
+        out.append((k, v, 0, b - a))
+    return out
+
+
+def _block_context(model: ToyModel, cache: KvCache | None, prompt_ctx, stager: _Stager,
+                   passes: int):
+    """engine.py:297-298 — the block's context fetch: self-attention layers 0..L-1, then
+    cross-attention, as ONE move batch (the LRU churn of a context larger than the device
+    tier cancels out instead of moving every page twice), then K1's paged view."""
+    if cache is None:
+        return None, _cross_from_cache(model, None, prompt_ctx)
+    with cache.batch():
+        ctx = _KvContext(model, cache, stager, passes)
+        rngs = _touch_cross(model, cache)
+    cross = _gather_cross(cache, rngs) if rngs is not None else _cross_from_cache(model, None, prompt_ctx)
+    ctx.prepare()
+    return ctx, cross
+
+
 def _cross_from_cache(model: ToyModel, cache: KvCache | None, prompt_ctx):
-    """engine.py:240-250 — per layer the prompt K/V rows, gathered (K7) into a contiguous
-    bf16 buffer once per block (a few rows; pages may sit on either tier)."""
-    if cache is not None:
-        lo, hi = cache.addressable_range(0, CROSS_ATTN)
-        if hi > lo:
-            out = []
-            for li in range(model.config.layers):
-                a, b = cache.addressable_range(li, CROSS_ATTN)
-                cache.touch_range(li, (a, b), CROSS_ATTN)
-                k, v = cache._gather(li, CROSS_ATTN, None, a, b - a, a, b, raw=True)
-                out.append((k, v, 0, b - a))
-            return out
+    """engine.py:240-250 — per layer the prompt K/V rows (from the cache when layer 0 has
+    any), else projected from the prompt embedding."""
+    rngs = _touch_cross(model, cache)
+    if rngs is not None:
+        return _gather_cross(cache, rngs)
     if prompt_ctx is None:
         return None
     out = []
@@ -686,10 +719,7 @@ def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSche
     lat = torch.empty(src.shape, device=require_cuda(), dtype=torch.float32)
     lat.copy_(src, non_blocking=True)  # async H2D when the noise lives in pinned memory
     runner = _runner(model)
-    ctx = _ctx_from_cache(model, cache, runner.stager, passes=len(schedule.steps) + 1)
-    cross = _cross_from_cache(model, cache, prompt_ctx)
-    if ctx is not None:
-        ctx.prepare()
+    ctx, cross = _block_context(model, cache, prompt_ctx, runner.stager, len(schedule.steps) + 1)
     runner.denoise(lat, schedule, ctx, cross, cache, chunk_index)
     if not to_host:
         return GeneratedBlock(chunk_index, lat, [], prompt_text)

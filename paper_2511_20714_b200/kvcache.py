@@ -20,6 +20,7 @@ K1 reads bf16 tiles). Returned fetches are new CUDA tensors.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import struct
 import threading
@@ -262,6 +263,12 @@ class PageTable:
                                         out.size, ctypes.byref(n)))
         return out
 
+    def batch_begin(self) -> None:
+        _abi.check(_abi.lib().ifx_pt_batch_begin(self._h))
+
+    def batch_end(self) -> None:
+        _abi.check(_abi.lib().ifx_pt_batch_end(self._h))
+
     def pool_extent(self) -> list:
         """Slots ever used: [self device, self host, cross device, cross host]."""
         out = (ctypes.c_int64 * 4)()
@@ -388,6 +395,27 @@ class KvCache:
             count_launch()
             self.moved_pages[d] += int(hi - lo)
 
+    @contextlib.contextmanager
+    def batch(self, stream=None):
+        """Bookkeeping calls inside share one move batch; the moves run (K6) at exit. The
+        data of pages touched inside is only consistent after exit (the engine fetches the
+        whole context this way, then builds K1's slot tables)."""
+        with self._lock:
+            self._pt.batch_begin()
+            self._batch = getattr(self, "_batch", 0) + 1
+            try:
+                yield self
+            finally:
+                self._batch -= 1
+                self._pt.batch_end()
+                if self._batch == 0:
+                    self._sync(stream)
+
+    def _no_batch(self, what: str) -> None:
+        if getattr(self, "_batch", 0):
+            raise RuntimeError(f"{what} inside KvCache.batch(): page data is only consistent "
+                               f"after the batch's moves ran")
+
     def slot_table(self, layer: int, kind: str, start: int, end: int):
         """(int32 slot codes of the pages covering tokens [start, end), first page's start)."""
         return self._pt.slots(layer, kind, start, end)
@@ -414,6 +442,7 @@ class KvCache:
         if k.stride(1) != 1 or v.stride(1) != 1 or k.stride(0) != v.stride(0):
             k, v = k.contiguous(), v.contiguous()
         with self._lock:
+            self._no_batch("append_block")
             rc, bid, start, written, pages = self._pt.append(layer, kind, t, chunk_index)
             self._sync(stream)
             if written > 0:  # rows already packed even if allocation then failed (kvcache.py:210-223)
@@ -440,11 +469,13 @@ class KvCache:
     def evict_window(self, keep_last_n_tokens: int) -> int:
         """kvcache.py:258-285 (freed pages return their slots to the pools)."""
         with self._lock:
+            self._no_batch("evict_window")
             return self._pt.evict_window(keep_last_n_tokens)
 
     def clear_cross_attention(self) -> int:
         """kvcache.py:287-299."""
         with self._lock:
+            self._no_batch("clear_cross_attention")
             return self._pt.clear_cross()
 
     # -- reads ----------------------------------------------------------------------------
@@ -457,10 +488,12 @@ class KvCache:
             try:
                 self._pt.touch_range(layer, kind, a, b)
             finally:
-                self._sync(stream)
+                if not getattr(self, "_batch", 0):
+                    self._sync(stream)
 
     def _gather(self, layer, kind, tokens: torch.Tensor | None, first: int, n: int, lo: int, hi: int,
                 raw: bool = False):
+        self._no_batch("a fetch")
         p = self._pools[kind]
         dev = require_cuda()
         ko = torch.empty(n, p.width, device=dev, dtype=p.dtype)

@@ -462,7 +462,7 @@ class UlyssesEngine:
 
     def generate(self, request, noise_provider=None, gather: bool = True):
         """Returns per-block full latents (gathered) if `gather`, else local shards."""
-        from .engine import (_cross_from_cache, _ctx_from_cache, _cross_kv, _init_noise,
+        from .engine import (_block_context, _cross_kv, _init_noise_pinned,
                              _prompt_for_chunk, embed_prompt)
         from .kvcache import CROSS_ATTN, KvCache
         request.validate()
@@ -471,7 +471,9 @@ class UlyssesEngine:
         self.cache = KvCache(self.kv_config, dtype=torch.bfloat16,
                              reserve_tokens=T * request.num_blocks, row_width=r.wl,
                              cross_row_width=m.attn_width)
-        make_noise = noise_provider or (lambda ch: _init_noise(c, request.seed, ch))
+        # the reference's seeded host noise (engine.py:280-282), generated bit-exactly by the
+        # native parallel PCG64 parser; each rank copies only its sequence slice to the GPU
+        make_noise = noise_provider or (lambda ch: _init_noise_pinned(c, request.seed, ch))
         cur = None
         out = []
         for chunk in range(request.num_blocks):
@@ -484,10 +486,9 @@ class UlyssesEngine:
                 cur = prompt
             noise = make_noise(chunk)
             full = noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)
-            lat = full[rank * n:(rank + 1) * n].to(m.time_vec.device, torch.float32).clone()
-            ctx = _ctx_from_cache(m, self.cache, r.stager, passes=len(request.schedule.steps) + 1)
-            cross = _cross_from_cache(m, self.cache, None)
-            ctx.prepare()  # slot tables once the block's fetches (self, then cross) are done
+            lat = full[rank * n:(rank + 1) * n].to(m.time_vec.device, torch.float32,
+                                                   non_blocking=True).clone()
+            ctx, cross = _block_context(m, self.cache, None, r.stager, len(request.schedule.steps) + 1)
             r.denoise(lat, request.schedule, ctx, cross, self.cache, chunk)
             if request.kv_window is not None:
                 self.cache.evict_window(request.kv_window)

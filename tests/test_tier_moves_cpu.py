@@ -83,6 +83,16 @@ def _run(seed):
                     slot = int(c) if c >= 0 else -1 - int(c)
                     pools[(k, tier)][slot] = payload[p[0]]  # K2 writes the page's rows
             execute()
+        elif op == 4 and rng.random() < 0.5:  # a batch of fetches (one epoch), drained once
+            pt.batch_begin()
+            for _ in range(int(rng.integers(1, 6))):
+                li, kd = int(rng.integers(0, 2)), kinds[int(rng.random() < 0.25)]
+                base, total = pt.range(li, kd)
+                if total > base:
+                    a = int(rng.integers(base, total))
+                    pt.touch_range(li, kd, a, int(rng.integers(a, total + 1)))
+            pt.batch_end()
+            execute()
         elif op < 8:
             base, total = pt.range(layer, kind)
             if total > base:
@@ -123,3 +133,40 @@ def test_tile_run_codes():
     assert list(tile_run_codes(codes, 16)) == [NO, -5]
     assert list(tile_run_codes(codes, 64)) == [-1, -3, 5, NO, -5, -7, -9, -11]
     assert list(tile_run_codes(np.array([3], np.int32), 128)) == [3]
+
+
+def test_batched_context_fetch_cancels_lru_churn():
+    """The engine's per-block context fetch (every layer's whole range, layer order) over a
+    cache larger than the device tier: call by call, LRU demotion makes almost every page
+    round-trip; as one batch the churn cancels and only net tier changes move."""
+    L, P, per_block, blocks, cap = 6, 4, 5, 12, 150
+
+    def run(batched):
+        pt = PageTable(KvConfig(num_layers=L, head_dim=4, page_len=P, capacity_pages_device=cap,
+                                capacity_pages_host=10**5))
+        moved = []
+        for b in range(blocks):
+            n = 0
+            if batched:
+                pt.batch_begin()
+            for li in range(L):
+                base, total = pt.range(li, "self_attn")
+                if total > base:
+                    pt.touch_range(li, "self_attn", base, total)
+                    if not batched:
+                        n += len(pt.drain_moves())
+            if batched:
+                pt.batch_end()
+                n += len(pt.drain_moves())
+            for li in range(L):
+                pt.append(li, "self_attn", per_block * P, b)
+            moved.append(n)
+        return moved, pt.state()
+
+    per_call, st1 = run(False)
+    batched, st2 = run(True)
+    assert st1 == st2  # bookkeeping is identical either way
+    total_pages = L * blocks * per_block
+    assert total_pages > 2 * cap
+    assert sum(per_call[-3:]) > 6 * sum(batched[-3:])
+    assert max(batched[-3:]) <= 2 * L * per_block  # ~ the pages whose tier really changes
