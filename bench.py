@@ -63,7 +63,7 @@ CONFIGS = {
     # tier is live. Blocks [0, prefill) are appended from synthetic K/V (no denoising), then
     # `blocks` more are generated through generate_block and timed.
     "c5": dict(layers=40, heads=40, head_dim=128, block_len=4680, blocks=2, prefill=60,
-               device_blocks=30, frame_shape=(16, 16), weights="device",
+               device_blocks=30, stage_budget_gb=24, frame_shape=(16, 16), weights="device",
                desc="c5: Wan2.1-14B-shaped LV rollout on 1 GPU: 60+ cached blocks (30 blocks of "
                     "pages = 115 GB in HBM, the rest on the pinned host tier), 2 blocks timed"),
 }
@@ -377,6 +377,7 @@ def run_host_tier_bench(args, c, cfgname, local):
     sched = E.DenoiseSchedule(STEPS)
     noise = torch.randn(T, mc.model_dim, device="cuda", generator=g)
     runner = E._runner(model)
+    runner.stager.budget = c.get("stage_budget_gb", 8) << 30  # HBM left after pool + weights
 
     def block(ch):
         return E.generate_block(model, cache, sched, None, ch, 0, noise=noise.clone(), to_host=False)

@@ -129,7 +129,7 @@ struct Move {
   int64_t epoch;  // the call that logged it: batches execute per call, in call order
   int kind;
   int dir;  // 0 device -> host (demote), 1 host -> device (restore)
-  int64_t dev_slot, host_slot;
+  int64_t dev_slot, host_slot;  // a demotion's host slot is assigned when its epoch ends
   bool live;
 };
 
@@ -171,6 +171,7 @@ struct ifx_pagetable {
   // (the LRU churn of a whole-context fetch) cancels instead of moving twice.
   void begin_call() {
     if (batch_depth > 0) return;
+    finalize_epoch();
     epoch++;
     for (Page* p : pend_pages) p->pending = -1;
     pend_pages.clear();
@@ -228,6 +229,20 @@ struct ifx_pagetable {
     lru_sync();
   }
 
+  // End of an epoch: pages still demoted get their host slot now. Assigning it lazily
+  // means a page demoted and restored again within the epoch never holds one, so a batch
+  // whose LRU churn cycles the whole device tier needs host slots only for the pages
+  // whose tier really changed (not for every page in flight). Host slots freed by this
+  // epoch's restores are still deferred here, so no H2D source is handed out.
+  void finalize_epoch() {
+    for (Page* p : pend_pages)
+      if (p->tier == 1 && p->slot < 0 && p->pending >= 0) {
+        const int64_t hs = pools[p->stream & 1][1].take();
+        moves[p->pending].host_slot = hs;
+        p->slot = hs;
+      }
+  }
+
   // Make device slot s available to a page being restored in the epoch that demoted it:
   // free -> take it; held by a page whose H2D into s is still pending -> retarget that H2D.
   bool reclaim_device_slot(SlotPool& dp, int64_t s) {
@@ -254,12 +269,11 @@ struct ifx_pagetable {
       p->slot = p->prev_slot;
       p->pending = -1;
     } else {
-      const int64_t hs = pools[k][1].take();
-      moves.push_back(Move{epoch, k, 0, p->slot, hs, true});
+      moves.push_back(Move{epoch, k, 0, p->slot, -1, true});  // host slot: finalize_epoch()
       pools[k][0].give(p->slot);  // read by the D2H batch before any H2D may refill it
       p->pending = (int64_t)moves.size() - 1;
       p->prev_slot = p->slot;
-      p->slot = hs;
+      p->slot = -1;
       pend_pages.push_back(p);
     }
     p->tier = 1;
@@ -282,8 +296,7 @@ struct ifx_pagetable {
       // demoted earlier in this epoch: its data never left its device slot, which it gets
       // back (a page restored into that slot meanwhile is pointed at another one before its
       // H2D runs) -- the demotion's D2H is cancelled, nothing moves
-      moves[p->pending].live = false;
-      pools[k][1].give(p->slot);  // written only by the cancelled D2H
+      moves[p->pending].live = false;  // (no host slot was assigned to it yet)
       p->pending = -1;
       p->slot = p->prev_slot;
       dp.holder[p->slot] = p;
@@ -296,6 +309,10 @@ struct ifx_pagetable {
     }
     const int64_t ds = dp.take();
     dp.holder[ds] = p;
+    if (p->slot < 0) {  // demoted in this epoch and its device slot could not be reclaimed:
+      p->slot = pools[k][1].take();  // round trip through a host slot (D2H before H2D)
+      moves[p->pending].host_slot = p->slot;
+    }
     {
       // (a demotion earlier in this call, if any, stays live: D2H runs before H2D)
       moves.push_back(Move{epoch, k, 1, ds, p->slot, true});
@@ -571,6 +588,7 @@ int ifx_pt_batch_end(ifx_pagetable* pt) {
 
 int ifx_pt_drain_moves(ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* n_records) {
   std::lock_guard<std::mutex> g(pt->mu);
+  pt->finalize_epoch();
   std::vector<const Move*> live;
   for (const Move& m : pt->moves)
     if (m.live) live.push_back(&m);
@@ -605,6 +623,7 @@ int ifx_pt_slots(ifx_pagetable* pt, int64_t layer, int kind, int64_t start, int6
   std::lock_guard<std::mutex> g(pt->mu);
   if (int rc = check_stream(pt, layer, kind)) return rc;
   Stream& st = pt->streams[layer * 2 + kind];
+  pt->finalize_epoch();
   *n = 0;
   *first_token = start;
   if (start >= end) return IFX_OK;

@@ -407,14 +407,15 @@ PAGED_K1_PAGE_LENS = (8, 16, 32, 64, 128)  # page boxes that tile K1's 128-key t
 
 
 class _Stager:
-    """HBM staging pool for host-tier context pages (one per runner, reused by blocks).
+    """HBM staging buffers for host-tier context pages (one per runner, reused by blocks).
 
     K1 cannot stream pages out of host memory at tensor-core speed (every key tile is read
     by all query tiles), so before a layer's attention its host pages are copied H2D (K6,
-    PCIe) into staging slots, on a side stream, one attention call ahead: the copy for the
-    next layer overlaps this layer's attention. If every layer's host pages fit the budget
-    they are staged once per block (the data is constant within a block); otherwise 2
-    buffers rotate between consecutive layers (3 for an odd layer count)."""
+    PCIe) into a staging buffer on a side stream, ahead of use. Buffers hold one layer's
+    host pages each; if every host layer gets its own buffer within the budget, pages are
+    staged once per block (their data is constant within a block), otherwise the buffers
+    rotate over the host-layer attention calls in order, so the copies for the next host
+    layers run while device-resident layers compute."""
 
     def __init__(self, dev, budget_bytes: int | None = None):
         self.dev = dev
@@ -423,6 +424,7 @@ class _Stager:
         self.budget = budget_bytes if budget_bytes is not None else int(
             os.environ.get("IFX_STAGE_BUDGET_MB", "8192")) << 20
         self.staged_pages = 0  # pages copied H2D for attention (all blocks)
+        self.buffers = None     # fixed number of rotating buffers (tests), None = budget
 
     def ensure(self, slots: int, page_len: int, width: int, dtype) -> None:
         rows = slots * page_len
@@ -430,7 +432,7 @@ class _Stager:
                 and self.k.dtype == dtype:
             return
         self.copy.synchronize()  # no staging copy may still write the old buffers
-        rows = max(rows, 2 * (self.k.shape[0] if self.k is not None else 0))
+        self.k = self.v = None
         self.k = torch.zeros(rows, width, device=self.dev, dtype=dtype)
         self.v = torch.zeros_like(self.k)
 
@@ -440,9 +442,10 @@ class _KvContext:
 
     Built once per block after the context fetch's bookkeeping (restore-on-read + clock,
     whose tier moves the cache executes). K1 reads device-tier pages IN PLACE from the pool
-    through a per-layer slot table; host-tier pages come from the staging pool (_Stager).
-    Page lengths K1 cannot box (not in PAGED_K1_PAGE_LENS) fall back to a K7 gather of the
-    context into a contiguous scratch per call."""
+    through a per-layer slot table; host-tier pages (table code -1-i = the layer's i-th
+    host page) come from a staging buffer (_Stager). Page lengths K1 cannot box (not in
+    PAGED_K1_PAGE_LENS) fall back to a K7 gather of the context into a contiguous scratch
+    per call."""
 
     def __init__(self, model, cache: KvCache, stager: _Stager, passes: int):
         self.cache = cache
@@ -453,7 +456,7 @@ class _KvContext:
         self.paged = cfg.page_len in PAGED_K1_PAGE_LENS
         self.stager = stager
         self.calls = 0
-        self.n_calls = passes * L
+        self.passes = passes
         self.ranges = []
         for li in range(L):  # the reference's fetch order: layer 0..L-1 (engine.py:228-237)
             lo, hi = cache.addressable_range(li, SELF_ATTN)
@@ -471,87 +474,85 @@ class _KvContext:
         self.prepared = True
         cache, stager, L = self.cache, self.stager, self.L
         self.first = [0] * L
-        self.host_moves = [None] * L
-        self.buf_of = [0] * L
-        self.moves_dev = None
+        self.jobs = []  # host layers in call order within a pass
         if not self.paged:
             return
-        tables, host = [], []
+        tables, host_slots = [], [None] * L
         for li, (lo, hi) in enumerate(self.ranges):
             codes, first = cache.slot_table(li, SELF_ATTN, lo, hi) if hi > lo else (np.zeros(0, np.int32), lo)
             self.first[li] = first
+            h = np.flatnonzero(codes < 0)
+            if len(h):
+                host_slots[li] = (-1 - codes[h]).astype(np.int64)
+                codes = codes.copy()
+                codes[h] = -1 - np.arange(len(h), dtype=np.int32)  # i-th host page of the layer
+                self.jobs.append(li)
             tables.append(codes)
-            host.append(np.flatnonzero(codes < 0))
-        per_layer = max((len(h) for h in host), default=0)
-        W = self.pool.width
-        if per_layer:
-            slot_b = self.P * W * self.pool.esz
-            total = sum(len(h) for h in host)
-            self.once = bool(total * slot_b <= stager.budget or L <= 3)
-            if self.once:  # every layer its own region: staged once per block
-                self.buf_of = list(range(L))
-                offs = np.cumsum([0] + [len(h) for h in host])
-            else:          # 2 rotating buffers (3 for an odd layer count)
-                self.buf_of = [li % 2 for li in range(L)]
-                if L % 2:
-                    self.buf_of[L - 1] = 2
-                offs = [self.buf_of[li] * per_layer for li in range(L)]
-            need = max(int(offs[li]) + len(h) for li, h in enumerate(host))
-            stager.ensure(need, self.P, W, self.pool.dtype)
-            for li, h in enumerate(host):
-                if len(h):
-                    hs = -1 - tables[li][h].astype(np.int64)
-                    st = int(offs[li]) + np.arange(len(h), dtype=np.int64)
-                    tables[li] = tables[li].copy()
-                    tables[li][h] = (-1 - st).astype(np.int32)
-                    self.host_moves[li] = np.stack([st, hs], axis=1)
         dev = require_cuda()
         runs = [tile_run_codes(t, self.P) for t in tables]
+        pairs = [np.stack([np.arange(len(hs), dtype=np.int64), hs], axis=1)
+                 for hs in host_slots if hs is not None]
         flat = np.concatenate(tables + runs)
         allt = torch.from_numpy(flat).to(dev, non_blocking=True)
         lens = np.cumsum([0] + [len(t) for t in tables + runs])
         self.tables = [allt[lens[i]:lens[i + 1]] for i in range(L)]
         self.runs = [allt[lens[L + i]:lens[L + i + 1]] for i in range(L)]
-        mv = [m for m in self.host_moves if m is not None]
-        if mv:
-            allm = torch.from_numpy(np.concatenate(mv)).to(dev, non_blocking=True)
-            self.moves_dev, o = [None] * L, 0
-            for li, m in enumerate(self.host_moves):
-                if m is not None:
-                    self.moves_dev[li] = allm[o:o + len(m)]
-                    o += len(m)
-            self.staged = {}
-            self.consumed = {}
-            start = torch.cuda.Event()
-            start.record()  # tier moves + table uploads of this block are enqueued before it
-            stager.copy.wait_event(start)
-            if self.once:
-                for li in range(L):
-                    self._stage(li, li)
-            else:
-                self._stage(0, 0)
-
-    def _stage(self, call: int, li: int) -> None:
-        """Enqueue the H2D copy of layer li's host pages for attention call `call`."""
-        if self.moves_dev is None or self.moves_dev[li] is None:
+        if not self.jobs:
             return
-        st = self.stager
-        buf = self.buf_of[li]
+        allm = torch.from_numpy(np.concatenate(pairs)).to(dev, non_blocking=True)
+        self.moves = [None] * L
+        o = 0
+        for li in self.jobs:
+            n = len(host_slots[li])
+            self.moves[li] = allm[o:o + n]
+            o += n
+        self.job_of = {li: i for i, li in enumerate(self.jobs)}
+        H = len(self.jobs)
+        self.R = max(len(host_slots[li]) for li in self.jobs)  # slots per buffer
+        buf_bytes = self.R * self.P * self.pool.width * self.pool.esz
+        fit = max(1, stager.budget // max(1, buf_bytes))
+        self.nbuf = H if (fit >= H or H == 1) else max(2, fit)
+        if stager.buffers is not None:
+            self.nbuf = max(1 if H == 1 else 2, min(H, stager.buffers))
+        self.resident = self.nbuf == H  # every host layer keeps its buffer: stage once
+        stager.ensure(self.nbuf * self.R, self.P, self.pool.width, self.pool.dtype)
+        self.n_jobs = H if self.resident else H * self.passes
+        self.staged, self.consumed = {}, {}
+        start = torch.cuda.Event()
+        start.record()  # tier moves + table uploads of this block are enqueued before it
+        stager.copy.wait_event(start)
+        for j in range(min(self.nbuf, self.n_jobs)):
+            self._stage(j)
+
+    def _buf(self, j: int) -> int:
+        return j % self.nbuf
+
+    def _stage_views(self, buf: int):
+        r0, r1 = buf * self.R * self.P, (buf + 1) * self.R * self.P
+        return self.stager.k[r0:r1], self.stager.v[r0:r1]
+
+    def _stage(self, j: int) -> None:
+        """Enqueue job j: the H2D copy of host layer jobs[j % H]'s pages into buffer j % nbuf,
+        after the attention that last read that buffer."""
+        st, li = self.stager, self.jobs[j % len(self.jobs)]
+        buf = self._buf(j)
         if buf in self.consumed:
             st.copy.wait_event(self.consumed[buf])
-        p = _abi.KvPool()
+        k, v = self._stage_views(buf)
         pool = self.pool
-        p.dev_k, p.dev_v = st.k.data_ptr(), st.v.data_ptr()
+        p = _abi.KvPool()
+        p.dev_k, p.dev_v = k.data_ptr(), v.data_ptr()
         p.host_k, p.host_v = pool.host_k.ptr, pool.host_v.ptr
-        p.width, p.page_len, p.type = pool.width, pool.page_len, _abi.BF16 if pool.dtype == torch.bfloat16 else _abi.F32
-        m = self.moves_dev[li]
+        p.width, p.page_len = pool.width, pool.page_len
+        p.type = _abi.BF16 if pool.dtype == torch.bfloat16 else _abi.F32
+        m = self.moves[li]
         _abi.check(_abi.lib().ifx_kv_move_pages(ctypes.byref(p), m.data_ptr(), m.shape[0], 1,
                                                st.copy.cuda_stream), "stage")
         count_launch()
         st.staged_pages += m.shape[0]
         ev = torch.cuda.Event()
         ev.record(st.copy)
-        self.staged[call if not self.once else li] = ev
+        self.staged[j] = ev
 
     def attend(self, li: int, q, heads: int, dhp: int, out, cur_k, cur_v, scale: float, attn=None):
         """K1 for layer li: q over [this layer's cached context ∥ the block's own K/V]."""
@@ -565,21 +566,22 @@ class _KvContext:
         if not self.paged:  # K7 gather of the context (host pages read over PCIe in place)
             k, v = self.cache._gather(li, SELF_ATTN, None, lo, hi - lo, lo, hi, raw=True)
             return attn(q, heads, dhp, out, k, v, 0, hi - lo, cur_k, cur_v, scale=scale)
-        staged = self.moves_dev is not None and self.moves_dev[li] is not None
-        if staged:
-            torch.cuda.current_stream().wait_event(self.staged[li if self.once else call])
-        pool, st = self.pool, self.stager
+        j = None
+        if self.jobs and li in self.job_of:
+            idx = self.job_of[li]
+            j = idx if self.resident else (call // self.L) * len(self.jobs) + idx
+            torch.cuda.current_stream().wait_event(self.staged[j])
+        sk, sv = self._stage_views(self._buf(j)) if j is not None else (None, None)
+        pool = self.pool
         attn(q, heads, dhp, out, pool.dev_k, pool.dev_v, lo, hi - lo, cur_k, cur_v, scale=scale,
              ctx_slots=self.tables[li], page_len=self.P, first_token=self.first[li],
-             stage_k=st.k if staged else None, stage_v=st.v if staged else None,
-             tile_runs=self.runs[li])
-        if self.moves_dev is not None and not self.once:
-            if staged:
-                ev = torch.cuda.Event()
-                ev.record()
-                self.consumed[self.buf_of[li]] = ev
-            if call + 1 < self.n_calls:
-                self._stage(call + 1, (li + 1) % self.L)
+             stage_k=sk, stage_v=sv, tile_runs=self.runs[li])
+        if j is not None and not self.resident:
+            ev = torch.cuda.Event()
+            ev.record()
+            self.consumed[self._buf(j)] = ev
+            if j + self.nbuf < self.n_jobs:
+                self._stage(j + self.nbuf)
         return out
 
 

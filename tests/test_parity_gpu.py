@@ -348,9 +348,9 @@ def test_long_context_c3_bookkeeping_bit_exact():
 
 # ---------------------------------------------------------------- pinned-host tier
 @pytest.mark.parametrize("case", [
-    # layers, page_len, device capacity (pages), stage budget (bytes), window
-    (5, 16, 18, 0, None),          # rotating 3-buffer staging (odd layer count)
-    (4, 16, 14, 0, None),          # rotating 2-buffer staging
+    # layers, page_len, device capacity (pages), stage budget (bytes or "N buffers"), window
+    (5, 16, 18, "3", None),        # 3 staging buffers rotating over the host layers
+    (4, 16, 14, 0, None),          # 2 rotating buffers (the minimum)
     (3, 16, 12, 1 << 30, None),    # every layer's host pages staged once per block
     (2, 16, 7, 0, None),           # few layers: staged once per block regardless of budget
     (2, 8, 9, 0, 70),              # 8-row pages + window eviction
@@ -371,7 +371,10 @@ def test_engine_host_tier_vs_oracle(case):
                capacity_pages_host=10**4)
     model = E.build_model(E.ModelConfig(**kw))
     runner = E._runner(model)
-    runner.stager.budget = budget
+    if isinstance(budget, str):
+        runner.stager.buffers, runner.stager.budget = int(budget), 0
+    else:
+        runner.stager.buffers, runner.stager.budget = None, budget
     staged0 = runner.stager.staged_pages
     eng = E.Engine(model, E.KvConfig(**kvc))
     got = np.stack([b.latent for b in eng.generate(E.GenerationRequest(

@@ -161,6 +161,8 @@ def test_batched_context_fetch_cancels_lru_churn():
             for li in range(L):
                 pt.append(li, "self_attn", per_block * P, b)
             moved.append(n)
+            # host slots are only held by pages really on the host (plus this batch's slack)
+            assert pt.pool_extent()[1] <= pt.state()["host_used"] + 2 * L * per_block
         return moved, pt.state()
 
     per_call, st1 = run(False)
