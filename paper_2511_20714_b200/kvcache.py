@@ -375,12 +375,17 @@ class KvCache:
     def _sync(self, stream=None) -> None:
         """Grow the pools to the page table's slot high-water marks, then execute the tier
         moves its last call logged (K6: device->host batch, then host->device batch)."""
+        mv = self._pt.drain_moves()  # first: the drain assigns demotions' host slots
         ext = self._pt.pool_extent()
         self._pools[SELF_ATTN].ensure(ext[0], ext[1])
         self._pools[CROSS_ATTN].ensure(ext[2], ext[3])
-        mv = self._pt.drain_moves()
         if not len(mv):
             return
+        for kind_code, pool in ((0, self._pools[SELF_ATTN]), (1, self._pools[CROSS_ATTN])):
+            sel = mv[:, 1] == kind_code
+            if sel.any() and (mv[sel, 3].max() >= pool.dev_slots or mv[sel, 4].max() >= pool.host_slots
+                              or mv[sel, 3:5].min() < 0):
+                raise RuntimeError("page move outside the pools (page table / pool size mismatch)")
         dev = require_cuda()
         pairs = torch.from_numpy(np.ascontiguousarray(mv[:, 3:5])).to(dev, non_blocking=True)
         # consecutive records with the same (epoch, dir, kind) form one hazard-free launch
