@@ -356,6 +356,16 @@ def run_host_tier_bench(args, c, cfgname, local):
     T, L, W = mc.block_len, mc.layers, model.attn_width
     pages_blk = -(-T // 16)
     nb_pre, nb = c["prefill"], max(c["blocks"], args.steps)
+    # the host tier lives in pinned RAM: size the rollout to what this box can pin
+    # (MemAvailable x 0.6), so the run reports the longest cache it can actually hold
+    blk_host_bytes = L * pages_blk * 2 * 16 * W * 2
+    try:
+        with open("/proc/meminfo") as f:
+            avail = next(int(x.split()[1]) * 1024 for x in f if x.startswith("MemAvailable"))
+        max_host_blocks = int(0.6 * avail // blk_host_bytes)
+        nb_pre = max(1, min(nb_pre, c["device_blocks"] + max_host_blocks - nb - 3))
+    except (OSError, StopIteration):
+        pass
     kvc = E.default_kv_config(mc, capacity_pages_device=c["device_blocks"] * L * pages_blk,
                               capacity_pages_host=(nb_pre + nb + 2) * L * pages_blk)
     cache = KvCache(kvc, dtype=torch.bfloat16, reserve_tokens=T * (c["device_blocks"] + 1), row_width=W)
