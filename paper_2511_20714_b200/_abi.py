@@ -38,7 +38,7 @@ EXPORTS = (
     "ifx_pt_create", "ifx_pt_destroy", "ifx_pt_append", "ifx_pt_offload", "ifx_pt_evict_window",
     "ifx_pt_clear_cross", "ifx_pt_touch_range", "ifx_pt_touch_indices", "ifx_pt_range",
     "ifx_pt_stats", "ifx_pt_snapshot", "ifx_pt_drain_moves", "ifx_pt_pool_extent", "ifx_pt_slots",
-    "ifx_pt_batch_begin", "ifx_pt_batch_end",
+    "ifx_pt_batch_begin", "ifx_pt_batch_end", "ifx_pt_pending",
     "ifx_kv_append", "ifx_kv_gather", "ifx_kv_move_pages", "ifx_host_alloc", "ifx_host_free",
     "ifx_attn_fwd", "ifx_attn_workspace_bytes",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_ulysses_pack", "ifx_ulysses_unpack",
@@ -112,6 +112,7 @@ def lib() -> ctypes.CDLL:
             L.ifx_pt_drain_moves.argtypes = [P, PI64, I64, PI64]
             L.ifx_pt_batch_begin.argtypes = [P]
             L.ifx_pt_batch_end.argtypes = [P]
+            L.ifx_pt_pending.argtypes = [P, PI64]
             L.ifx_pt_pool_extent.argtypes = [P, PI64]
             L.ifx_pt_slots.argtypes = [P, I64, ctypes.c_int, I64, I64, P, I64, PI64, PI64]
             PPOOL = ctypes.POINTER(KvPool)

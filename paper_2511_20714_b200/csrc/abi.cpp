@@ -87,6 +87,33 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   const int64_t width = p->heads * p->head_dim;
   if (p->n_q > INT32_MAX || p->ctx_rows > INT32_MAX || p->n_cur > INT32_MAX)
     return fail(IFX_EDIM, "attention extents must fit int32");
+  // a handful of keys (cross-attention to the prompt): K1s, SIMT, no tensor-core tile
+  if (!paged && p->mask == nullptr && p->row_max == nullptr &&
+      p->n_ctx + p->n_cur <= attn_few_keys_max() && p->n_q * p->heads >= 1024 &&
+      4 * (p->n_ctx + p->n_cur) * width <= 200 * 1024 &&  // K and V of all heads in smem
+      ((p->q_ld | p->ctx_ld | p->cur_ld | p->o_ld | width) % 8) == 0 &&
+      ((reinterpret_cast<uintptr_t>(p->k_ctx) | reinterpret_cast<uintptr_t>(p->v_ctx) |
+        reinterpret_cast<uintptr_t>(p->k_cur) | reinterpret_cast<uintptr_t>(p->v_cur) |
+        reinterpret_cast<uintptr_t>(p->q) | reinterpret_cast<uintptr_t>(p->o)) & 15) == 0) {
+    FewKeysArgs f;
+    f.q = static_cast<const __nv_bfloat16*>(p->q);
+    f.q_ld = p->q_ld;
+    f.k_ctx = static_cast<const __nv_bfloat16*>(p->k_ctx) + p->ctx_row0 * p->ctx_ld;
+    f.v_ctx = static_cast<const __nv_bfloat16*>(p->v_ctx) + p->ctx_row0 * p->ctx_ld;
+    f.ctx_ld = p->ctx_ld;
+    f.k_cur = static_cast<const __nv_bfloat16*>(p->k_cur);
+    f.v_cur = static_cast<const __nv_bfloat16*>(p->v_cur);
+    f.cur_ld = p->cur_ld;
+    f.o = static_cast<__nv_bfloat16*>(p->o);
+    f.o_ld = p->o_ld;
+    f.n_q = (int)p->n_q;
+    f.n_ctx = (int)p->n_ctx;
+    f.n_cur = (int)p->n_cur;
+    f.heads = (int)p->heads;
+    f.scale_log2 = p->scale * 1.4426950408889634f;
+    return cuda_fail(attn_few_keys_launch(f, (int)p->head_dim, static_cast<cudaStream_t>(stream)),
+                     "attn_few_keys launch");
+  }
   AttnKernelArgs a;
   std::memset(&a, 0, sizeof(a));
   int rc;

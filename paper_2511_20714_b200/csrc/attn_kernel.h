@@ -45,6 +45,22 @@ struct AttnKernelArgs {
   float* part_l;          // [n_splits, heads, n_q] denominator w.r.t. part_m
 };
 
+// K1s (attn_few_keys.cu): attention over <= attn_few_keys_max() keys, SIMT
+struct FewKeysArgs {
+  const __nv_bfloat16* q;
+  int64_t q_ld;
+  const __nv_bfloat16 *k_ctx, *v_ctx;
+  int64_t ctx_ld;
+  const __nv_bfloat16 *k_cur, *v_cur;
+  int64_t cur_ld;
+  __nv_bfloat16* o;
+  int64_t o_ld;
+  int n_q, n_ctx, n_cur, heads;
+  float scale_log2;
+};
+int attn_few_keys_max();
+int attn_few_keys_launch(const FewKeysArgs& a, int head_dim, cudaStream_t st);
+
 // Grid (ceil(n_q/128), heads, n_splits) x 320 threads (+ K4 combine when n_splits > 1).
 // Returns cudaError_t.
 int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int n_q, int heads, cudaStream_t st);

@@ -586,6 +586,16 @@ int ifx_pt_batch_end(ifx_pagetable* pt) {
   return IFX_OK;
 }
 
+int ifx_pt_pending(const ifx_pagetable* pt, int64_t* out2) {
+  int64_t live = 0, lazy = 0;
+  for (const Move& m : pt->moves) live += m.live ? 1 : 0;
+  for (const Page* p : pt->pend_pages)
+    lazy += (p->tier == 1 && p->slot < 0 && p->pending >= 0) ? 1 : 0;
+  out2[0] = live;
+  out2[1] = lazy;
+  return IFX_OK;
+}
+
 int ifx_pt_drain_moves(ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* n_records) {
   std::lock_guard<std::mutex> g(pt->mu);
   pt->finalize_epoch();

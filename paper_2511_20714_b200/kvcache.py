@@ -269,6 +269,12 @@ class PageTable:
     def batch_end(self) -> None:
         _abi.check(_abi.lib().ifx_pt_batch_end(self._h))
 
+    def pending(self) -> tuple:
+        """(live moves, demotions waiting for a host slot) of the open epoch."""
+        out = (ctypes.c_int64 * 2)()
+        _abi.check(_abi.lib().ifx_pt_pending(self._h, out))
+        return out[0], out[1]
+
     def pool_extent(self) -> list:
         """Slots ever used: [self device, self host, cross device, cross host]."""
         out = (ctypes.c_int64 * 4)()
@@ -415,6 +421,28 @@ class KvCache:
                 self._pt.batch_end()
                 if self._batch == 0:
                     self._sync(stream)
+
+    def batch_checkpoint(self, stream=None) -> None:
+        """Inside batch(): if the demotions waiting for a host slot would outgrow the pinned
+        host pool already allocated, run this batch's moves now and continue in a fresh
+        one (bounds the host footprint of a fetch whose tiers change a lot, e.g. the first
+        fetch after a long prefill, at the price of fewer cancelled moves)."""
+        if not getattr(self, "_batch", 0):
+            return
+        _, lazy = self._pt.pending()
+        ext = self._pt.pool_extent()
+        spare = []
+        for pool, used in ((self._pools[SELF_ATTN], ext[1]), (self._pools[CROSS_ATTN], ext[3])):
+            free = pool.host_slots - used
+            if pool.host_slots * pool.slot_bytes < (4 << 30):  # small pools may still double
+                free = max(free, pool.host_slots)
+            spare.append(free)
+        if lazy > max(min(spare), 0):
+            self._pt.batch_end()
+            try:
+                self._sync(stream)
+            finally:
+                self._pt.batch_begin()
 
     def _no_batch(self, what: str) -> None:
         if getattr(self, "_batch", 0):

@@ -39,6 +39,12 @@ CASES = [
     (12, 128, 520, 384, 0, 520),
     (1, 128, 64, 3, 0, 0),
     (2, 64, 33, 0, 0, 2),
+    # K1s (few keys: cross-attention to a prompt), dispatched inside ifx_attn_fwd
+    (12, 128, 4680, 3, 0, 0),
+    (12, 128, 1000, 3, 5, 2),
+    (4, 64, 600, 0, 0, 17),
+    (40, 128, 300, 8, 1, 0),
+    (40, 128, 300, 32, 1, 0),  # K/V of 40 heads x 32 keys exceed K1s' smem: K1 instead
 ]
 
 
