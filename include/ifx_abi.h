@@ -101,10 +101,12 @@ int ifx_pt_drain_moves(ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* n_
  * drain after the outermost end, before reading the data. */
 int ifx_pt_batch_begin(ifx_pagetable* pt);
 int ifx_pt_batch_end(ifx_pagetable* pt);
-/* Pending work of the open epoch: out2[0] = live moves, out2[1] = demotions still waiting
- * for a host slot (each needs one at the drain, on top of the slots in use). A caller
- * whose host pool cannot absorb that many closes the batch early (drain, run, reopen). */
-int ifx_pt_pending(const ifx_pagetable* pt, int64_t* out2);
+/* Pending work of the open epoch: out3[0] = live moves, out3[1] = demotions still waiting
+ * for a host slot (each needs one at the drain, on top of the slots in use), out3[2] = those
+ * of them on self-attention streams of layers <= max_layer (in a layer-ordered context fetch
+ * they will not be restored again before the batch ends). A caller whose host pool cannot
+ * absorb the committed ones closes the batch early (drain, run, reopen). */
+int ifx_pt_pending(const ifx_pagetable* pt, int64_t max_layer, int64_t* out3);
 /* slots ever used per pool: out4[kind*2 + tier] (tier 0 device, 1 host) */
 int ifx_pt_pool_extent(const ifx_pagetable* pt, int64_t* out4);
 /* Slot codes of the pages covering tokens [start, end) of a stream (within its stored

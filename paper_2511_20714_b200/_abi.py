@@ -112,7 +112,7 @@ def lib() -> ctypes.CDLL:
             L.ifx_pt_drain_moves.argtypes = [P, PI64, I64, PI64]
             L.ifx_pt_batch_begin.argtypes = [P]
             L.ifx_pt_batch_end.argtypes = [P]
-            L.ifx_pt_pending.argtypes = [P, PI64]
+            L.ifx_pt_pending.argtypes = [P, I64, PI64]
             L.ifx_pt_pool_extent.argtypes = [P, PI64]
             L.ifx_pt_slots.argtypes = [P, I64, ctypes.c_int, I64, I64, P, I64, PI64, PI64]
             PPOOL = ctypes.POINTER(KvPool)

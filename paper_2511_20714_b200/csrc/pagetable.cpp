@@ -586,13 +586,18 @@ int ifx_pt_batch_end(ifx_pagetable* pt) {
   return IFX_OK;
 }
 
-int ifx_pt_pending(const ifx_pagetable* pt, int64_t* out2) {
-  int64_t live = 0, lazy = 0;
+int ifx_pt_pending(const ifx_pagetable* pt, int64_t max_layer, int64_t* out3) {
+  int64_t live = 0, lazy = 0, committed = 0;
   for (const Move& m : pt->moves) live += m.live ? 1 : 0;
+  std::set<const Page*> seen;
   for (const Page* p : pt->pend_pages)
-    lazy += (p->tier == 1 && p->slot < 0 && p->pending >= 0) ? 1 : 0;
-  out2[0] = live;
-  out2[1] = lazy;
+    if (p->tier == 1 && p->slot < 0 && p->pending >= 0 && seen.insert(p).second) {
+      lazy++;
+      if (p->stream % 2 == IFX_SELF_ATTN && p->stream / 2 <= max_layer) committed++;
+    }
+  out3[0] = live;
+  out3[1] = lazy;
+  out3[2] = committed;
   return IFX_OK;
 }
 

@@ -462,7 +462,7 @@ class _KvContext:
             lo, hi = cache.addressable_range(li, SELF_ATTN)
             if hi > lo:
                 cache.touch_range(li, (lo, hi), SELF_ATTN)
-                cache.batch_checkpoint()
+                cache.batch_checkpoint(fetched_layer=li)
             self.ranges.append((lo, hi))
         self.prepared = False
 

@@ -269,11 +269,12 @@ class PageTable:
     def batch_end(self) -> None:
         _abi.check(_abi.lib().ifx_pt_batch_end(self._h))
 
-    def pending(self) -> tuple:
-        """(live moves, demotions waiting for a host slot) of the open epoch."""
-        out = (ctypes.c_int64 * 2)()
-        _abi.check(_abi.lib().ifx_pt_pending(self._h, out))
-        return out[0], out[1]
+    def pending(self, max_layer: int = -1) -> tuple:
+        """(live moves, demotions waiting for a host slot, those of them on self streams of
+        layers <= max_layer) of the open epoch."""
+        out = (ctypes.c_int64 * 3)()
+        _abi.check(_abi.lib().ifx_pt_pending(self._h, max_layer, out))
+        return out[0], out[1], out[2]
 
     def pool_extent(self) -> list:
         """Slots ever used: [self device, self host, cross device, cross host]."""
@@ -422,14 +423,16 @@ class KvCache:
                 if self._batch == 0:
                     self._sync(stream)
 
-    def batch_checkpoint(self, stream=None) -> None:
-        """Inside batch(): if the demotions waiting for a host slot would outgrow the pinned
-        host pool already allocated, run this batch's moves now and continue in a fresh
-        one (bounds the host footprint of a fetch whose tiers change a lot, e.g. the first
-        fetch after a long prefill, at the price of fewer cancelled moves)."""
+    def batch_checkpoint(self, fetched_layer: int = 10**9, stream=None) -> None:
+        """Inside a layer-ordered context fetch in batch(): if the demotions that will not be
+        undone before the batch ends (pages of layers <= fetched_layer) would outgrow the
+        pinned host pool already allocated, run this batch's moves now and continue in a
+        fresh one. Bounds the host footprint of a fetch whose tiers change a lot (e.g. the
+        first fetch after a long prefill) without splitting the steady-state fetch, whose
+        mid-fetch demotions of later layers are all undone."""
         if not getattr(self, "_batch", 0):
             return
-        _, lazy = self._pt.pending()
+        _, _, lazy = self._pt.pending(fetched_layer)
         ext = self._pt.pool_extent()
         spare = []
         for pool, used in ((self._pools[SELF_ATTN], ext[1]), (self._pools[CROSS_ATTN], ext[3])):
