@@ -62,10 +62,11 @@ CONFIGS = {
     # c5 on ONE GPU: the cache of a minute-long rollout does not fit HBM, so the pinned host
     # tier is live. Blocks [0, prefill) are appended from synthetic K/V (no denoising), then
     # `blocks` more are generated through generate_block and timed.
-    "c5": dict(layers=40, heads=40, head_dim=128, block_len=4680, blocks=2, prefill=60,
+    "c5": dict(layers=40, heads=40, head_dim=128, block_len=4680, blocks=2, prefill=58,
                device_blocks=30, stage_budget_gb=24, frame_shape=(16, 16), weights="device",
                desc="c5: Wan2.1-14B-shaped LV rollout on 1 GPU: 60+ cached blocks (30 blocks of "
-                    "pages = 115 GB in HBM, the rest on the pinned host tier), 2 blocks timed"),
+                    "pages = 115 GB in HBM, the rest on the pinned host tier; cache state of a "
+                    "58-block rollout: per-block fetch + append bookkeeping), blocks 60-61 timed"),
 }
 
 
@@ -378,15 +379,18 @@ def run_host_tier_bench(args, c, cfgname, local):
         cache.append_block(li, kc, vc, kind=CROSS_ATTN, chunk_index=0)
     g = torch.Generator(device="cuda").manual_seed(0)
     kv = [torch.randn(T, W, device="cuda", generator=g).bfloat16() for _ in range(2)]
+    runner = E._runner(model)
     t0 = time.perf_counter()
-    for b in range(nb_pre):
+    for b in range(nb_pre):  # the cache state of a rollout: each block's context fetch
+        with cache.batch():  # (bookkeeping + tier moves, engine.py:297-298), then appends
+            E._KvContext(model, cache, runner.stager, 1)
+            E._touch_cross(model, cache)
         for li in range(L):
             cache.append_block(li, kv[0], kv[1], kind=SELF_ATTN, chunk_index=b)
     torch.cuda.synchronize()
     prefill_s = time.perf_counter() - t0
     sched = E.DenoiseSchedule(STEPS)
     noise = torch.randn(T, mc.model_dim, device="cuda", generator=g)
-    runner = E._runner(model)
     runner.stager.budget = c.get("stage_budget_gb", 8) << 30  # HBM left after pool + weights
 
     def block(ch):

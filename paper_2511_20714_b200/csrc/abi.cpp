@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -88,7 +89,8 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   if (p->n_q > INT32_MAX || p->ctx_rows > INT32_MAX || p->n_cur > INT32_MAX)
     return fail(IFX_EDIM, "attention extents must fit int32");
   // a handful of keys (cross-attention to the prompt): K1s, SIMT, no tensor-core tile
-  if (!paged && p->mask == nullptr && p->row_max == nullptr &&
+  static const bool few_keys_off = std::getenv("IFX_NO_FEW_KEYS") != nullptr;  // A/B probes
+  if (!few_keys_off && !paged && p->mask == nullptr && p->row_max == nullptr &&
       p->n_ctx + p->n_cur <= attn_few_keys_max() && p->n_q * p->heads >= 1024 &&
       4 * (p->n_ctx + p->n_cur) * width <= 200 * 1024 &&  // K and V of all heads in smem
       ((p->q_ld | p->ctx_ld | p->cur_ld | p->o_ld | width) % 8) == 0 &&

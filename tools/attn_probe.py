@@ -20,12 +20,29 @@ def main():
     ap.add_argument("--heads", type=int, default=12)
     ap.add_argument("--no-split", action="store_true")
     ap.add_argument("--paged", action="store_true", help="context through a page_len-16 slot table")
+    ap.add_argument("--cross", type=int, default=0, help="n prompt keys only (cross-attention)")
     args = ap.parse_args()
     T, H, dh = 4680, args.heads, 128
     D = H * dh
     res = []
-    for b in ((0, 1, 3, 6, 20) if not args.quick else (3,)):
+    for b in ((0, 1, 3, 6, 20) if not args.quick and not args.cross else (3,)):
         C = b * T
+        if args.cross:  # q over a few prompt keys, no own-block keys
+            k3 = torch.randn(args.cross, D, device="cuda").bfloat16()
+            out = torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
+            q = torch.randn(T, D, device="cuda").bfloat16()
+            f = lambda: attn_fwd(q, H, dh, out, k3, k3, 0, args.cross)  # noqa: E731
+            for _ in range(3):
+                f()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.iters):
+                f()
+            e1.record()
+            torch.cuda.synchronize()
+            print(json.dumps({"cross_keys": args.cross, "us": round(e0.elapsed_time(e1) / args.iters * 1e3, 2)}))
+            return
         qkv = torch.randn(T, 3 * D, device="cuda").bfloat16()
         ks = torch.randn(max(C, 1), D, device="cuda").bfloat16()
         vs = torch.randn(max(C, 1), D, device="cuda").bfloat16()
