@@ -92,7 +92,7 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   static const bool few_keys_off = std::getenv("IFX_NO_FEW_KEYS") != nullptr;  // A/B probes
   if (!few_keys_off && !paged && p->mask == nullptr && p->row_max == nullptr &&
       p->n_ctx + p->n_cur <= attn_few_keys_max() && p->n_q * p->heads >= 1024 &&
-      4 * (p->n_ctx + p->n_cur) * width <= 200 * 1024 &&  // K and V of all heads in smem
+      8 * (p->n_ctx + p->n_cur) * width <= 200 * 1024 &&  // K and V (fp32) of all heads in smem
       ((p->q_ld | p->ctx_ld | p->cur_ld | p->o_ld | width) % 8) == 0 &&
       ((reinterpret_cast<uintptr_t>(p->k_ctx) | reinterpret_cast<uintptr_t>(p->v_ctx) |
         reinterpret_cast<uintptr_t>(p->k_cur) | reinterpret_cast<uintptr_t>(p->v_cur) |

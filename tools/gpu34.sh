@@ -1,0 +1,7 @@
+export PYTHONPATH=$PWD
+mkdir -p gpurun_out
+timeout -k 10 120 python tools/attn_probe.py --cross 3 2>&1 | tail -1
+IFX_NO_FEW_KEYS=1 timeout -k 10 120 python tools/attn_probe.py --cross 3 2>&1 | tail -1
+timeout -k 10 300 python -m pytest tests/test_kernels_gpu.py -q -p no:cacheprovider -k attention 2>&1 | tail -2
+timeout -k 10 300 python tools/host_cost_probe.py 2>&1 | tail -1
+timeout -k 10 900 python bench.py --no-cpu-baseline 2>&1 | tail -1 | tee gpurun_out/bench_r03_c2.json
