@@ -146,6 +146,12 @@ int ifx_kv_gather(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_t
  * dir 0 device -> host, 1 host -> device. */
 int ifx_kv_move_pages(const ifx_kv_pool* pool, const int64_t* moves, int64_t n, int dir,
                       void* stream);
+/* The same page copies on the DMA copy engines instead of SMs: runs = HOST int64
+ * [n][3] (device slot, host slot, page count) of consecutive slots on both sides, one
+ * cudaMemcpyAsync per run and K/V. Used to stage host pages for attention while K1 holds
+ * every SM (a copy kernel would wait for free SMs). */
+int ifx_kv_copy_runs(const ifx_kv_pool* pool, const int64_t* runs, int64_t n, int dir,
+                     void* stream);
 /* pinned host memory mapped into the device address space (cudaHostAllocMapped; under UVA
  * the device address equals the host address) for the host pools */
 int ifx_host_alloc(int64_t bytes, void** out);
@@ -223,6 +229,13 @@ int ifx_attn_workspace_bytes(const ifx_attn_params* p, int64_t* bytes);
  * conditioned fp32 row is also written there. tvec may be NULL. */
 int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
                  float* x_out, void* y, void* stream);
+
+/* Folded cross-attention (engine.py:211-215 with the prompt's few keys): the logits of all
+ * heads come from one GEMM, s = rms(x) @ (cq . K^T) [rows, groups*group_size] fp32 (row
+ * stride ld); this writes p = bf16(softmax over each group of group_size logits * scale)
+ * (row stride p_ld), which then meets (V . co) in one more GEMM. */
+int ifx_group_softmax(const float* s, int64_t rows, int64_t groups, int64_t group_size,
+                      int64_t ld, float scale, void* p, int64_t p_ld, void* stream);
 
 /* 3D RoPE (B200 extension; the reference has no positional encoding, attention.py:6):
  * rotate, in place, the interleaved pairs (2k, 2k+1), k < pairs, of every head of the Q

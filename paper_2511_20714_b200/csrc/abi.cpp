@@ -92,7 +92,6 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   static const bool few_keys_off = std::getenv("IFX_NO_FEW_KEYS") != nullptr;  // A/B probes
   if (!few_keys_off && !paged && p->mask == nullptr && p->row_max == nullptr &&
       p->n_ctx + p->n_cur <= attn_few_keys_max() && p->n_q * p->heads >= 1024 &&
-      8 * (p->n_ctx + p->n_cur) * width <= 200 * 1024 &&  // K and V (fp32) of all heads in smem
       ((p->q_ld | p->ctx_ld | p->cur_ld | p->o_ld | width) % 8) == 0 &&
       ((reinterpret_cast<uintptr_t>(p->k_ctx) | reinterpret_cast<uintptr_t>(p->v_ctx) |
         reinterpret_cast<uintptr_t>(p->k_cur) | reinterpret_cast<uintptr_t>(p->v_cur) |
@@ -286,6 +285,27 @@ int ifx_kv_move_pages(const ifx_kv_pool* pool, const int64_t* moves, int64_t n, 
   return ifx::cuda_fail(e, "kv_move_pages launch");
 }
 
+int ifx_kv_copy_runs(const ifx_kv_pool* pool, const int64_t* runs, int64_t n, int dir,
+                     void* stream) {
+  if (int rc = check_pool(pool)) return rc;
+  if (n < 0 || (dir != 0 && dir != 1)) return ifx::fail(IFX_EDIM, "bad page run batch");
+  const int esz = pool->type == IFX_BF16 ? 2 : 4;
+  const int64_t slot_b = pool->page_len * pool->width * esz;
+  auto st = static_cast<cudaStream_t>(stream);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t ds = runs[3 * i], hs = runs[3 * i + 1], cnt = runs[3 * i + 2];
+    if (ds < 0 || hs < 0 || cnt < 1) return ifx::fail(IFX_EDIM, "bad page run");
+    for (int kv = 0; kv < 2; ++kv) {
+      char* dev = static_cast<char*>(kv ? pool->dev_v : pool->dev_k) + ds * slot_b;
+      char* host = static_cast<char*>(kv ? pool->host_v : pool->host_k) + hs * slot_b;
+      cudaError_t e = dir == 1 ? cudaMemcpyAsync(dev, host, cnt * slot_b, cudaMemcpyHostToDevice, st)
+                               : cudaMemcpyAsync(host, dev, cnt * slot_b, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return ifx::cuda_fail((int)e, "kv_copy_runs");
+    }
+  }
+  return IFX_OK;
+}
+
 int ifx_host_alloc(int64_t bytes, void** out) {
   *out = nullptr;
   if (bytes <= 0) return IFX_OK;
@@ -313,6 +333,17 @@ int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec,
   if (rows == 0) return IFX_OK;
   int e = ifx::rms_launch(x, rows, width, tvec, t, x_out, y, static_cast<cudaStream_t>(stream));
   return ifx::cuda_fail(e, "rms launch");
+}
+
+int ifx_group_softmax(const float* s, int64_t rows, int64_t groups, int64_t group_size,
+                      int64_t ld, float scale, void* p, int64_t p_ld, void* stream) {
+  if (rows < 0 || groups < 1 || group_size < 1 || ld < groups * group_size || p_ld < groups * group_size)
+    return ifx::fail(IFX_EDIM, "bad group softmax sizes");
+  if (rows == 0) return IFX_OK;
+  int e = ifx::group_softmax_launch(s, rows, (int)groups, (int)group_size, ld,
+                                    scale * 1.4426950408889634f, p, p_ld,
+                                    static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "group softmax launch");
 }
 
 int ifx_rope_qk(void* qkv, int64_t rows, int64_t ld, int64_t heads, int64_t head_stride,

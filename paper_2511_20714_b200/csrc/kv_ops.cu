@@ -242,6 +242,27 @@ __global__ void rope_qk_kernel(__nv_bfloat16* __restrict__ qkv, int64_t rows, in
   }
 }
 
+// ---- softmax over groups of a few logits (the folded cross-attention, engine.py:211-215):
+// p[r, g*gs + j] = bf16(softmax_j(s[r, g*gs + j] * scale)), one thread per (row, group)
+__global__ void group_softmax_kernel(const float* __restrict__ s, int64_t rows, int groups,
+                                     int gs, int64_t ld, float scale_log2,
+                                     __nv_bfloat16* __restrict__ p, int64_t p_ld) {
+  const int64_t total = rows * groups;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / groups;
+    const int g = (int)(i - r * groups);
+    const float* sr = s + r * ld + (int64_t)g * gs;
+    __nv_bfloat16* pr = p + r * p_ld + (int64_t)g * gs;
+    float m = -INFINITY;
+    for (int j = 0; j < gs; ++j) m = fmaxf(m, sr[j] * scale_log2);
+    float l = 0.f;
+    for (int j = 0; j < gs; ++j) l += exp2f(sr[j] * scale_log2 - m);
+    const float inv = 1.f / l;
+    for (int j = 0; j < gs; ++j) pr[j] = __float2bfloat16(exp2f(sr[j] * scale_log2 - m) * inv);
+  }
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t blocks = (work + threads - 1) / threads;
   const int64_t cap = (int64_t)kSMs * 8;
@@ -296,6 +317,14 @@ int kv_move_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t widt
   const int64_t units = n * 2 * ((page_vecs + piece - 1) / piece);
   move_pages<<<grid_for(units * 32, threads), threads, 0, st>>>(pool, moves, n, dir, page_vecs,
                                                                 piece);
+  return (int)cudaGetLastError();
+}
+
+int group_softmax_launch(const float* s, int64_t rows, int groups, int gs, int64_t ld,
+                         float scale_log2, void* p, int64_t p_ld, cudaStream_t st) {
+  const int threads = 256;
+  group_softmax_kernel<<<grid_for(rows * groups, threads), threads, 0, st>>>(
+      s, rows, groups, gs, ld, scale_log2, static_cast<__nv_bfloat16*>(p), p_ld);
   return (int)cudaGetLastError();
 }
 

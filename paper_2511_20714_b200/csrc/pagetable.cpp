@@ -68,40 +68,31 @@ struct Page {
 // slot allocator of one (kind, tier) pool: LIFO free list + high-water mark; frees of
 // host slots made during a call are deferred to the drain (see header)
 struct SlotPool {
-  std::vector<int64_t> free_list;  // LIFO; may hold stale entries (is_free decides)
-  std::vector<char> is_free;
-  std::vector<Page*> holder;       // page in each slot (device pools)
+  // free slots ordered: take() returns the smallest, so pages allocated or moved together
+  // get ascending consecutive slots (one TMA box per key tile in K1, one DMA per run when
+  // staging host pages)
+  std::set<int64_t> free_set;
+  std::vector<Page*> holder;  // page in each slot (device pools)
   std::vector<int64_t> deferred;
   std::vector<char> is_deferred;
   int64_t hwm = 0;
   void grow(int64_t s) {
-    if ((int64_t)is_free.size() <= s) {
-      is_free.resize(s + 1, 0);
-      holder.resize(s + 1, nullptr);
-    }
+    if ((int64_t)holder.size() <= s) holder.resize(s + 1, nullptr);
   }
   int64_t take() {
-    while (!free_list.empty()) {
-      int64_t s = free_list.back();
-      free_list.pop_back();
-      if (is_free[s]) {
-        is_free[s] = 0;
-        return s;
-      }
+    if (!free_set.empty()) {
+      const int64_t s = *free_set.begin();
+      free_set.erase(free_set.begin());
+      return s;
     }
     grow(hwm);
     return hwm++;
   }
-  bool take_specific(int64_t s) {  // the entry left on the stack becomes stale
-    if (s >= (int64_t)is_free.size() || !is_free[s]) return false;
-    is_free[s] = 0;
-    return true;
-  }
+  bool take_specific(int64_t s) { return free_set.erase(s) > 0; }
   void give(int64_t s) {
     grow(s);
-    is_free[s] = 1;
     holder[s] = nullptr;
-    free_list.push_back(s);
+    free_set.insert(s);
   }
   void defer(int64_t s) {
     if ((int64_t)is_deferred.size() <= s) is_deferred.resize(s + 1, 0);

@@ -304,6 +304,54 @@ def _cross_kv(model: ToyModel, prompt_emb: np.ndarray):
     return [(e @ lw.ck, e @ lw.cv) for lw in model.layers]
 
 
+class _CrossFold:
+    """Cross-attention of one layer folded through its few prompt keys (engine.py:211-215).
+
+    With n prompt keys per head, softmax(q K^T) V co with q = h cq equals
+    softmax_per_head(h (cq . K^T)) (V . co): cq . K^T is [D, H*n] and V . co is [H*n, D], so
+    the two D x D projections around the attention (cq, co: 2 * 2*T*D*D FLOP per layer-pass)
+    and the attention become two GEMMs of width H*n (3 * 12 = 36 at c2: 2 * 2*T*D*36) and a
+    group softmax. Same math, reassociated; built once per block from the cached prompt K/V
+    (fp32 einsum, bf16 GEMM operands, width padded to a multiple of 8 with zero columns)."""
+
+    def __init__(self, model: "ToyModel", lw, k: torch.Tensor, v: torch.Tensor):
+        D, H, dhp = model.config.model_dim, model.heads_pad, model.dh_pad
+        n = k.shape[0]
+        kk = k.float().reshape(n, H, dhp)
+        vv = v.float().reshape(n, H, dhp)
+        wqk = torch.einsum("dhe,jhe->dhj", lw.cq.float().reshape(D, H, dhp), kk).reshape(D, H * n)
+        wvo = torch.einsum("jhe,hed->hjd", vv, lw.co.float().reshape(H, dhp, D)).reshape(H * n, D)
+        self.n, self.groups, self.width = n, H, -(-(H * n) // 8) * 8
+        pad = self.width - H * n
+        self.wqk = torch.nn.functional.pad(wqk, (0, pad)).to(torch.bfloat16).contiguous()
+        self.wvo = torch.nn.functional.pad(wvo, (0, 0, 0, pad)).to(torch.bfloat16).contiguous()
+
+
+def _fold_cross(model: "ToyModel", cross):
+    """cross[l] = (k, v, row0, n) -> per-layer _CrossFold (None passes through)."""
+    if cross is None:
+        return None
+    return [_CrossFold(model, lw, k[r0:r0 + n], v[r0:r0 + n])
+            for lw, (k, v, r0, n) in zip(model.layers, cross)]
+
+
+def _cross_attend(ws, fold: _CrossFold, x: torch.Tensor, h: torch.Tensor, scale: float):
+    """x += softmax_per_head(h . wqk * scale) . wvo (the folded cross-attention)."""
+    T = h.shape[0]
+    key = (T, fold.width)
+    buf = ws.cross_bufs.get(key)
+    if buf is None:  # logits fp32 / probabilities bf16; padding columns of p stay zero
+        buf = ws.cross_bufs[key] = (torch.empty(T, fold.width, device=h.device),
+                                    torch.zeros(T, fold.width, device=h.device, dtype=torch.bfloat16))
+    s, p = buf
+    torch.mm(h, fold.wqk, out_dtype=torch.float32, out=s)
+    _abi.check(_abi.lib().ifx_group_softmax(s.data_ptr(), T, fold.groups, fold.n, fold.width,
+                                            float(scale), p.data_ptr(), fold.width,
+                                            torch.cuda.current_stream().cuda_stream), "group_softmax")
+    count_launch()
+    torch.addmm(x, p, fold.wvo, out_dtype=torch.float32, out=x)
+
+
 class _Workspace:
     """Per-(T, D) device buffers reused across passes (no allocator traffic in the loop)."""
 
@@ -311,11 +359,11 @@ class _Workspace:
         self.x = torch.empty(T, D, device=dev, dtype=torch.float32)
         self.h = torch.empty(T, D, device=dev, dtype=torch.bfloat16)
         self.qkv = torch.empty(T, 3 * Dp, device=dev, dtype=torch.bfloat16)
-        self.q2 = torch.empty(T, Dp, device=dev, dtype=torch.bfloat16)
         self.attn = torch.empty(T, Dp, device=dev, dtype=torch.bfloat16)
         self.ffn = torch.empty(T, 2 * D, device=dev, dtype=torch.bfloat16)
         self.tmp = torch.empty(T, D, device=dev, dtype=torch.float32)
         self.zero_bias = torch.zeros(2 * D, device=dev, dtype=torch.bfloat16)
+        self.cross_bufs = {}
 
 
 def _residual(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor, tmp: torch.Tensor = None):
@@ -346,7 +394,7 @@ class BlockRunner:
     def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
                 collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None,
                 rope=None):
-        """One pass. ctx: _KvContext of the block or None; cross[l] = (k, v, row0, n) or
+        """One pass. ctx: _KvContext of the block or None; cross: per-layer _CrossFold or
         None; rope = (cos, sin) tables of this block (rope_tables) or None."""
         m, ws = self.model, self.ws
         c = m.config
@@ -374,12 +422,9 @@ class BlockRunner:
                 e1.record()
                 ev.append((e0, e1))
             _residual(ws.x, ws.attn, lw.wo, ws.tmp)
-            if cross is not None:
-                xk, xv, row0, n = cross[li]
+            if cross is not None:  # folded through the prompt's few keys (_CrossFold)
                 rms_bf16(ws.x, ws.h)
-                torch.mm(ws.h, lw.cq, out=ws.q2)
-                attn_fwd(ws.q2, H, dhp, ws.attn, xk, xv, row0, n, scale=sc)
-                _residual(ws.x, ws.attn, lw.co, ws.tmp)
+                _cross_attend(ws, cross[li], ws.x, ws.h, sc)
             rms_bf16(ws.x, ws.h)
             _ffn_up(ws.h, lw.w1, ws.zero_bias, ws.ffn)
             _residual(ws.x, ws.ffn, lw.w2, ws.tmp)
@@ -404,6 +449,7 @@ class BlockRunner:
 
 
 PAGED_K1_PAGE_LENS = (8, 16, 32, 64, 128)  # page boxes that tile K1's 128-key tiles
+MAX_DMA_RUNS = 256  # staging of a layer with more slot runs goes through K6 instead
 
 
 class _Stager:
@@ -502,11 +548,18 @@ class _KvContext:
             return
         allm = torch.from_numpy(np.concatenate(pairs)).to(dev, non_blocking=True)
         self.moves = [None] * L
+        self.runs_h = [None] * L  # (staging slot, host slot, count) of consecutive host slots
         o = 0
         for li in self.jobs:
-            n = len(host_slots[li])
+            hs = host_slots[li]
+            n = len(hs)
             self.moves[li] = allm[o:o + n]
             o += n
+            cut = np.flatnonzero(np.diff(hs) != 1) + 1
+            starts = np.r_[0, cut]
+            if len(starts) <= MAX_DMA_RUNS:
+                counts = np.diff(np.r_[starts, n])
+                self.runs_h[li] = np.ascontiguousarray(np.stack([starts, hs[starts], counts], 1), np.int64)
         self.job_of = {li: i for i, li in enumerate(self.jobs)}
         H = len(self.jobs)
         self.R = max(len(host_slots[li]) for li in self.jobs)  # slots per buffer
@@ -547,9 +600,15 @@ class _KvContext:
         p.width, p.page_len = pool.width, pool.page_len
         p.type = _abi.BF16 if pool.dtype == torch.bfloat16 else _abi.F32
         m = self.moves[li]
-        _abi.check(_abi.lib().ifx_kv_move_pages(ctypes.byref(p), m.data_ptr(), m.shape[0], 1,
-                                               st.copy.cuda_stream), "stage")
-        count_launch()
+        runs = self.runs_h[li]
+        if runs is not None:  # DMA engines: runs while K1 occupies every SM
+            _abi.check(_abi.lib().ifx_kv_copy_runs(
+                ctypes.byref(p), runs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(runs), 1,
+                st.copy.cuda_stream), "stage")
+        else:  # many short runs: one gather kernel (K6)
+            _abi.check(_abi.lib().ifx_kv_move_pages(ctypes.byref(p), m.data_ptr(), m.shape[0], 1,
+                                                   st.copy.cuda_stream), "stage")
+            count_launch()
         st.staged_pages += m.shape[0]
         ev = torch.cuda.Event()
         ev.record(st.copy)
@@ -626,13 +685,13 @@ def _block_context(model: ToyModel, cache: KvCache | None, prompt_ctx, stager: _
     cross-attention, as ONE move batch (the LRU churn of a context larger than the device
     tier cancels out instead of moving every page twice), then K1's paged view."""
     if cache is None:
-        return None, _cross_from_cache(model, None, prompt_ctx)
+        return None, _fold_cross(model, _cross_from_cache(model, None, prompt_ctx))
     with cache.batch():
         ctx = _KvContext(model, cache, stager, passes)
         rngs = _touch_cross(model, cache)
     cross = _gather_cross(cache, rngs) if rngs is not None else _cross_from_cache(model, None, prompt_ctx)
     ctx.prepare()
-    return ctx, cross
+    return ctx, _fold_cross(model, cross)
 
 
 def _cross_from_cache(model: ToyModel, cache: KvCache | None, prompt_ctx):
@@ -674,7 +733,7 @@ def denoise_step(model: ToyModel, latent, t: float, step_scale: float, cache: Kv
         r.ws = _Workspace(lat.shape[0], c.model_dim, model.attn_width, r.dev)
     eps = torch.empty_like(lat)
     r.forward(lat, float(t), _ctx_from_cache(model, cache, getattr(r, "stager", None)),
-              _cross_from_cache(model, cache, prompt_ctx),
+              _fold_cross(model, _cross_from_cache(model, cache, prompt_ctx)),
               cache, eps_out=eps, rope=rope_tables(c, 0, lat.device) if lat.shape[0] == c.block_len
               else None)
     return lat.sub_(eps, alpha=float(step_scale))
@@ -712,8 +771,12 @@ def _prompt_for_chunk(schedule, chunk: int) -> str:
 
 def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSchedule, prompt_ctx,
                    chunk_index: int, seed: int, prompt_text: str = "", noise=None,
-                   to_host: bool = True) -> GeneratedBlock:
-    """engine.py:285-312 — denoise one block from seeded noise, append its clean K/V."""
+                   to_host: bool = True, _ready=None) -> GeneratedBlock:
+    """engine.py:285-312 — denoise one block from seeded noise, append its clean K/V.
+
+    `_ready` (internal, Engine.generate): a list that receives the copy-done event instead
+    of synchronising here, so the host can enqueue the next block while this one runs; the
+    block's numpy arrays are valid once that event completed."""
     schedule.validate()
     c = model.config
     if noise is None:
@@ -733,7 +796,12 @@ def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSche
     px_h = torch.empty(px.shape, dtype=torch.uint8, pin_memory=True)
     lat_h.copy_(lat, non_blocking=True)
     px_h.copy_(px, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    if _ready is None:
+        torch.cuda.current_stream().synchronize()
+    else:
+        ev = torch.cuda.Event()
+        ev.record()
+        _ready.append(ev)
     return GeneratedBlock(chunk_index, lat_h.numpy(), list(px_h.view(-1, h, w).numpy()), prompt_text)
 
 
@@ -790,6 +858,7 @@ class Engine:
         pool = ThreadPoolExecutor(1)
         nxt = pool.submit(make_noise, 0)
         blocks = []
+        pending = []  # copy-done events of blocks whose host arrays are still being filled
         current_prompt = None
         prof = self.profiler
         try:
@@ -813,18 +882,26 @@ class Engine:
                 if span:
                     span.__enter__()
                 torch.cuda.nvtx.range_push(f"block{chunk}")  # ncu --nvtx-include scoping
+                ready = [] if to_host else None
                 block = generate_block(self.model, self.cache, request.schedule, None, chunk,
                                        request.seed, prompt_text=prompt, noise=noise,
-                                       to_host=to_host)
+                                       to_host=to_host, _ready=ready)
+                if ready:
+                    pending.append(ready[0])
                 torch.cuda.nvtx.range_pop()
                 if span:
                     span.__exit__(None, None, None)
                 if request.kv_window is not None:
                     self.cache.evict_window(request.kv_window)
                 self.event_log.append(("block", chunk))
+                if sinks and pending:  # sinks see finished host arrays (engine.py:405-407)
+                    pending.pop().synchronize()
+                    pending.clear()
                 for sink in sinks:
                     sink(block)
                 blocks.append(block)
+            for ev in pending:  # without sinks, one wait at the end keeps the GPU fed
+                ev.synchronize()
         finally:
             pool.shutdown(wait=False)
         with self._lock:

@@ -380,10 +380,10 @@ class UlyssesRunner:
         self.qkv = torch.empty(n, 3 * Dp, device=dev, dtype=torch.bfloat16)
         self.attn_h = torch.empty(T, self.wl, device=dev, dtype=torch.bfloat16)
         self.attn_s = torch.empty(n, Dp, device=dev, dtype=torch.bfloat16)
-        self.q2 = torch.empty(n, Dp, device=dev, dtype=torch.bfloat16)
         self.ffn = torch.empty(n, 2 * D, device=dev, dtype=torch.bfloat16)
         self.eps = torch.empty(n, D, device=dev)
         self.zero_bias = torch.zeros(2 * D, device=dev, dtype=torch.bfloat16)
+        self.cross_bufs = {}
         self.attn_events = None
         from .engine import _Stager
         self.stager = _Stager(dev)
@@ -394,7 +394,7 @@ class UlyssesRunner:
 
     def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None,
                 rope=None):
-        from .engine import _ffn_up, _residual
+        from .engine import _cross_attend, _ffn_up, _residual
         from .kvcache import SELF_ATTN
         m = self.model
         c = m.config
@@ -424,11 +424,8 @@ class UlyssesRunner:
             self.comm.head_to_seq(self.attn_h, self.attn_s)      # [n, Dp]
             _residual(self.x, self.attn_s, lw.wo)
             if cross is not None:  # sequence-sharded vs replicated prompt K/V: no comm
-                xk, xv, row0, nx = cross[li]
                 self._rms(self.x, self.h)
-                torch.mm(self.h, lw.cq, out=self.q2)
-                self._attn(self.q2, m.heads_pad, dhp, self.attn_s, xk, xv, row0, nx, scale=sc)
-                _residual(self.x, self.attn_s, lw.co)
+                _cross_attend(self, cross[li], self.x, self.h, sc)
             self._rms(self.x, self.h)
             _ffn_up(self.h, lw.w1, self.zero_bias, self.ffn)
             _residual(self.x, self.ffn, lw.w2)

@@ -44,7 +44,8 @@ CASES = [
     (12, 128, 1000, 3, 5, 2),
     (4, 64, 600, 0, 0, 17),
     (40, 128, 300, 8, 1, 0),
-    (40, 128, 300, 32, 1, 0),  # K/V of 40 heads x 32 keys exceed K1s' smem: K1 instead
+    (40, 128, 300, 32, 1, 0),
+    (3, 128, 400, 33, 0, 0),   # 33 keys: K1 (K1s takes <= 32)
 ]
 
 
