@@ -433,6 +433,8 @@ def run_host_tier_bench(args, c, cfgname, local):
         "roofline": {"bound": "tensor", "achieved": flops / (attn_ms / 1e3) / 1e12, "peak": peak,
                      "unit": "TFLOP/s", "frac": flops / (attn_ms / 1e3) / 1e12 / peak,
                      "traffic": None, "peak_source": peak_src, "kernel": "K1 (paged)",
+                     "note": "event window includes each layer's wait for its host pages "
+                             "to be staged (PCIe-bound); see tools/attn_probe.py for K1 alone",
                      "kernel_ms_per_step": attn_ms, "share_of_step": attn_ms / ms},
         "host_tier": {"d2h_bytes_per_step": moved[0], "h2d_bytes_per_step": moved[1],
                       "staged_h2d_bytes_per_step": staged,
