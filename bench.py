@@ -458,7 +458,7 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
     mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
                        block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
                        weight_seed=0)
-    model = E.ToyModel(mc, weights="device", head_multiple=world)
+    model = E.ToyModel(mc, weights="device")  # heads % N != 0: balanced query split, no padding
     comm = UlyssesComm()
     nb = c["blocks"]
     kvc = E.default_kv_config(mc, capacity_pages_device=10**8, capacity_pages_host=4096)
@@ -509,7 +509,9 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (device-seeded noise, random-init weights)",
                 "config": {"workload": c["desc"], "parallelism": f"ulysses{world}",
-                           "heads_padded": model.heads_pad, "l2": "inputs larger than L2"},
+                           "head_split": "whole heads" if eng.runner.plan is None else
+                           f"balanced: {eng.runner.plan.hl} heads / {len(eng.runner.plan.segs)} "
+                           f"segments on rank 0", "l2": "inputs larger than L2"},
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak if achieved else None, "traffic": None,
                              "peak_source": peak_src, "scope": "rank 0's K1 launches"},

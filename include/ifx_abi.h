@@ -256,6 +256,13 @@ int ifx_ulysses_pack(const void* src, int64_t n, int64_t groups, int64_t world, 
 int ifx_ulysses_unpack(const void* src, int64_t n, int64_t groups, int64_t world, int64_t chunk,
                        int type, void* dst, int64_t dst_ld, void* stream);
 
+/* K5b — Ulysses re-shard when heads do not divide the ranks (balanced query split): copy
+ * n_blocks 2-D byte blocks from src to dst in one launch. desc = DEVICE int64 [n][6]:
+ * (src offset, src row stride, dst offset, dst row stride, rows, row bytes), all in bytes,
+ * row bytes a multiple of 16; max_rows = the largest block's row count. */
+int ifx_copy_blocks(const void* src, void* dst, const int64_t* desc, int64_t n_blocks,
+                    int64_t max_rows, void* stream);
+
 /* Initial block noise, host side (engine.py:280-282): writes the first n values of
  * np.random.default_rng([seed, chunk]).standard_normal(...).astype(float32) into `out`
  * (host memory, e.g. pinned), bit-identically, using `threads` host threads (0 = all).

@@ -335,6 +335,15 @@ int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec,
   return ifx::cuda_fail(e, "rms launch");
 }
 
+int ifx_copy_blocks(const void* src, void* dst, const int64_t* desc, int64_t n_blocks,
+                    int64_t max_rows, void* stream) {
+  if (n_blocks < 0 || max_rows < 0 || n_blocks > 65535) return ifx::fail(IFX_EDIM, "bad block copy");
+  if (n_blocks == 0 || max_rows == 0) return IFX_OK;
+  int e = ifx::copy_blocks_launch(src, dst, desc, n_blocks, max_rows,
+                                  static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "copy_blocks launch");
+}
+
 int ifx_group_softmax(const float* s, int64_t rows, int64_t groups, int64_t group_size,
                       int64_t ld, float scale, void* p, int64_t p_ld, void* stream) {
   if (rows < 0 || groups < 1 || group_size < 1 || ld < groups * group_size || p_ld < groups * group_size)

@@ -13,6 +13,8 @@ int kv_gather_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t wi
                      int64_t n, void* ko, void* vo, cudaStream_t st);
 int kv_move_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t width,
                    int64_t page_len, const int64_t* moves, int64_t n, int dir, cudaStream_t st);
+int copy_blocks_launch(const void* src, void* dst, const int64_t* desc, int64_t n_blocks,
+                       int64_t max_rows, cudaStream_t st);
 int group_softmax_launch(const float* s, int64_t rows, int groups, int gs, int64_t ld,
                          float scale_log2, void* p, int64_t p_ld, cudaStream_t st);
 int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, float t,

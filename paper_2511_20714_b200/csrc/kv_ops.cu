@@ -242,6 +242,22 @@ __global__ void rope_qk_kernel(__nv_bfloat16* __restrict__ qkv, int64_t rows, in
   }
 }
 
+// ---- gather / scatter of 2-D byte blocks between two buffers (Ulysses re-shard with
+// uneven head splits): desc[b] = (src offset, src row stride, dst offset, dst row stride,
+// rows, row bytes) in bytes, row bytes a multiple of 16. grid.x = block, grid.y = row chunk.
+__global__ void copy_blocks_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                   const int64_t* __restrict__ desc, int rows_per_cta) {
+  const int64_t* d = desc + 6 * blockIdx.x;
+  const int64_t rows = d[4];
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta;
+  if (r0 >= rows) return;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  const int64_t vecs = d[5] / 16;
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = r0 + (threadIdx.x >> 5); r < r1; r += blockDim.x >> 5)
+    copy_row<4>(src + d[0] + r * d[1], dst + d[2] + r * d[3], vecs, lane);
+}
+
 // ---- softmax over groups of a few logits (the folded cross-attention, engine.py:211-215):
 // p[r, g*gs + j] = bf16(softmax_j(s[r, g*gs + j] * scale)), one thread per (row, group)
 __global__ void group_softmax_kernel(const float* __restrict__ s, int64_t rows, int groups,
@@ -317,6 +333,15 @@ int kv_move_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t widt
   const int64_t units = n * 2 * ((page_vecs + piece - 1) / piece);
   move_pages<<<grid_for(units * 32, threads), threads, 0, st>>>(pool, moves, n, dir, page_vecs,
                                                                 piece);
+  return (int)cudaGetLastError();
+}
+
+int copy_blocks_launch(const void* src, void* dst, const int64_t* desc, int64_t n_blocks,
+                       int64_t max_rows, cudaStream_t st) {
+  const int rows_per_cta = 64;
+  dim3 grid((unsigned)n_blocks, (unsigned)((max_rows + rows_per_cta - 1) / rows_per_cta));
+  copy_blocks_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(src),
+                                           static_cast<uint8_t*>(dst), desc, rows_per_cta);
   return (int)cudaGetLastError();
 }
 

@@ -614,29 +614,38 @@ class _KvContext:
         ev.record(st.copy)
         self.staged[j] = ev
 
-    def attend(self, li: int, q, heads: int, dhp: int, out, cur_k, cur_v, scale: float, attn=None):
-        """K1 for layer li: q over [this layer's cached context ∥ the block's own K/V]."""
+    def attend(self, li: int, q, heads: int, dhp: int, out, cur_k, cur_v, scale: float, attn=None,
+               cols: tuple | None = None, first: bool = True, last: bool = True):
+        """K1 for layer li: q over [this layer's cached context ∥ the block's own K/V].
+
+        cols = (c0, c1): only these columns of the cached rows (one head of a Ulysses rank
+        whose query rows are split across ranks); a layer may then be attended in several
+        calls (first / last mark the first and last of them in this pass)."""
         attn = attn or attn_fwd
         self.prepare()
         lo, hi = self.ranges[li]
-        call = self.calls
-        self.calls += 1
+        if first:
+            self.calls += 1
+        call = self.calls - 1
+        sl = (lambda t: t) if cols is None else (lambda t: t[:, cols[0]:cols[1]])  # noqa: E731
         if hi <= lo:
             return attn(q, heads, dhp, out, cur_k=cur_k, cur_v=cur_v, scale=scale)
         if not self.paged:  # K7 gather of the context (host pages read over PCIe in place)
             k, v = self.cache._gather(li, SELF_ATTN, None, lo, hi - lo, lo, hi, raw=True)
-            return attn(q, heads, dhp, out, k, v, 0, hi - lo, cur_k, cur_v, scale=scale)
+            return attn(q, heads, dhp, out, sl(k), sl(v), 0, hi - lo, cur_k, cur_v, scale=scale)
         j = None
         if self.jobs and li in self.job_of:
             idx = self.job_of[li]
             j = idx if self.resident else (call // self.L) * len(self.jobs) + idx
-            torch.cuda.current_stream().wait_event(self.staged[j])
+            if first:
+                torch.cuda.current_stream().wait_event(self.staged[j])
         sk, sv = self._stage_views(self._buf(j)) if j is not None else (None, None)
         pool = self.pool
-        attn(q, heads, dhp, out, pool.dev_k, pool.dev_v, lo, hi - lo, cur_k, cur_v, scale=scale,
-             ctx_slots=self.tables[li], page_len=self.P, first_token=self.first[li],
-             stage_k=sk, stage_v=sv, tile_runs=self.runs[li])
-        if j is not None and not self.resident:
+        attn(q, heads, dhp, out, sl(pool.dev_k), sl(pool.dev_v), lo, hi - lo, cur_k, cur_v,
+             scale=scale, ctx_slots=self.tables[li], page_len=self.P, first_token=self.first[li],
+             stage_k=sl(sk) if sk is not None else None, stage_v=sl(sv) if sv is not None else None,
+             tile_runs=self.runs[li])
+        if j is not None and not self.resident and last:
             ev = torch.cuda.Event()
             ev.record()
             self.consumed[self._buf(j)] = ev

@@ -342,6 +342,18 @@ class UlyssesComm:
         self.bytes += send.numel() * send.element_size() * (w - 1) // w
         return recv
 
+    def a2a_var(self, send: torch.Tensor, send_sizes, recv: torch.Tensor, recv_sizes) -> torch.Tensor:
+        """All-to-all with per-peer sizes (elements), for the balanced re-shard."""
+        if send.is_cuda and self.dist.get_backend(self.group) != "nccl":
+            r = torch.empty(recv.shape, dtype=recv.dtype)
+            self.dist.all_to_all_single(r, send.cpu(), recv_sizes, send_sizes, group=self.group)
+            recv.copy_(r)
+        else:
+            self.dist.all_to_all_single(recv, send, recv_sizes, send_sizes, group=self.group)
+        self.messages += sum(1 for k, sz in enumerate(send_sizes) if sz and k != self.rank)
+        self.bytes += sum(sz for k, sz in enumerate(send_sizes) if k != self.rank) * send.element_size()
+        return recv
+
     def seq_to_head(self, x: torch.Tensor, groups: int) -> torch.Tensor:
         n = x.shape[0]
         chunk = x.shape[1] // (groups * self.world)
@@ -356,6 +368,120 @@ class UlyssesComm:
         return self._unpack(recv, out, 1, self.world, chunk)
 
 
+class BalancedPlan:
+    """Ulysses re-shard for heads that do not divide the ranks, without dummy heads.
+
+    The (head, query row) grid of a block, head-major, is cut into W equal ranges: rank k
+    attends segments (h, r0, r1) covering H*T/W query rows in total (e.g. 12 heads on 8
+    ranks: 1.5 heads each instead of 2 padded ones), holds K/V of the <= ceil(H/W)+1 heads
+    its segments touch (its KV-cache shard; a head split across two ranks is cached on
+    both), and activations stay sequence-sharded (rank i owns rows [i*n, (i+1)*n)).
+    Static per runner: the byte-block descriptors of the four copies around the two
+    all-to-alls (K5b `ifx_copy_blocks`) and the all-to-all split sizes."""
+
+    def __init__(self, heads: int, T: int, world: int, rank: int, dhp: int, dev):
+        if T % world or (heads * T) % world:
+            raise DimensionError("block_len must split evenly over the ranks")
+        n, per = T // world, heads * T // world
+        segs = []
+        for k in range(world):
+            g, g1, sk = k * per, (k + 1) * per, []
+            while g < g1:
+                h, r = divmod(g, T)
+                e = min(g1, (h + 1) * T)
+                sk.append((h, r, r + e - g))
+                g = e
+            segs.append(sk)
+        heads_of = [sorted({h for h, _, _ in sk}) for sk in segs]
+        self.n, self.T, self.world, self.rank, self.dhp = n, T, world, rank, dhp
+        self.segs, self.heads_of = segs[rank], heads_of[rank]
+        self.hl = len(self.heads_of)
+        Dp, eb = heads * dhp, 2  # bf16
+        rb = dhp * eb            # bytes of one head row
+
+        def qrows(seg, i):
+            _, r0, r1 = seg
+            a, b = max(r0, i * n), min(r1, (i + 1) * n)
+            return a, max(0, b - a)
+
+        # --- seq -> head: what this rank sends to k, and what it receives from i
+        pack, self.send_sizes, off = [], [], 0
+        for k in range(world):
+            start = off
+            for (h, r0, r1) in segs[k]:
+                a, m = qrows((h, r0, r1), rank)
+                if m:
+                    pack.append(((a - rank * n) * 3 * Dp * eb + h * rb, 3 * Dp * eb, off, rb, m, rb))
+                    off += m * rb
+            for which in (1, 2):  # K then V of k's heads, my n rows
+                for h in heads_of[k]:
+                    pack.append((which * Dp * eb + h * rb, 3 * Dp * eb, off, rb, n, rb))
+                    off += n * rb
+            self.send_sizes.append((off - start) // eb)
+        self.send_elems = off // eb
+        # receive layout: Q region [QR, dhp] (segments stacked), K / V regions [T, hl*dhp]
+        self.seg_base, qr = [], 0
+        for (h, r0, r1) in self.segs:
+            self.seg_base.append(qr)
+            qr += r1 - r0
+        self.qr = qr
+        kv_w = self.hl * rb
+        k_off, v_off = qr * rb, qr * rb + T * kv_w
+        self.region_bytes = v_off + T * kv_w
+        unpack, self.recv_sizes, off = [], [], 0
+        for i in range(world):
+            start = off
+            for si, seg in enumerate(self.segs):
+                a, m = qrows(seg, i)
+                if m:
+                    unpack.append((off, rb, (self.seg_base[si] + a - seg[1]) * rb, rb, m, rb))
+                    off += m * rb
+            for reg in (k_off, v_off):
+                for hi_, h in enumerate(self.heads_of):
+                    unpack.append((off, rb, reg + i * n * kv_w + hi_ * rb, kv_w, n, rb))
+                    off += n * rb
+            self.recv_sizes.append((off - start) // eb)
+        self.recv_elems = off // eb
+        self.k_off, self.v_off, self.kv_w = k_off, v_off, kv_w
+        # --- head -> seq: O rows of my segments back to their sequence owners
+        opack, self.o_send_sizes, off = [], [], 0
+        for i in range(world):
+            start = off
+            for si, seg in enumerate(self.segs):
+                a, m = qrows(seg, i)
+                if m:
+                    opack.append(((self.seg_base[si] + a - seg[1]) * rb, rb, off, rb, m, rb))
+                    off += m * rb
+            self.o_send_sizes.append((off - start) // eb)
+        self.o_send_elems = off // eb
+        ounpack, self.o_recv_sizes, off = [], [], 0
+        for k in range(world):
+            start = off
+            for (h, r0, r1) in segs[k]:
+                a, m = qrows((h, r0, r1), rank)
+                if m:
+                    ounpack.append((off, rb, (a - rank * n) * Dp * eb + h * rb, Dp * eb, m, rb))
+                    off += m * rb
+            self.o_recv_sizes.append((off - start) // eb)
+        self.o_recv_elems = off // eb
+
+        def dev_desc(d):
+            t = torch.tensor(d if d else [[0] * 6], dtype=torch.int64).to(dev)
+            return t, len(d), max((x[4] for x in d), default=0)
+
+        self.pack, self.unpack = dev_desc(pack), dev_desc(unpack)
+        self.opack, self.ounpack = dev_desc(opack), dev_desc(ounpack)
+
+
+def _copy_blocks(src: torch.Tensor, dst: torch.Tensor, desc) -> None:
+    from ._device import count_launch, stream_ptr
+    t, nb, max_rows = desc
+    if nb:
+        _abi.check(_abi.lib().ifx_copy_blocks(src.data_ptr(), dst.data_ptr(), t.data_ptr(), nb,
+                                              max_rows, stream_ptr()), "copy_blocks")
+        count_launch()
+
+
 class UlyssesRunner:
     """BlockRunner (engine.py) for one Ulysses rank: sequence-sharded activations,
     head-sharded attention over the rank-local KV shard (engine.py:185-221 semantics)."""
@@ -365,16 +491,29 @@ class UlyssesRunner:
         self.model, self.comm = model, comm
         c = model.config
         W = comm.world
-        if model.heads_pad % W:
-            raise DimensionError(f"heads {model.heads_pad} not divisible by world_size {W}")
         if c.block_len % W:
             raise DimensionError(f"block_len {c.block_len} not divisible by world_size {W}")
         self.n = c.block_len // W
-        self.hl = model.heads_pad // W
+        dev = model.time_vec.device
+        # heads divisible by the ranks: classic Ulysses (whole heads per rank, K5 pack);
+        # otherwise the balanced plan (query rows of a head split across ranks)
+        self.plan = None
+        if model.heads_pad % W:
+            self.plan = BalancedPlan(model.heads_pad, c.block_len, W, comm.rank, model.dh_pad, dev)
+            self.hl = self.plan.hl
+        else:
+            self.hl = model.heads_pad // W
         self.wl = self.hl * model.dh_pad
         self._attn = attn or attn_fwd
-        dev = model.time_vec.device
         D, Dp, n, T = c.model_dim, model.attn_width, self.n, c.block_len
+        if self.plan is not None:
+            pl = self.plan
+            self.b_send = torch.empty(pl.send_elems, device=dev, dtype=torch.bfloat16)
+            self.b_recv = torch.empty(pl.recv_elems, device=dev, dtype=torch.bfloat16)
+            self.b_region = torch.empty(pl.region_bytes // 2, device=dev, dtype=torch.bfloat16)
+            self.b_o = torch.empty(pl.qr, model.dh_pad, device=dev, dtype=torch.bfloat16)
+            self.b_osend = torch.empty(max(1, pl.o_send_elems), device=dev, dtype=torch.bfloat16)
+            self.b_orecv = torch.empty(max(1, pl.o_recv_elems), device=dev, dtype=torch.bfloat16)
         self.x = torch.empty(n, D, device=dev)
         self.h = torch.empty(n, D, device=dev, dtype=torch.bfloat16)
         self.qkv = torch.empty(n, 3 * Dp, device=dev, dtype=torch.bfloat16)
@@ -387,6 +526,37 @@ class UlyssesRunner:
         self.attn_events = None
         from .engine import _Stager
         self.stager = _Stager(dev)
+
+    def _balanced_attention(self, li, ctx, sc, ev):
+        """BalancedPlan: re-shard (one all-to-all), one K1 per segment (a head's query rows,
+        that head's cached columns and own K/V), re-shard back. Returns this rank's K / V
+        [T, hl*dhp] (the page write of the clean pass)."""
+        pl, dhp = self.plan, self.model.dh_pad
+        _copy_blocks(self.qkv, self.b_send, pl.pack)
+        self.comm.a2a_var(self.b_send, pl.send_sizes, self.b_recv, pl.recv_sizes)
+        _copy_blocks(self.b_recv, self.b_region, pl.unpack)
+        T = pl.T
+        kv = self.b_region[pl.k_off // 2:].view(-1)[:2 * T * self.wl].view(2, T, self.wl)
+        kc, vc = kv[0], kv[1]
+        qreg = self.b_region[:pl.qr * dhp].view(pl.qr, dhp)
+        if ev is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        last = len(pl.segs) - 1
+        for si, (h, r0, r1) in enumerate(pl.segs):
+            hi_ = pl.heads_of.index(h)
+            b, m = pl.seg_base[si], r1 - r0
+            c0, c1 = hi_ * dhp, (hi_ + 1) * dhp
+            ctx.attend(li, qreg[b:b + m], 1, dhp, self.b_o[b:b + m], kc[:, c0:c1], vc[:, c0:c1], sc,
+                       attn=self._attn, cols=(c0, c1), first=si == 0, last=si == last)
+        if ev is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            ev.append((e0, e1))
+        _copy_blocks(self.b_o, self.b_osend, pl.opack)
+        self.comm.a2a_var(self.b_osend, pl.o_send_sizes, self.b_orecv, pl.o_recv_sizes)
+        _copy_blocks(self.b_orecv, self.attn_s, pl.ounpack)
+        return kc, vc
 
     def _rms(self, x, out, tvec=None, t=0.0, x_out=None):
         from ._device import rms_bf16
@@ -410,18 +580,21 @@ class UlyssesRunner:
                 from ._device import rope_qk
                 rope_qk(self.qkv, m.heads_pad, dhp, c.head_dim // 2, 0, m.attn_width, rope[0],
                         rope[1], tab_row0=self.comm.rank * self.n)
-            qkv_h = self.comm.seq_to_head(self.qkv, 3)          # [T, 3*wl] local heads
-            q, kc, vc = qkv_h[:, :wl], qkv_h[:, wl:2 * wl], qkv_h[:, 2 * wl:]
             ev = self.attn_events
-            if ev is not None:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-            ctx.attend(li, q, self.hl, dhp, self.attn_h, kc, vc, sc, attn=self._attn)
-            if ev is not None:
-                e1 = torch.cuda.Event(enable_timing=True)
-                e1.record()
-                ev.append((e0, e1))
-            self.comm.head_to_seq(self.attn_h, self.attn_s)      # [n, Dp]
+            if self.plan is None:
+                qkv_h = self.comm.seq_to_head(self.qkv, 3)          # [T, 3*wl] local heads
+                q, kc, vc = qkv_h[:, :wl], qkv_h[:, wl:2 * wl], qkv_h[:, 2 * wl:]
+                if ev is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                ctx.attend(li, q, self.hl, dhp, self.attn_h, kc, vc, sc, attn=self._attn)
+                if ev is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record()
+                    ev.append((e0, e1))
+                self.comm.head_to_seq(self.attn_h, self.attn_s)      # [n, Dp]
+            else:
+                kc, vc = self._balanced_attention(li, ctx, sc, ev)
             _residual(self.x, self.attn_s, lw.wo)
             if cross is not None:  # sequence-sharded vs replicated prompt K/V: no comm
                 self._rms(self.x, self.h)

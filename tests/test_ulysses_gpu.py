@@ -64,7 +64,7 @@ CFG = dict(layers=2, heads=4, head_dim=64, block_len=256, frame_shape=(8, 8), pr
 REQ = dict(num_blocks=3, seed=0, prompt_schedule=[(0, "a quiet scene"), (2, "rain")])
 
 
-def _rank(rank, world, port, q, cfg=None, kvc=None):
+def _rank(rank, world, port, q, cfg=None, kvc=None, pad=True):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -73,7 +73,7 @@ def _rank(rank, world, port, q, cfg=None, kvc=None):
         from paper_2511_20714_b200 import engine as E
         from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
 
-        model = E.ToyModel(E.ModelConfig(**(cfg or CFG)), head_multiple=world)
+        model = E.ToyModel(E.ModelConfig(**(cfg or CFG)), head_multiple=world if pad else 1)
         eng = UlyssesEngine(model, UlyssesComm(), E.KvConfig(**kvc) if kvc else None)
         lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
         q.put((rank, [l.cpu().numpy() for l in lats], eng.cache.state(), eng.comm.bytes))
@@ -90,8 +90,11 @@ KV_SPILL = dict(num_layers=2, head_dim=256, page_len=16, capacity_pages_device=4
                 capacity_pages_host=10**4)
 
 
-@pytest.mark.parametrize("world,cfg,kvc", [(2, CFG, None), (2, CFG_ROPE, None), (2, CFG, KV_SPILL)])
-def test_ulysses_engine_matches_single_gpu(world, cfg, kvc):
+@pytest.mark.parametrize("world,cfg,kvc,pad", [(2, CFG, None, True), (2, CFG_ROPE, None, True),
+                                              (2, CFG, KV_SPILL, True),
+                                              (2, CFG_ROPE, None, False),  # balanced: 1.5 heads/rank
+                                              (2, dict(CFG, heads=3), dict(KV_SPILL, head_dim=192), False)])
+def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad):
     from paper_2511_20714_b200 import engine as E
 
     ref_model = E.build_model(E.ModelConfig(**cfg))
@@ -100,7 +103,7 @@ def test_ulysses_engine_matches_single_gpu(world, cfg, kvc):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, q, cfg, kvc)) for r in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, cfg, kvc, pad)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
