@@ -33,7 +33,8 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._device import attn_fwd, count_launch, require_cuda, rms_bf16, rope_qk, tile_run_codes
+from ._device import (attn_fwd, count_launch, require_cuda, rms_bf16, rope_qk, stream_ptr,
+                      tile_run_codes)
 from .errors import ConfigError, DimensionError
 from .kvcache import CROSS_ATTN, SELF_ATTN, KvCache, KvConfig
 
@@ -347,7 +348,7 @@ def _cross_attend(ws, fold: _CrossFold, x: torch.Tensor, h: torch.Tensor, scale:
     torch.mm(h, fold.wqk, out_dtype=torch.float32, out=s)
     _abi.check(_abi.lib().ifx_group_softmax(s.data_ptr(), T, fold.groups, fold.n, fold.width,
                                             float(scale), p.data_ptr(), fold.width,
-                                            torch.cuda.current_stream().cuda_stream), "group_softmax")
+                                            stream_ptr()), "group_softmax")
     count_launch()
     torch.addmm(x, p, fold.wvo, out_dtype=torch.float32, out=x)
 
@@ -403,7 +404,10 @@ class BlockRunner:
         q, kc, vc = ws.qkv[:, :Dp], ws.qkv[:, Dp:2 * Dp], ws.qkv[:, 2 * Dp:]
         for li, lw in enumerate(m.layers):
             if li == 0:  # x = latent + t*time_vec fused into the first norm (engine.py:199)
-                rms_bf16(latent, ws.h, m.time_vec, t, x_out=ws.x)
+                if isinstance(t, torch.Tensor):  # t*time_vec precomputed on device (graphs)
+                    rms_bf16(latent, ws.h, t, 1.0, x_out=ws.x)
+                else:
+                    rms_bf16(latent, ws.h, m.time_vec, t, x_out=ws.x)
             else:
                 rms_bf16(ws.x, ws.h)
             torch.mm(ws.h, lw.wqkv, out=ws.qkv)
@@ -440,12 +444,54 @@ class BlockRunner:
         eps = self.ws.tmp.new_empty(self.ws.tmp.shape) if not hasattr(self, "_eps") else self._eps
         self._eps = eps
         rope = rope_tables(self.model.config, chunk_index, self.dev)
-        for t in schedule.steps:
-            self.forward(latent, float(t), ctx, cross, cache, eps_out=eps, rope=rope)
-            latent.add_(eps, alpha=-float(schedule.step_scale))
+        _euler_steps(self, latent, schedule, ctx, cross, cache, eps, rope)
         self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
                      chunk_index=chunk_index, rope=rope)
         return latent
+
+
+GRAPHS = os.environ.get("IFX_CUDA_GRAPHS", "1") != "0"
+
+
+def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, eps, rope,
+                 graphs_ok: bool = True) -> None:
+    """The S denoise passes of a block (engine.py:299-301). Within a block every pass
+    launches the same kernels on the same buffers with the same context, only t differs:
+    the first pass is captured once as a CUDA graph (t*time_vec read from a device buffer)
+    and replayed S times, so the host enqueues one pass per block instead of S (what keeps
+    a Ulysses rank, whose GPU share of a pass shrinks with the world size, GPU-bound).
+    Eager when capture is off (IFX_CUDA_GRAPHS=0), when K1 launches are being timed
+    (attn_events), or when host-tier pages are staged on the side stream."""
+    steps = [float(t) for t in schedule.steps]
+    m = runner.model
+    use = (GRAPHS and graphs_ok and len(steps) > 1 and runner.attn_events is None
+           and (ctx is None or not getattr(ctx, "jobs", None)))
+    if not use:
+        for t in steps:
+            runner.forward(latent, t, ctx, cross, cache, eps_out=eps, rope=rope)
+            latent.add_(eps, alpha=-float(schedule.step_scale))
+        return
+    if getattr(runner, "_tv", None) is None:
+        runner._tv = torch.empty_like(m.time_vec)
+        runner._gpool = torch.cuda.graph_pool_handle()
+        runner._cap = torch.cuda.Stream(latent.device)
+    tv, cap = runner._tv, runner._cap
+    if ctx is not None:
+        ctx.prepare()
+    g = torch.cuda.CUDAGraph()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap):  # capture without torch.cuda.graph's device-wide sync
+        g.capture_begin(pool=runner._gpool, capture_error_mode="thread_local")
+        try:
+            runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
+            latent.add_(eps, alpha=-float(schedule.step_scale))
+        finally:
+            g.capture_end()
+    torch.cuda.current_stream().wait_stream(cap)
+    for t in steps:
+        torch.mul(m.time_vec, t, out=tv)
+        g.replay()
+    runner._graph = g  # kept until the next block (its kernels may still be running)
 
 
 PAGED_K1_PAGE_LENS = (8, 16, 32, 64, 128)  # page boxes that tile K1's 128-key tiles

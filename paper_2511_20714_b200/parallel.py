@@ -572,7 +572,10 @@ class UlyssesRunner:
         sc = 1.0 / math.sqrt(c.head_dim)
         for li, lw in enumerate(m.layers):
             if li == 0:
-                self._rms(latent, self.h, m.time_vec, t, self.x)
+                if isinstance(t, torch.Tensor):  # t*time_vec on device (graph replays)
+                    self._rms(latent, self.h, t, 1.0, self.x)
+                else:
+                    self._rms(latent, self.h, m.time_vec, t, self.x)
             else:
                 self._rms(self.x, self.h)
             torch.mm(self.h, lw.wqkv, out=self.qkv)
@@ -609,14 +612,19 @@ class UlyssesRunner:
             torch.mm(self.h, m.w_out, out_dtype=torch.float32, out=eps_out)
 
     def denoise(self, latent, schedule, ctx, cross, cache, chunk_index):
-        from .engine import rope_tables
+        from .engine import _euler_steps, rope_tables
         rope = rope_tables(self.model.config, chunk_index, latent.device)
-        for t in schedule.steps:
-            self.forward(latent, float(t), ctx, cross, cache, eps_out=self.eps, rope=rope)
-            latent.add_(self.eps, alpha=-float(schedule.step_scale))
+        # graph capture needs the all-to-alls on the GPU stream: NCCL only (a gloo group
+        # stages them through the host)
+        nccl = self.comm.dist.get_backend(self.comm.group) == "nccl"
+        _euler_steps(self, latent, schedule, ctx, cross, cache, self.eps, rope, graphs_ok=nccl)
         self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
                      chunk_index=chunk_index, rope=rope)
         return latent
+
+    def release_graphs(self) -> None:
+        """Free the captured pass graph (before destroying the NCCL process group)."""
+        self._graph = None
 
 
 class UlyssesEngine:

@@ -450,3 +450,23 @@ def test_host_tier_data_random_ops_vs_oracle():
                     assert c.evict_window(keep) == o.evict_window(keep)
             finally:
                 assert c.state() == o.state(), seed
+
+
+def test_graph_replayed_passes_equal_eager():
+    """The denoise passes captured as one CUDA graph per block and replayed (t*time_vec
+    from a device buffer) produce bit-identical latents and page tables to eager passes."""
+    from paper_2511_20714_b200 import engine as E
+
+    kw = dict(layers=2, heads=4, head_dim=64, block_len=256, frame_shape=(8, 8), prompt_dim=8)
+    req = E.GenerationRequest(3, E.DenoiseSchedule([1.0, 0.75, 0.5, 0.25]), 0,
+                              [(0, "a b"), (2, "c")])
+    out = {}
+    for graphs in (True, False):
+        E.GRAPHS = graphs
+        try:
+            eng = E.Engine(E.build_model(E.ModelConfig(**kw)))
+            out[graphs] = (np.stack([b.latent for b in eng.generate(req)]), eng.cache.state())
+        finally:
+            E.GRAPHS = True
+    assert np.array_equal(out[True][0], out[False][0])
+    assert out[True][1] == out[False][1]
