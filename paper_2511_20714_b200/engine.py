@@ -461,23 +461,26 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     and replayed S times, so the host enqueues one pass per block instead of S (what keeps
     a Ulysses rank, whose GPU share of a pass shrinks with the world size, GPU-bound).
     Eager when capture is off (IFX_CUDA_GRAPHS=0), when K1 launches are being timed
-    (attn_events), or when host-tier pages are staged on the side stream."""
+    (attn_events), when host-tier pages are staged on the side stream, or when the page
+    length forces the K7-gather path; both modes compute t*time_vec the same way, so they
+    are bit-identical."""
     steps = [float(t) for t in schedule.steps]
     m = runner.model
-    use = (GRAPHS and graphs_ok and len(steps) > 1 and runner.attn_events is None
-           and (ctx is None or not getattr(ctx, "jobs", None)))
-    if not use:
-        for t in steps:
-            runner.forward(latent, t, ctx, cross, cache, eps_out=eps, rope=rope)
-            latent.add_(eps, alpha=-float(schedule.step_scale))
-        return
     if getattr(runner, "_tv", None) is None:
-        runner._tv = torch.empty_like(m.time_vec)
+        runner._tv = torch.empty_like(m.time_vec)  # t*time_vec of the pass (both modes)
         runner._gpool = torch.cuda.graph_pool_handle()
         runner._cap = torch.cuda.Stream(latent.device)
     tv, cap = runner._tv, runner._cap
     if ctx is not None:
         ctx.prepare()
+    use = (GRAPHS and graphs_ok and len(steps) > 1 and runner.attn_events is None
+           and (ctx is None or (ctx.paged and not ctx.jobs)))
+    if not use:
+        for t in steps:
+            torch.mul(m.time_vec, t, out=tv)
+            runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
+            latent.add_(eps, alpha=-float(schedule.step_scale))
+        return
     g = torch.cuda.CUDAGraph()
     cap.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(cap):  # capture without torch.cuda.graph's device-wide sync

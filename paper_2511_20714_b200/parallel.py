@@ -326,7 +326,10 @@ class UlyssesComm:
         self._pack = pack or _pack_cuda
         self._unpack = unpack or _unpack_cuda
         self.messages = 0
-        self.bytes = 0
+        self.bytes = 0  # counted at enqueue: a pass captured in a CUDA graph counts once
+        if dist.get_backend(group) == "nccl":  # communicator up before any graph capture
+            t = torch.zeros(self.world, device="cuda")
+            dist.all_to_all_single(torch.empty_like(t), t, group=group)
 
     def _a2a(self, send: torch.Tensor) -> torch.Tensor:
         recv = torch.empty_like(send)
