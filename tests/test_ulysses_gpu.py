@@ -118,3 +118,41 @@ def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad):
         assert nbytes > 0
     if kvc:
         assert ref_eng.cache.memory_stats().host_pages_used > 0
+
+
+def _rank_nccl(port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2511_20714_b200 import engine as E
+        from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
+
+        eng = UlyssesEngine(E.ToyModel(E.ModelConfig(**CFG)), UlyssesComm())
+        lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
+        q.put(([l.cpu().numpy() for l in lats], eng.cache.state(), eng.runner._graph is not None))
+        eng.runner.release_graphs()
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ulysses_nccl_graph_capture_world1():
+    """The NCCL path of the Ulysses runner on one GPU: its denoise passes are captured as
+    CUDA graphs with the all-to-alls inside (world size 1 exercises ProcessGroupNCCL under
+    stream capture), and match the single-GPU engine."""
+    from paper_2511_20714_b200 import engine as E
+
+    ref_eng = E.Engine(E.build_model(E.ModelConfig(**CFG)))
+    ref = ref_eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_rank_nccl, args=(_free_port(), q))
+    p.start()
+    lats, state, graphed = q.get(timeout=300)
+    p.join(timeout=120)
+    assert p.exitcode == 0 and graphed
+    for a, b in zip(lats, ref):
+        assert np.abs(a - b.latent).max() <= 2e-2
+    assert state == ref_eng.cache.state()
