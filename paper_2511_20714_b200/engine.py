@@ -391,6 +391,8 @@ class BlockRunner:
         self.ws = _Workspace(c.block_len, c.model_dim, model.attn_width, self.dev)
         self.attn_events = None
         self.stager = _Stager(self.dev)
+        self._eps = None
+        self._tv = self._gpool = self._cap = self._graph = None  # CUDA-graph state (_euler_steps)
 
     def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
                 collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None,
@@ -441,8 +443,9 @@ class BlockRunner:
     def denoise(self, latent: torch.Tensor, schedule: DenoiseSchedule, ctx, cross,
                 cache: KvCache | None, chunk_index: int) -> torch.Tensor:
         """engine.py:296-306: S Euler steps in place on `latent`, then the clean K/V pass."""
-        eps = self.ws.tmp.new_empty(self.ws.tmp.shape) if not hasattr(self, "_eps") else self._eps
-        self._eps = eps
+        if self._eps is None:
+            self._eps = self.ws.tmp.new_empty(self.ws.tmp.shape)
+        eps = self._eps
         rope = rope_tables(self.model.config, chunk_index, self.dev)
         _euler_steps(self, latent, schedule, ctx, cross, cache, eps, rope)
         self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
@@ -466,7 +469,7 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     are bit-identical."""
     steps = [float(t) for t in schedule.steps]
     m = runner.model
-    if getattr(runner, "_tv", None) is None:
+    if runner._tv is None:
         runner._tv = torch.empty_like(m.time_vec)  # t*time_vec of the pass (both modes)
         runner._gpool = torch.cuda.graph_pool_handle()
         runner._cap = torch.cuda.Stream(latent.device)

@@ -351,6 +351,7 @@ class KvCache:
         self._pools = {SELF_ATTN: _Pool(w, dtype, config.page_len, cd, ch),
                        CROSS_ATTN: _Pool(wc, dtype, config.page_len, cd, ch)}
         self.moved_pages = [0, 0]  # pages copied device->host, host->device (tier moves)
+        self._batch = 0  # depth of open batch() contexts
         if reserve_tokens:
             per_layer = -(-reserve_tokens // config.page_len) + 1
             self._pools[SELF_ATTN].ensure(min(config.capacity_pages_device,
@@ -414,7 +415,7 @@ class KvCache:
         whole context this way, then builds K1's slot tables)."""
         with self._lock:
             self._pt.batch_begin()
-            self._batch = getattr(self, "_batch", 0) + 1
+            self._batch += 1
             try:
                 yield self
             finally:
@@ -430,7 +431,7 @@ class KvCache:
         fresh one. Bounds the host footprint of a fetch whose tiers change a lot (e.g. the
         first fetch after a long prefill) without splitting the steady-state fetch, whose
         mid-fetch demotions of later layers are all undone."""
-        if not getattr(self, "_batch", 0):
+        if not self._batch:
             return
         _, _, lazy = self._pt.pending(fetched_layer)
         ext = self._pt.pool_extent()
@@ -448,7 +449,7 @@ class KvCache:
                 self._pt.batch_begin()
 
     def _no_batch(self, what: str) -> None:
-        if getattr(self, "_batch", 0):
+        if self._batch:
             raise RuntimeError(f"{what} inside KvCache.batch(): page data is only consistent "
                                f"after the batch's moves ran")
 
@@ -524,7 +525,7 @@ class KvCache:
             try:
                 self._pt.touch_range(layer, kind, a, b)
             finally:
-                if not getattr(self, "_batch", 0):
+                if not self._batch:
                     self._sync(stream)
 
     def _gather(self, layer, kind, tokens: torch.Tensor | None, first: int, n: int, lo: int, hi: int,

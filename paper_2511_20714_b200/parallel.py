@@ -529,6 +529,7 @@ class UlyssesRunner:
         self.attn_events = None
         from .engine import _Stager
         self.stager = _Stager(dev)
+        self._tv = self._gpool = self._cap = self._graph = None  # CUDA-graph state (_euler_steps)
 
     def _balanced_attention(self, li, ctx, sc, ev):
         """BalancedPlan: re-shard (one all-to-all), one K1 per segment (a head's query rows,
