@@ -22,7 +22,8 @@ from .errors import (
     OutOfRangeError,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libinferix_b200.so")
+LIB_PATH = os.environ.get("IFX_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libinferix_b200.so")  # override: A/B builds
 
 OK, EDIM, EMASK, ECAPACITY, ERANGE, ECONFIG, ECUDA, EUNSUPPORTED = 0, 1, 2, 3, 4, 5, 16, 17
 SELF_ATTN, CROSS_ATTN = 0, 1

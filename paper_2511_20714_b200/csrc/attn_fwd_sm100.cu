@@ -17,7 +17,7 @@
 //               online softmax over them (own running max / denominator, own accumulator
 //               O_h), so the two warps of a sub-partition never synchronise per tile and
 //               overlap freely (one in TMEM loads while the other is on MUFU/FMA). 64
-//               exponentials per warp per tile, 3 pairs in 8 as a cubic on the FMA pipe,
+//               exponentials per warp per tile, 2 pairs in 8 as a cubic on the FMA pipe,
 //               FFMA2/FADD2 packed math; P (bf16) overwrites the S columns it came from;
 //               lazy O rescale (only when the running max grows by > 2^8). The epilogue
 //               merges (O_0, m_0, l_0) and (O_1, m_1, l_1) (attention.py:157-180) and each
@@ -51,7 +51,7 @@ constexpr int NTHREADS = 320;    // 10 warps
 constexpr int NSOFT = 256;       // softmax threads
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if max grows > 2^8
 #ifndef IFX_POLY_PAIRS_OF_8
-#define IFX_POLY_PAIRS_OF_8 3  // measured best of 2, 3, 4 (profiles/r02_attn_variants.md)
+#define IFX_POLY_PAIRS_OF_8 2  // r03 power-capped bench: 1-2 beat 3 (profiles/r03_attn_poly.md)
 #endif
 // exp2 pairs (out of every 8 pairs) evaluated as a cubic on the FMA pipe instead of MUFU
 constexpr int kPolyPairsOf8 = IFX_POLY_PAIRS_OF_8;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const float2 x = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), sl2v, negm);
           float2 p;
           if ((i & 7) >= 8 - kPolyPairsOf8) {
-            p = ex2_poly2(x);  // 1 pair in 4 = 25% of the exponentials on the FMA pipe
+            p = ex2_poly2(x);  // kPolyPairsOf8 of every 8 pairs on the FMA pipe
           } else {
             p.x = ex2(x.x);
             p.y = ex2(x.y);
