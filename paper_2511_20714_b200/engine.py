@@ -486,13 +486,25 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
         return
     g = torch.cuda.CUDAGraph()
     cap.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(cap):  # capture without torch.cuda.graph's device-wide sync
-        g.capture_begin(pool=runner._gpool, capture_error_mode="thread_local")
-        try:
+    try:
+        with torch.cuda.stream(cap):  # capture without torch.cuda.graph's device-wide sync
+            g.capture_begin(pool=runner._gpool, capture_error_mode="thread_local")
+            try:
+                runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
+                latent.add_(eps, alpha=-float(schedule.step_scale))
+            finally:
+                g.capture_end()
+    except RuntimeError as err:  # capture refused (driver / library): run eagerly from now on
+        global GRAPHS
+        GRAPHS = False
+        import warnings
+        warnings.warn(f"CUDA graph capture failed ({err}); denoise passes run eagerly")
+        torch.cuda.current_stream().wait_stream(cap)
+        for t in steps:  # nothing ran during the failed capture
+            torch.mul(m.time_vec, t, out=tv)
             runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
             latent.add_(eps, alpha=-float(schedule.step_scale))
-        finally:
-            g.capture_end()
+        return
     torch.cuda.current_stream().wait_stream(cap)
     for t in steps:
         torch.mul(m.time_vec, t, out=tv)
