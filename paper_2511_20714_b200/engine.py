@@ -495,8 +495,7 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
             finally:
                 g.capture_end()
     except RuntimeError as err:  # capture refused (driver / library): run eagerly from now on
-        global GRAPHS
-        GRAPHS = False
+        globals()["GRAPHS"] = False
         import warnings
         warnings.warn(f"CUDA graph capture failed ({err}); denoise passes run eagerly")
         torch.cuda.current_stream().wait_stream(cap)
