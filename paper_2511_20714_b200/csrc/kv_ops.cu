@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kv_kernels.h"
 
@@ -107,6 +108,81 @@ __global__ void append_f32_bf16(const float* __restrict__ ks, const float* __res
       st_na(drow + c * 16, o);
     }
   }
+}
+
+// K2 (same type, TMA bulk): each warp streams rows through a 2-deep shared-memory ring with
+// the bulk-copy engine — cp.async.bulk global->shared completing on an mbarrier, then
+// cp.async.bulk shared->global into the page slot — so a row costs a handful of
+// instructions and the copy engine, not registers, keeps the bytes in flight. Rows whose
+// page is on the host tier are written by the warp's lanes from shared memory instead.
+constexpr int kBulkMaxRowBytes = 12288;  // 2 buffers x 8 warps fit 192 KB of smem
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(256) append_bulk(const uint8_t* __restrict__ ks,
+                                                   const uint8_t* __restrict__ vs,
+                                                   int64_t src_ld_b, PoolPtrs pool,
+                                                   const int32_t* __restrict__ slots, int64_t rel0,
+                                                   int64_t t, int row_b) {
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  __shared__ __align__(8) uint64_t bars[8][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* buf[2] = {bulk_smem + (warp * 2) * row_b, bulk_smem + (warp * 2 + 1) * row_b};
+  if (lane == 0) {
+    for (int i = 0; i < 2; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[warp][i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t u0 = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
+  auto src_of = [&](int64_t u) {
+    const bool is_v = u >= t;
+    return (is_v ? vs : ks) + (is_v ? u - t : u) * src_ld_b;
+  };
+  auto issue_load = [&](int64_t u, int k) {
+    const uint32_t bar = smem_addr(&bars[warp][k]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_b) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(buf[k])), "l"(src_of(u)), "r"(row_b), "r"(bar) : "memory");
+  };
+  uint32_t phase[2] = {0, 0};
+  if (lane == 0 && u0 < 2 * t) issue_load(u0, 0);
+  int k = 0;
+  for (int64_t u = u0; u < 2 * t; u += n_warps, k ^= 1) {
+    const int64_t un = u + n_warps;
+    if (lane == 0 && un < 2 * t) {
+      // the other buffer is free once its previous bulk store finished reading it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue_load(un, k ^ 1);
+    }
+    // wait for this row's bytes
+    const uint32_t bar = smem_addr(&bars[warp][k]);
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+                   "selp.b32 %0, 1, 0, P;\n\t}" : "=r"(ok) : "r"(bar), "r"(phase[k]) : "memory");
+    phase[k] ^= 1;
+    const bool is_v = u >= t;
+    const int64_t rel = rel0 + (is_v ? u - t : u);
+    const int pg = (int)(rel / pool.page_len);
+    const int32_t code = __ldg(slots + pg);
+    uint8_t* d = pool_row(pool, is_v, code, (int)(rel - (int64_t)pg * pool.page_len));
+    if (code >= 0) {
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(d), "r"(smem_addr(buf[k])), "r"(row_b) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else {  // host tier (mapped pinned memory): the lanes write it
+      for (int c = lane; c < row_b / 16; c += 32)
+        reinterpret_cast<uint4*>(d)[c] = reinterpret_cast<const uint4*>(buf[k])[c];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // K7: out[i] = pool row of token tokens[i] (tokens == NULL: token0 + i), K and V; tokens
@@ -304,6 +380,22 @@ int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf1
     append_f32_bf16<<<grid_for(2 * t * 32, threads), threads, 0, st>>>(
         static_cast<const float*>(ks), static_cast<const float*>(vs), src_ld, pool, slots, rel0, t,
         width / 8);
+  } else if ((width * (pool_bf16 ? 2 : 4)) <= kBulkMaxRowBytes && !std::getenv("IFX_K2_SIMT")) {
+    const int row_b = (int)(width * (pool_bf16 ? 2 : 4));
+    const size_t smem = (size_t)16 * row_b;  // 8 warps x 2 buffers
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(append_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           16 * kBulkMaxRowBytes);
+      attr = true;
+    }
+    int blocks = (int)((2 * t + 7) / 8);
+    const int cap = kSMs * (row_b <= 4096 ? 4 : 1);
+    if (blocks > cap) blocks = cap;
+    append_bulk<<<blocks, threads, smem, st>>>(static_cast<const uint8_t*>(ks),
+                                               static_cast<const uint8_t*>(vs),
+                                               src_ld * (pool_bf16 ? 2 : 4), pool, slots, rel0, t,
+                                               row_b);
   } else {
     const int esz = pool_bf16 ? 2 : 4;
     append_same<<<grid_for(2 * t * 32, threads), threads, 0, st>>>(
