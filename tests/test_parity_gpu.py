@@ -470,3 +470,26 @@ def test_graph_replayed_passes_equal_eager():
             E.GRAPHS = True
     assert np.array_equal(out[True][0], out[False][0])
     assert out[True][1] == out[False][1]
+
+
+def test_engine_full_c2_shape_vs_oracle():
+    """BASELINE configs[1] at full width and block length (12 heads x 128, T = 4680 tokens =
+    3 latent frames x 1560), 2 layers, 2 blocks, 2 denoise steps, the reference's PCG64
+    weights and seeded noise: final latents vs the numpy oracle (fp32) within the stated
+    tolerance, page table bit-exact (about a minute of numpy on the host)."""
+    from oracle import engine as OE
+    from paper_2511_20714_b200 import engine as E
+
+    kw = dict(layers=2, heads=12, head_dim=128, block_len=4680, frame_shape=(4, 4), prompt_dim=16,
+              weight_seed=0)
+    req = dict(num_blocks=2, seed=0, prompt_schedule=[(0, "a quiet scene")])
+    eng = E.Engine(E.build_model(E.ModelConfig(**kw)))
+    got = np.stack([b.latent for b in eng.generate(E.GenerationRequest(
+        schedule=E.DenoiseSchedule([1.0, 0.5]), **req))])
+    want, ocache = OE.generate_sequence(OE.ToyModel(OE.ModelConfig(**kw)), OE.GenerationRequest(
+        schedule=OE.DenoiseSchedule([1.0, 0.5]), **req))
+    want = np.stack(want)
+    err, cos = float(np.abs(got - want).max()), _cos(got, want)
+    print(f"c2 shape, 2 layers x 2 blocks: max-abs {err:.3e} cosine {cos:.7f}")
+    assert err <= ATOL_LATENT and cos > 0.999
+    assert eng.cache.state() == ocache.state()
