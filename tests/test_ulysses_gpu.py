@@ -93,7 +93,8 @@ KV_SPILL = dict(num_layers=2, head_dim=256, page_len=16, capacity_pages_device=4
 @pytest.mark.parametrize("world,cfg,kvc,pad", [(2, CFG, None, True), (2, CFG_ROPE, None, True),
                                               (2, CFG, KV_SPILL, True),
                                               (2, CFG_ROPE, None, False),  # balanced: 1.5 heads/rank
-                                              (2, dict(CFG, heads=3), dict(KV_SPILL, head_dim=192), False)])
+                                              (2, dict(CFG, heads=3), dict(KV_SPILL, head_dim=192), False),
+                                              (3, dict(CFG, block_len=192), None, False)])  # 4 heads / 3 ranks
 def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad):
     from paper_2511_20714_b200 import engine as E
 
