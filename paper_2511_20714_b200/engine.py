@@ -981,6 +981,65 @@ class Engine:
         return blocks
 
 
+def recompute_reference(model: ToyModel, request: GenerationRequest) -> list:
+    """engine.py:424-489 — the cache-free check: every denoise step recomputes the whole
+    sequence [clean prior blocks ∥ current latent] under the (windowed) block-causal mask,
+    context tokens at t = 0, each block's rows cross-attending its own prompt. On device:
+    the same kernels as the engine (RMS, bf16 GEMMs, K1 with a dense mask, K1s for the
+    prompt keys); O(blocks^2) work, meant for validation-size configs."""
+    from .attention import windowed_block_causal_mask
+    request.validate()
+    c = model.config
+    dev = require_cuda()
+    T, D, H, dhp, Dp = c.block_len, c.model_dim, model.heads_pad, model.dh_pad, model.attn_width
+    sc = 1.0 / math.sqrt(c.head_dim)
+    clean, prompts, blocks = [], [], []
+    for chunk in range(request.num_blocks):
+        prompt = _prompt_for_chunk(request.prompt_schedule, chunk)
+        prompts.append([(k.to(torch.bfloat16).contiguous(), v.to(torch.bfloat16).contiguous())
+                        for k, v in _cross_kv(model, embed_prompt(model, prompt))])
+        lat = torch.from_numpy(_init_noise(c, request.seed, chunk)).to(dev)
+        nb = len(clean) + 1
+        n = nb * T
+        mask = windowed_block_causal_mask(nb, T, request.kv_window).to(torch.uint8).contiguous()
+        rope = None
+        if c.rope_grid is not None:  # every token at its own block's absolute positions
+            tabs = [rope_tables(c, bi, dev) for bi in range(nb)]
+            rope = (torch.cat([a for a, _ in tabs]), torch.cat([b for _, b in tabs]))
+        for t in request.schedule.steps:
+            tcol = torch.zeros(n, 1, device=dev)
+            tcol[(nb - 1) * T:] = float(t)
+            x = (torch.cat(clean + [lat]) + tcol * model.time_vec).contiguous()
+            h = torch.empty(n, D, device=dev, dtype=torch.bfloat16)
+            qkv = torch.empty(n, 3 * Dp, device=dev, dtype=torch.bfloat16)
+            att = torch.empty(n, Dp, device=dev, dtype=torch.bfloat16)
+            for lw in model.layers:
+                rms_bf16(x, h)
+                torch.mm(h, lw.wqkv, out=qkv)
+                if rope is not None:
+                    rope_qk(qkv, H, dhp, c.head_dim // 2, 0, Dp, rope[0], rope[1])
+                attn_fwd(qkv[:, :Dp], H, dhp, att, qkv[:, Dp:2 * Dp], qkv[:, 2 * Dp:], 0, n,
+                         scale=sc, mask=mask)
+                _residual(x, att, lw.wo)
+                rms_bf16(x, h)
+                q2 = torch.mm(h, lw.cq)
+                for bi in range(nb):  # each block's rows vs its own prompt (engine.py:470-476)
+                    r = slice(bi * T, (bi + 1) * T)
+                    kc, vc = prompts[bi][model.layers.index(lw)]
+                    attn_fwd(q2[r], H, dhp, att[r], kc, vc, 0, kc.shape[0], scale=sc)
+                _residual(x, att, lw.co)
+                rms_bf16(x, h)
+                f = torch.empty(n, 2 * D, device=dev, dtype=torch.bfloat16)
+                _ffn_up(h, lw.w1, torch.zeros(2 * D, device=dev, dtype=torch.bfloat16), f)
+                _residual(x, f, lw.w2)
+            rms_bf16(x, h)
+            eps = torch.mm(h[(nb - 1) * T:], model.w_out, out_dtype=torch.float32)
+            lat = lat - float(request.schedule.step_scale) * eps
+        clean.append(lat)
+        blocks.append(GeneratedBlock(chunk, lat.cpu().numpy(), decode_frames(model, lat), prompt))
+    return blocks
+
+
 def generate_sequence(model: ToyModel, request: GenerationRequest, sinks=(),
                       kv_config: KvConfig | None = None, profiler=None) -> list:
     """engine.py:414-421."""

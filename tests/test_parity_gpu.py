@@ -493,3 +493,24 @@ def test_engine_full_c2_shape_vs_oracle():
     print(f"c2 shape, 2 layers x 2 blocks: max-abs {err:.3e} cosine {cos:.7f}")
     assert err <= ATOL_LATENT and cos > 0.999
     assert eng.cache.state() == ocache.state()
+
+
+@pytest.mark.parametrize("win", [None, 20])
+def test_recompute_reference_on_device(win):
+    """engine.recompute_reference (engine.py:424-489) on the GPU: matches the oracle's
+    cache-free recompute and the cached engine (the reference's own cache == recompute
+    check, test_engine.py:187-218)."""
+    from oracle import engine as OE
+    from paper_2511_20714_b200 import engine as E
+
+    kw = dict(layers=2, heads=2, head_dim=64, block_len=24, frame_shape=(4, 4), prompt_dim=8)
+    req = dict(num_blocks=3, seed=5, prompt_schedule=[(0, "a b"), (2, "c")], kv_window=win)
+    model = E.build_model(E.ModelConfig(**kw))
+    rec = np.stack([b.latent for b in E.recompute_reference(model, E.GenerationRequest(
+        schedule=E.DenoiseSchedule([1.0, 0.5]), **req))])
+    want = np.stack(OE.recompute_reference(OE.ToyModel(OE.ModelConfig(**kw)), OE.GenerationRequest(
+        schedule=OE.DenoiseSchedule([1.0, 0.5]), **req)))
+    cached = np.stack([b.latent for b in E.Engine(model).generate(E.GenerationRequest(
+        schedule=E.DenoiseSchedule([1.0, 0.5]), **req))])
+    assert np.abs(rec - want).max() <= ATOL_LATENT and _cos(rec, want) > 0.999
+    assert np.abs(rec - cached).max() <= ATOL_LATENT
