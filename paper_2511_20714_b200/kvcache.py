@@ -78,6 +78,21 @@ class KvConfig:
 
 
 @dataclass
+class KvPage:
+    """kvcache.py:68-76 — one page of a stream. k_data / v_data are the page's stored rows
+    ([filled, stored_width] CUDA tensors, read from whichever tier holds them); `slot` is
+    the B200 physical slot in that tier's pool."""
+    id: int
+    tier: str
+    k_data: object
+    v_data: object
+    filled: int = 0
+    start_token: int = 0
+    last_access: int = 0
+    slot: int = -1
+
+
+@dataclass
 class BlockEntry:
     """kvcache.py:79-86."""
     block_id: int
@@ -588,6 +603,21 @@ class KvCache:
     def state(self) -> dict:
         with self._lock:
             return self._pt.state()
+
+    def pages(self, layer: int, kind: str = SELF_ATTN) -> list:
+        """The pages of a stream in token order as KvPage records (kvcache.py:98-101), with
+        their rows gathered from their tier (no access-clock tick, like dump())."""
+        with self._lock:
+            for lay, knd, _base, total, pgs in self.state()["streams"]:
+                if lay == layer and knd == kind and pgs:
+                    s0 = pgs[0][3]
+                    k, v = self._gather(layer, kind, None, s0, total - s0, s0, total, raw=True)
+                    codes, _ = self._pt.slots(layer, kind, s0, total)
+                    return [KvPage(pid, DEVICE if tier == 0 else HOST, k[st - s0:st - s0 + f],
+                                   v[st - s0:st - s0 + f], f, st, la,
+                                   int(c) if c >= 0 else -1 - int(c))
+                            for (pid, tier, f, st, la), c in zip(pgs, codes)]
+            return []
 
     def block_entries(self) -> list:
         """kvcache.py:374-376."""

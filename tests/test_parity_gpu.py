@@ -514,3 +514,19 @@ def test_recompute_reference_on_device(win):
         schedule=E.DenoiseSchedule([1.0, 0.5]), **req))])
     assert np.abs(rec - want).max() <= ATOL_LATENT and _cos(rec, want) > 0.999
     assert np.abs(rec - cached).max() <= ATOL_LATENT
+
+
+def test_kvcache_pages_records():
+    """KvPage records (kvcache.py:68-76) carry each page's rows from whichever tier holds it."""
+    from paper_2511_20714_b200.kvcache import DEVICE, HOST, KvCache, KvConfig
+
+    c = KvCache(KvConfig(num_layers=1, head_dim=8, page_len=4, capacity_pages_device=2,
+                         capacity_pages_host=8))
+    rng = np.random.default_rng(0)
+    k = rng.standard_normal((10, 8)).astype(np.float32)
+    c.append_block(0, k, -k)
+    pages = c.pages(0)
+    assert [p.tier for p in pages] == [DEVICE, DEVICE, HOST]
+    assert [p.filled for p in pages] == [4, 4, 2] and [p.start_token for p in pages] == [0, 4, 8]
+    got = np.concatenate([_np(p.k_data) for p in pages])
+    assert np.array_equal(got, k) and np.array_equal(np.concatenate([_np(p.v_data) for p in pages]), -k)
