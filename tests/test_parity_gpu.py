@@ -530,3 +530,45 @@ def test_kvcache_pages_records():
     assert [p.filled for p in pages] == [4, 4, 2] and [p.start_token for p in pages] == [0, 4, 8]
     got = np.concatenate([_np(p.k_data) for p in pages])
     assert np.array_equal(got, k) and np.array_equal(np.concatenate([_np(p.v_data) for p in pages]), -k)
+
+
+def test_host_tier_bit_identical_at_full_block_length():
+    """1.3B width and block length (12 x 128, T = 4680), 2 layers, 5 blocks: a device tier
+    far below the working set (pages spill, fetches restore/demote in batches, host pages
+    are staged for K1) must give bit-identical latents to an all-device cache — the tiers
+    move bytes, never change them — and the reference's page-table state."""
+    from oracle import kvcache as OK
+    from paper_2511_20714_b200 import engine as E
+
+    T, nb, L = 4680, 5, 2
+    cfg = E.ModelConfig(layers=L, heads=12, head_dim=128, block_len=T, frame_shape=(4, 4),
+                        prompt_dim=16)
+    model = E.build_model(cfg, weights="device")
+    req = E.GenerationRequest(nb, E.DenoiseSchedule([1.0, 0.5]), seed=0)
+    pages_blk = -(-T // 16)
+    outs, states = [], []
+    for cap in (10**6, 3 * L * pages_blk // 2):  # all device / 1.5 blocks of pages in HBM
+        kvc = E.default_kv_config(cfg, capacity_pages_device=cap, capacity_pages_host=10**5)
+        eng = E.Engine(model, kvc)
+        outs.append(np.stack([b.latent for b in eng.generate(req)]))
+        states.append(eng.cache.state())
+        if cap < 10**6:
+            assert eng.cache.memory_stats().host_pages_used > 0 and eng.cache.moved_pages[1] > 0
+    assert np.array_equal(outs[0], outs[1])
+    # bookkeeping of the spilling run == the oracle driven by the engine's call sequence
+    o = OK.create_cache(OK.KvConfig(num_layers=L, head_dim=8, page_len=16,
+                                    capacity_pages_device=3 * L * pages_blk // 2,
+                                    capacity_pages_host=10**5))
+    z3, zt = np.zeros((3, 8), np.float32), np.zeros((T, 8), np.float32)
+    for li in range(L):
+        o.append_block(li, z3, z3, kind="cross_attn", chunk_index=0)
+    for chunk in range(nb):
+        for li in range(L):
+            lo, hi = o.addressable_range(li)
+            if hi > lo:
+                o.fetch_range(li, (lo, hi))
+        for li in range(L):
+            o.fetch_range(li, o.addressable_range(li, "cross_attn"), "cross_attn")
+        for li in range(L):
+            o.append_block(li, zt, zt, chunk_index=chunk)
+    assert states[1] == o.state()
