@@ -9,6 +9,14 @@
 #include <cstdio>
 #include <vector>
 
+__global__ void fill_rand(__nv_bfloat16* p, size_t n, unsigned seed, float scale) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned h = (unsigned)i * 2654435761u ^ seed;
+    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+    p[i] = __float2bfloat16(((h & 0xFFFF) / 65535.f - 0.5f) * scale);
+  }
+}
+
 #define CK(x) do { auto e = (x); if (e != 0) { printf("err %d at %s:%d\n", (int)e, __FILE__, __LINE__); return 1; } } while (0)
 
 int run(cublasLtHandle_t lt, int M, int N, int K, bool beta1, const char* name) {
@@ -18,8 +26,8 @@ int run(cublasLtHandle_t lt, int M, int N, int K, bool beta1, const char* name) 
   CK(cudaMalloc(&A, (size_t)M * K * 2));
   CK(cudaMalloc(&B, (size_t)K * N * 2));
   CK(cudaMalloc(&C, (size_t)M * N * 4));
-  cudaMemset(A, 0, (size_t)M * K * 2);
-  cudaMemset(B, 0, (size_t)K * N * 2);
+  fill_rand<<<1184, 256>>>(A, (size_t)M * K, 1u, 4.f);  // random operands: realistic power
+  fill_rand<<<1184, 256>>>(B, (size_t)K * N, 2u, 0.1f);
   cudaMemset(C, 0, (size_t)M * N * 4);
   void* ws;
   size_t ws_bytes = 64 << 20;
