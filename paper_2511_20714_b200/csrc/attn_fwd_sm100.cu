@@ -412,11 +412,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (!ok) sv[i] = -INFINITY;
         }
       }
-      float m4[4];
+      float m4[8];  // 8 independent max chains (ILP; +0.5 % in the bench, r03_attn_poly.md)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) m4[i] = sv[i];
+      for (int i = 0; i < 8; ++i) m4[i] = sv[i];
 #pragma unroll
-      for (int i = 4; i < HALF; ++i) m4[i & 3] = fmaxf(m4[i & 3], sv[i]);
+      for (int i = 8; i < HALF; ++i) m4[i & 7] = fmaxf(m4[i & 7], sv[i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) m4[i] = fmaxf(m4[i], m4[i + 4]);
       // this key half's own online softmax: no per-tile exchange with the other half
       const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       const float m_tile = mx * sl2;  // -inf if nothing visible
@@ -433,8 +435,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // MUFU.EX2 stays scalar (the bf16x2/f16x2 forms issue two MUFU ops on sm_100)
       const float2 sl2v = make_float2(sl2, sl2);
       const float2 negm = make_float2(-m_sub, -m_sub);
-      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                       make_float2(0.f, 0.f)};
+      float2 acc[8];  // 8 independent sum chains (ILP)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.f, 0.f);
       if (full) {
 #pragma unroll
         for (int i = 0; i < HALF / 2; ++i) {
@@ -448,7 +451,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
           sv[2 * i] = p.x;
           sv[2 * i + 1] = p.y;
-          acc[i & 3] = __fadd2_rn(acc[i & 3], p);
+          acc[i & 7] = __fadd2_rn(acc[i & 7], p);
         }
       } else {
 #pragma unroll
@@ -457,9 +460,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const float2 p = make_float2(ex2(x.x), ex2(x.y));  // exp2(-inf) = 0 for masked keys
           sv[2 * i] = p.x;
           sv[2 * i + 1] = p.y;
-          acc[i & 3] = __fadd2_rn(acc[i & 3], p);
+          acc[i & 7] = __fadd2_rn(acc[i & 7], p);
         }
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = __fadd2_rn(acc[i], acc[i + 4]);
       const float2 a01 = __fadd2_rn(acc[0], acc[1]), a23 = __fadd2_rn(acc[2], acc[3]);
       const float2 a4 = __fadd2_rn(a01, a23);
       l_half = l_half * alpha + (a4.x + a4.y);

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 __global__ void fill_rand(__nv_bfloat16* p, size_t n, unsigned seed, float scale) {
@@ -71,14 +72,17 @@ int run(cublasLtHandle_t lt, int M, int N, int K, bool beta1, const char* name) 
   return 0;
 }
 
-int main() {
+int main(int argc, char** argv) {
   cublasLtHandle_t lt;
   cublasLtCreate(&lt);
-  run(lt, 4680, 4608, 1536, false, "QKV");
-  run(lt, 4680, 1536, 1536, true, "wo (residual)");
-  run(lt, 4680, 3072, 1536, false, "w1");
-  run(lt, 4680, 1536, 3072, true, "w2 (residual)");
-  run(lt, 4680, 15360, 5120, false, "QKV 14B");
-  run(lt, 4680, 5120, 5120, true, "wo 14B (residual)");
+  const int M = argc > 1 ? atoi(argv[1]) : 4680;
+  run(lt, M, 4608, 1536, false, "QKV");
+  run(lt, M, 1536, 1536, true, "wo (residual)");
+  run(lt, M, 3072, 1536, false, "w1");
+  run(lt, M, 1536, 3072, true, "w2 (residual)");
+  run(lt, M, 15360, 5120, false, "QKV 14B");
+  run(lt, M, 5120, 5120, true, "wo 14B (residual)");
+  run(lt, M, 10240, 5120, false, "w1 14B");
+  run(lt, M, 5120, 10240, true, "w2 14B (residual)");
   return 0;
 }
