@@ -263,6 +263,12 @@ int ifx_ulysses_unpack(const void* src, int64_t n, int64_t groups, int64_t world
 int ifx_copy_blocks(const void* src, void* dst, const int64_t* desc, int64_t n_blocks,
                     int64_t max_rows, void* stream);
 
+/* Dense projection on cuBLASLt (a plain library GEMM; per-shape algorithm choice timed on
+ * the first call outside a CUDA-graph capture): D[M,N] = relu?(A[M,K] . B[K,N] + beta * D),
+ * row-major bf16 A (row stride lda) and B (ldb), fp32 accumulate, D fp32 or bf16 (ldd). */
+int ifx_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
+                  int d_type, int64_t M, int64_t N, int64_t K, float beta, int relu, void* stream);
+
 /* Initial block noise, host side (engine.py:280-282): writes the first n values of
  * np.random.default_rng([seed, chunk]).standard_normal(...).astype(float32) into `out`
  * (host memory, e.g. pinned), bit-identically, using `threads` host threads (0 = all).

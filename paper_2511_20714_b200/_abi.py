@@ -43,7 +43,7 @@ EXPORTS = (
     "ifx_kv_append", "ifx_kv_gather", "ifx_kv_move_pages", "ifx_kv_copy_runs", "ifx_host_alloc", "ifx_host_free",
     "ifx_attn_fwd", "ifx_attn_workspace_bytes",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_group_softmax", "ifx_ulysses_pack", "ifx_ulysses_unpack",
-    "ifx_copy_blocks",
+    "ifx_copy_blocks", "ifx_gemm_bf16",
     "ifx_noise_normal_f32",
 )
 
@@ -128,6 +128,8 @@ def lib() -> ctypes.CDLL:
             L.ifx_attn_workspace_bytes.argtypes = [ctypes.POINTER(AttnParams), PI64]
             L.ifx_rms_bf16.argtypes = [P, I64, I64, P, ctypes.c_float, P, P, P]
             L.ifx_copy_blocks.argtypes = [P, P, P, I64, I64, P]
+            L.ifx_gemm_bf16.argtypes = [P, I64, P, I64, P, I64, ctypes.c_int, I64, I64, I64,
+                                        ctypes.c_float, ctypes.c_int, P]
             L.ifx_group_softmax.argtypes = [P, I64, I64, I64, I64, ctypes.c_float, P, I64, P]
             L.ifx_rope_qk.argtypes = [P, I64, I64, I64, I64, I64, I64, I64, P, P, I64, P]
             L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]

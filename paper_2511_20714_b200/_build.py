@@ -17,7 +17,7 @@ OUT = os.path.join(PKG, "libinferix_b200.so")
 OBJ = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["attn_fwd_sm100.cu", "attn_few_keys.cu", "kv_ops.cu", "abi.cpp", "pagetable.cpp", "noise_host.cpp"]
+SOURCES = ["attn_fwd_sm100.cu", "attn_few_keys.cu", "kv_ops.cu", "gemm_lt.cpp", "abi.cpp", "pagetable.cpp", "noise_host.cpp"]
 
 
 def _npyrandom() -> str:
@@ -55,7 +55,8 @@ def build(verbose: bool = False) -> str:
         objs = list(ex.map(_compile, SOURCES))
     if os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(o) for o in objs):
         return OUT
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, _npyrandom(), "-lcudart_static", "-Xlinker", "--exclude-libs,ALL",
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, _npyrandom(), "-lcudart_static", "-L/usr/local/cuda/lib64", "-lcublasLt",
+           "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-Xlinker", "--exclude-libs,ALL",
            "-lm", "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -123,6 +123,21 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
     return out
 
 
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, beta: float = 0.0,
+         relu: bool = False, stream=None) -> torch.Tensor:
+    """out = relu?(a @ b + beta * out) on cuBLASLt through ifx_gemm_bf16: bf16 a [M, K] and
+    b [K, N] (rows contiguous), fp32 accumulate, out fp32 or bf16 [M, N]."""
+    M, K = a.shape
+    N = b.shape[1]
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or b.shape[0] != K or \
+            tuple(out.shape) != (M, N):
+        raise DimensionError("gemm expects bf16 a [M, K], b [K, N] and out [M, N]")
+    _abi.check(_abi.lib().ifx_gemm_bf16(a.data_ptr(), row_ld(a), b.data_ptr(), row_ld(b),
+                                        out.data_ptr(), row_ld(out), dtype_code(out.dtype), M, N,
+                                        K, float(beta), int(relu), stream_ptr(stream)), "gemm")
+    return out
+
+
 def tile_run_codes(codes: np.ndarray, page_len: int) -> np.ndarray:
     """Per 128-key tile of a paged context (K1's ctx_tile_runs): the first page's slot code
     when the tile's pages are one consecutive run of one pool, else INT32_MIN. The last

@@ -33,8 +33,8 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._device import (attn_fwd, count_launch, require_cuda, rms_bf16, rope_qk, stream_ptr,
-                      tile_run_codes)
+from ._device import (attn_fwd, count_launch, gemm, require_cuda, rms_bf16, rope_qk,
+                      stream_ptr, tile_run_codes)
 from .errors import ConfigError, DimensionError
 from .kvcache import CROSS_ATTN, SELF_ATTN, KvCache, KvConfig
 
@@ -345,12 +345,12 @@ def _cross_attend(ws, fold: _CrossFold, x: torch.Tensor, h: torch.Tensor, scale:
         buf = ws.cross_bufs[key] = (torch.empty(T, fold.width, device=h.device),
                                     torch.zeros(T, fold.width, device=h.device, dtype=torch.bfloat16))
     s, p = buf
-    torch.mm(h, fold.wqk, out_dtype=torch.float32, out=s)
+    gemm(h, fold.wqk, s)
     _abi.check(_abi.lib().ifx_group_softmax(s.data_ptr(), T, fold.groups, fold.n, fold.width,
                                             float(scale), p.data_ptr(), fold.width,
                                             stream_ptr()), "group_softmax")
     count_launch()
-    torch.addmm(x, p, fold.wvo, out_dtype=torch.float32, out=x)
+    gemm(p, fold.wvo, x, beta=1.0)
 
 
 class _Workspace:
@@ -363,19 +363,18 @@ class _Workspace:
         self.attn = torch.empty(T, Dp, device=dev, dtype=torch.bfloat16)
         self.ffn = torch.empty(T, 2 * D, device=dev, dtype=torch.bfloat16)
         self.tmp = torch.empty(T, D, device=dev, dtype=torch.float32)
-        self.zero_bias = torch.zeros(2 * D, device=dev, dtype=torch.bfloat16)
         self.cross_bufs = {}
 
 
 def _residual(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor, tmp: torch.Tensor = None):
     """x += a @ w with bf16 operands, fp32 accumulation and fp32 in-place epilogue (one
-    cuBLASLt call with beta = 1; 24 us vs 33 us for mm + add at the c2 shape)."""
-    torch.addmm(x, a, w, out_dtype=torch.float32, out=x)
+    cuBLASLt call with beta = 1, per-shape algorithm, `ifx_gemm_bf16`)."""
+    gemm(a, w, x, beta=1.0)
 
 
-def _ffn_up(h: torch.Tensor, w1: torch.Tensor, zero_bias: torch.Tensor, out: torch.Tensor):
+def _ffn_up(h: torch.Tensor, w1: torch.Tensor, out: torch.Tensor):
     """relu(h @ w1) with the ReLU in the cuBLASLt epilogue (engine.py:216)."""
-    torch._addmm_activation(zero_bias, h, w1, use_gelu=False, out=out)
+    gemm(h, w1, out, relu=True)
 
 
 class BlockRunner:
@@ -393,6 +392,7 @@ class BlockRunner:
         self.stager = _Stager(self.dev)
         self._eps = None
         self._tv = self._gpool = self._cap = self._graph = None  # CUDA-graph state (_euler_steps)
+        self._warm = False
 
     def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
                 collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None,
@@ -412,7 +412,7 @@ class BlockRunner:
                     rms_bf16(latent, ws.h, m.time_vec, t, x_out=ws.x)
             else:
                 rms_bf16(ws.x, ws.h)
-            torch.mm(ws.h, lw.wqkv, out=ws.qkv)
+            gemm(ws.h, lw.wqkv, ws.qkv)
             if rope is not None:  # Q and the block's own K, before K1 and the page write
                 rope_qk(ws.qkv, H, dhp, c.head_dim // 2, 0, Dp, rope[0], rope[1])
             ev = self.attn_events
@@ -432,13 +432,13 @@ class BlockRunner:
                 rms_bf16(ws.x, ws.h)
                 _cross_attend(ws, cross[li], ws.x, ws.h, sc)
             rms_bf16(ws.x, ws.h)
-            _ffn_up(ws.h, lw.w1, ws.zero_bias, ws.ffn)
+            _ffn_up(ws.h, lw.w1, ws.ffn)
             _residual(ws.x, ws.ffn, lw.w2, ws.tmp)
             if collect_kv:  # clean pass: page write of this layer's K/V (engine.py:303-306)
                 cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
         if eps_out is not None:
             rms_bf16(ws.x, ws.h)
-            torch.mm(ws.h, m.w_out, out_dtype=torch.float32, out=eps_out)
+            gemm(ws.h, m.w_out, eps_out)
 
     def denoise(self, latent: torch.Tensor, schedule: DenoiseSchedule, ctx, cross,
                 cache: KvCache | None, chunk_index: int) -> torch.Tensor:
@@ -476,6 +476,14 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     tv, cap = runner._tv, runner._cap
     if ctx is not None:
         ctx.prepare()
+    if not runner._warm and len(steps) > 1:
+        # the runner's first pass runs eagerly: library state (cuBLASLt handle, workspace,
+        # per-shape algorithm choice in ifx_gemm_bf16) is set up outside any capture
+        torch.mul(m.time_vec, steps[0], out=tv)
+        runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
+        latent.add_(eps, alpha=-float(schedule.step_scale))
+        runner._warm = True
+        steps = steps[1:]
     use = (GRAPHS and graphs_ok and len(steps) > 1 and runner.attn_events is None
            and (ctx is None or (ctx.paged and not ctx.jobs)))
     if not use:

@@ -524,12 +524,12 @@ class UlyssesRunner:
         self.attn_s = torch.empty(n, Dp, device=dev, dtype=torch.bfloat16)
         self.ffn = torch.empty(n, 2 * D, device=dev, dtype=torch.bfloat16)
         self.eps = torch.empty(n, D, device=dev)
-        self.zero_bias = torch.zeros(2 * D, device=dev, dtype=torch.bfloat16)
         self.cross_bufs = {}
         self.attn_events = None
         from .engine import _Stager
         self.stager = _Stager(dev)
         self._tv = self._gpool = self._cap = self._graph = None  # CUDA-graph state (_euler_steps)
+        self._warm = False
 
     def _balanced_attention(self, li, ctx, sc, ev):
         """BalancedPlan: re-shard (one all-to-all), one K1 per segment (a head's query rows,
@@ -568,6 +568,7 @@ class UlyssesRunner:
 
     def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None,
                 rope=None):
+        from ._device import gemm
         from .engine import _cross_attend, _ffn_up, _residual
         from .kvcache import SELF_ATTN
         m = self.model
@@ -582,7 +583,7 @@ class UlyssesRunner:
                     self._rms(latent, self.h, m.time_vec, t, self.x)
             else:
                 self._rms(self.x, self.h)
-            torch.mm(self.h, lw.wqkv, out=self.qkv)
+            gemm(self.h, lw.wqkv, self.qkv)
             if rope is not None:  # this rank's rows of the block: table rows rank*n ..
                 from ._device import rope_qk
                 rope_qk(self.qkv, m.heads_pad, dhp, c.head_dim // 2, 0, m.attn_width, rope[0],
@@ -607,13 +608,13 @@ class UlyssesRunner:
                 self._rms(self.x, self.h)
                 _cross_attend(self, cross[li], self.x, self.h, sc)
             self._rms(self.x, self.h)
-            _ffn_up(self.h, lw.w1, self.zero_bias, self.ffn)
+            _ffn_up(self.h, lw.w1, self.ffn)
             _residual(self.x, self.ffn, lw.w2)
             if collect_kv:  # rank-local page write of this rank's heads
                 cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
         if eps_out is not None:
             self._rms(self.x, self.h)
-            torch.mm(self.h, m.w_out, out_dtype=torch.float32, out=eps_out)
+            gemm(self.h, m.w_out, eps_out)
 
     def denoise(self, latent, schedule, ctx, cross, cache, chunk_index):
         from .engine import _euler_steps, rope_tables

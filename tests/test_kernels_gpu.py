@@ -283,3 +283,28 @@ def test_addmm_out_dtype_fp32_residual():
     y = torch.mm(a, b, out_dtype=torch.float32)
     assert y.dtype == torch.float32
     assert torch.allclose(y, a.float() @ b.float(), atol=1e-3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N,K", [(4680, 4608, 1536), (4680, 1536, 3072), (77, 96, 64)])
+def test_gemm_lt_matches_torch(M, N, K):
+    """ifx_gemm_bf16 (cuBLASLt, per-shape algorithm) against fp32 torch: bf16 out, fp32 out,
+    fp32 residual with beta = 1 and the ReLU epilogue."""
+    from paper_2511_20714_b200._device import gemm
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(K, N, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    ref = a.float() @ b.float()
+    o16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    gemm(a, b, o16)
+    torch.testing.assert_close(o16.float(), ref, atol=2e-2, rtol=1e-2)
+    o32 = torch.randn(M, N, device="cuda", generator=g)
+    x0 = o32.clone()
+    gemm(a, b, o32, beta=1.0)
+    torch.testing.assert_close(o32, x0 + ref, atol=2e-3, rtol=1e-3)
+    gemm(a, b, o16, relu=True)
+    torch.testing.assert_close(o16.float(), ref.clamp_min(0), atol=2e-2, rtol=1e-2)
+    # a strided A (a column block of a wider buffer), as the engine passes it
+    wide = torch.randn(M, K + 64, device="cuda", generator=g).bfloat16()
+    gemm(wide[:, 32:32 + K], b, o32)
+    torch.testing.assert_close(o32, wide[:, 32:32 + K].float() @ b.float(), atol=2e-3, rtol=1e-3)
