@@ -97,6 +97,7 @@ def lib() -> ctypes.CDLL:
                 raise ImportError(
                     f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                     f"g.build()'` (there is no CPU fallback)")
+            import torch  # noqa: F401  (torch's CUDA libraries first: one cuBLASLt per process)
             L = ctypes.CDLL(LIB_PATH)
             L.ifx_last_error.restype = ctypes.c_char_p
             L.ifx_pt_create.argtypes = [I64, I64, I64, I64, I64, ctypes.POINTER(P)]

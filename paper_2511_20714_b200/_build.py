@@ -49,15 +49,32 @@ def _compile(src: str) -> str:
     return obj
 
 
+def _cublaslt_dir() -> str:
+    """The cuBLASLt torch itself loads (the pip `nvidia-cublas` wheel): one copy per process
+    whichever of torch and this library is loaded first. Linking the toolkit's newer copy
+    instead made torch's libcublas run against a mismatched libcublasLt when this library
+    was loaded before torch (CUBLAS_STATUS_INVALID_VALUE in torch GEMMs)."""
+    try:
+        import nvidia.cublas as nc
+        d = os.path.join(list(nc.__path__)[0], "lib")
+        if os.path.exists(os.path.join(d, "libcublasLt.so.12")):
+            return d
+    except ImportError:
+        pass
+    return "/usr/local/cuda/lib64"
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(_compile, SOURCES))
     if os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(o) for o in objs):
         return OUT
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, _npyrandom(), "-lcudart_static", "-L/usr/local/cuda/lib64", "-lcublasLt",
-           "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-Xlinker", "--exclude-libs,ALL",
-           "-lm", "-Xcompiler", "-fPIC"]
+    lt = _cublaslt_dir()
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, _npyrandom(), "-lcudart_static",
+           f"-L{lt}", "-l:libcublasLt.so.12", "-Xlinker", f"-rpath={lt}",
+           "-Xlinker", "--disable-new-dtags",  # DT_RPATH: wins over LD_LIBRARY_PATH
+           "-Xlinker", "--exclude-libs,ALL", "-lm", "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -1038,7 +1038,7 @@ def recompute_reference(model: ToyModel, request: GenerationRequest) -> list:
                 _residual(x, att, lw.co)
                 rms_bf16(x, h)
                 f = torch.empty(n, 2 * D, device=dev, dtype=torch.bfloat16)
-                _ffn_up(h, lw.w1, torch.zeros(2 * D, device=dev, dtype=torch.bfloat16), f)
+                _ffn_up(h, lw.w1, f)
                 _residual(x, f, lw.w2)
             rms_bf16(x, h)
             eps = torch.mm(h[(nb - 1) * T:], model.w_out, out_dtype=torch.float32)

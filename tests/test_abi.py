@@ -113,3 +113,16 @@ def test_page_table_batch_api():
     pt.touch_range(0, "self_attn", 2, 4)  # outside a batch: one D2H + one H2D
     mv = pt.drain_moves()
     assert sorted(mv[:, 2].tolist()) == [0, 1]
+
+
+def test_one_cublaslt_per_process():
+    """The library links the cuBLASLt torch loads: loading it BEFORE torch must not pull in a
+    second (toolkit) copy, which made torch's own GEMMs fail with CUBLAS_STATUS_INVALID_VALUE."""
+    import subprocess
+    import sys
+    code = ("import ctypes; ctypes.CDLL(%r); import torch; "
+            "print(sorted({l.split()[-1] for l in open('/proc/self/maps') if 'libcublasLt' in l}))"
+            % _abi.LIB_PATH)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    paths = eval(out.stdout.strip().splitlines()[-1])
+    assert len(paths) == 1, paths
