@@ -5,9 +5,11 @@
 // context concat it needs: softmax(Q K^T * scale) V with online (flash) softmax; every key
 // is visible (engine.py:209) unless a dense mask is given (API parity, attention.py:89).
 //
-// One CTA = one 128-query tile of one head (37 tiles x 12 heads = 444 = 3 x 148 CTAs at
-// the Wan-1.3B shape: exact waves), 320 threads:
-//   warp 0      TMA producer: Q once, then K_j / V_j tiles (128 keys x head_dim, SW128)
+// Work item = one 128-query tile of one head (and key split): 37 tiles x 12 heads = 444 =
+// 3 x 148 at the Wan-1.3B shape. Persistent CTAs (one per SM, 320 threads) walk items
+// blockIdx.x, blockIdx.x + gridDim.x, ...:
+//   warp 0      TMA producer: Q per item (double-buffered), then K_j / V_j tiles (128 keys x
+//               head_dim, SW128)
 //               into 2-stage smem rings; mbarrier tx completion
 //   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into TMEM (double-buffered S),
 //               then per key half h: O_h += P_h V_h (P read from TMEM, TS form) as soon as
@@ -33,6 +35,8 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "attn_kernel.h"
 #include "sm100_ptx.cuh"
@@ -92,12 +96,13 @@ struct Layout {
   static constexpr int KCH = HD / 64;
   static constexpr int Q_BYTES = BM * HD * 2;
   static constexpr int KV_BYTES = BN * HD * 2;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_Q = 0;                      // two Q buffers (item parity)
+  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
   static constexpr int OFF_RED = OFF_V + NS * KV_BYTES;  // float [2 halves][3][BM] merge swap
   static constexpr int OFF_BAR = OFF_RED + 2 * 3 * BM * 4;
-  static constexpr int NBAR = 1 + 4 * NS + 5 * NB;  // ... s_full s_empty p_full[2] pv_done
+  // q_full[2] q_empty[2] k_full k_empty v_full v_empty s_full s_empty p_full[2] pv_done o_free
+  static constexpr int NBAR = 4 + 4 * NS + 5 * NB + 1;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
   // TMEM columns: S0 [0,128) S1 [128,256) O_lo [256, 256+HD) O_hi [384, 384+HD).
   // Key half h of S_b (columns 64h..64h+63) is overwritten in place by its packed bf16 P
@@ -128,6 +133,26 @@ __device__ __forceinline__ Tile tile_of(const AttnKernelArgs& a, int j, int n0) 
   return t;
 }
 
+// A work item = (128-query tile, head, key split). CTAs are persistent: CTA c runs items
+// c, c + gridDim.x, ... in order, so the next item's Q load and first S tiles overlap the
+// previous item's epilogue (and the per-CTA setup is paid once per SM, not per item).
+struct Item {
+  int head, q0, split, t0, n_tiles;
+};
+
+__device__ __forceinline__ Item item_of(const AttnKernelArgs& a, int it, int n_total) {
+  const int gx = (a.n_q + BM - 1) / BM;
+  Item r;
+  r.q0 = (it % gx) * BM;
+  r.head = (it / gx) % a.heads;
+  r.split = it / (gx * a.heads);
+  // split-KV: this item walks key tiles [t0, t0 + n_tiles) and, when the key range is
+  // split, writes a partial (normalised O, max, denominator) merged by K4
+  r.t0 = (int)(((int64_t)r.split * n_total) / a.n_splits);
+  r.n_tiles = (int)(((int64_t)(r.split + 1) * n_total) / a.n_splits) - r.t0;
+  return r;
+}
+
 template <int HD, bool PAGED>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_fwd_kernel(const __grid_constant__ AttnKernelArgs a) {
@@ -140,8 +165,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* sV = smem + L::OFF_V;
   float* red = reinterpret_cast<float*>(smem + L::OFF_RED);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
+  uint64_t* q_full = bars;       // [2]
+  uint64_t* q_empty = bars + 2;  // [2]
+  uint64_t* k_full = bars + 4;
   uint64_t* k_empty = k_full + NS;
   uint64_t* v_full = k_empty + NS;
   uint64_t* v_empty = v_full + NS;
@@ -149,22 +175,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* s_empty = s_full + NB;
   uint64_t* p_full = s_empty + NB;   // [NB][2 key halves]
   uint64_t* pv_done = p_full + 2 * NB;
+  uint64_t* o_free = pv_done + NB;  // the softmax warps have read O of their current item
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NBAR);
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int head = blockIdx.y;
-  const int q0 = blockIdx.x * BM;
   const int n0 = (a.n_ctx + BN - 1) / BN;
   const int n_total = n0 + (a.n_cur + BN - 1) / BN;
-  // split-KV (blockIdx.z): this CTA walks key tiles [t0, t0 + n_tiles) and, when the key
-  // range is split, writes a partial (normalised O, max, denominator) merged by K4
-  const int split = blockIdx.z;
-  const int t0 = (int)(((int64_t)split * n_total) / a.n_splits);
-  const int n_tiles = (int)(((int64_t)(split + 1) * n_total) / a.n_splits) - t0;
+  const int n_items = ((a.n_q + BM - 1) / BM) * a.heads * a.n_splits;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+    }
+    mbar_init(o_free, NSOFT);
     for (int s = 0; s < NS; ++s) {
       mbar_init(k_full + s, 1);
       mbar_init(k_empty + s, 1);
@@ -198,12 +223,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tma_prefetch_desc(&a.tm_kn);
         tma_prefetch_desc(&a.tm_vn);
       }
-      mbar_expect_tx(q_full, L::Q_BYTES);
+      int g = 0;  // key tiles loaded so far by this CTA (smem ring position)
+      for (int it = blockIdx.x, k = 0; it < n_items; it += gridDim.x, ++k) {
+      const Item im = item_of(a, it, n_total);
+      const int head = im.head, t0 = im.t0, n_tiles = im.n_tiles;
+      const int ib = k & 1;
+      if (k >= 2) mbar_wait(q_empty + ib, ((k >> 1) - 1) & 1);
+      mbar_expect_tx(q_full + ib, L::Q_BYTES);
       for (int c = 0; c < L::KCH; ++c)
-        tma_load_2d(sQ + c * BM * 128, &a.tm_q, q_full, head * HD + c * 64, q0);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int s = j % NS;
-        const uint32_t ph = (j / NS) & 1;
+        tma_load_2d(sQ + ib * L::Q_BYTES + c * BM * 128, &a.tm_q, q_full + ib,
+                    head * HD + c * 64, im.q0);
+      for (int j = 0; j < n_tiles; ++j, ++g) {
+        const int s = g % NS;
+        const uint32_t ph = (g / NS) & 1;
         const Tile t = tile_of(a, t0 + j, n0);
         const CUtensorMap* mk = t.seg == 0 ? &a.tm_kc : &a.tm_kn;
         const CUtensorMap* mv = t.seg == 0 ? &a.tm_vc : &a.tm_vn;
@@ -217,6 +249,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int c = 0; c < L::KCH; ++c)
           tma_load_2d(sV + s * L::KV_BYTES + c * BN * 128, mv, v_full + s, head * HD + c * 64,
                       t.row);
+      }
       }
     }
     __syncwarp();
@@ -245,13 +278,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tma_prefetch_desc(&a.tm_kn);
         tma_prefetch_desc(&a.tm_vn);
       }
-      mbar_expect_tx(q_full, L::Q_BYTES);
+      int g = 0;  // key tiles loaded so far by this CTA (smem ring position)
+      for (int it = blockIdx.x, k = 0; it < n_items; it += gridDim.x, ++k) {
+      const Item im = item_of(a, it, n_total);
+      const int head = im.head, t0 = im.t0, n_tiles = im.n_tiles;
+      const int ib = k & 1;
+      if (k >= 2) mbar_wait(q_empty + ib, ((k >> 1) - 1) & 1);
+      mbar_expect_tx(q_full + ib, L::Q_BYTES);
       for (int c = 0; c < L::KCH; ++c)
-        tma_load_2d(sQ + c * BM * 128, &a.tm_q, q_full, head * HD + c * 64, q0);
+        tma_load_2d(sQ + ib * L::Q_BYTES + c * BM * 128, &a.tm_q, q_full + ib,
+                    head * HD + c * 64, im.q0);
       int32_t rnext = (runs != nullptr && n_tiles > 0 && t0 < n0) ? __ldg(runs + t0) : kNoRun;
-      for (int j = 0; j < n_tiles; ++j) {
-        const int s = j % NS;
-        const uint32_t ph = (j / NS) & 1;
+      for (int j = 0; j < n_tiles; ++j, ++g) {
+        const int s = g % NS;
+        const uint32_t ph = (g / NS) & 1;
         const Tile t = tile_of(a, t0 + j, n0);
         int32_t rc = rnext;
         if (runs != nullptr && j + 1 < n_tiles && t0 + j + 1 < n0) rnext = __ldg(runs + t0 + j + 1);
@@ -312,6 +352,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
+      }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -319,55 +360,68 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (elect_one()) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);  // Q, K both K-major
       constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, HD, 0, 1);  // P (TMEM), V MN-major
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      const uint32_t q_base = smem_u32(sQ);
-      for (int j = 0; j <= n_tiles; ++j) {
-        if (j < n_tiles) {
-          const int s = j % NS;
-          const int b = j % NB;
-          const uint32_t bph = (j / NB) & 1;
-          mbar_wait(k_full + s, (j / NS) & 1);
-          mbar_wait(s_empty + b, bph ^ 1);                    // S_b of tile j-NB read
-          // P_b aliases S_b: explicit wait (measured free: the in-order-only variant was no faster)
-          if (j >= NB) mbar_wait(pv_done + b, bph ^ 1);
-          tc_fence_after();
-          const uint32_t k_base = smem_u32(sK + s * L::KV_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-            const uint32_t offk = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-            mma_bf16_ss(tmem + b * 128, smem_desc_sw128(q_base + off, 16, 1024),
-                        smem_desc_sw128(k_base + offk, 16, 1024), idesc_qk, kk > 0);
-          }
-          mma_commit(k_empty + s);
-          mma_commit(s_full + b);
-        }
-        if (j >= 1) {
-          const int jp = j - 1;
-          const int s = jp % NS;
-          const int b = jp % NB;
-          mbar_wait(v_full + s, (jp / NS) & 1);
-          const uint32_t v_base = smem_u32(sV + s * L::KV_BYTES);
-          // O_h += P_h V[64h .. 64h+63]: each key half has its own running max, so its own
-          // accumulator; issued as soon as that half's softmax warps published P_h
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            mbar_wait(p_full + 2 * b + h, (jp / NB) & 1);
+      int g0 = 0;  // key tiles of earlier items (ring / S-buffer position)
+      for (int it = blockIdx.x, k = 0; it < n_items; it += gridDim.x, ++k) {
+        const int n_tiles = item_of(a, it, n_total).n_tiles;
+        const int ib = k & 1;
+        mbar_wait(q_full + ib, (k >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ + ib * L::Q_BYTES);
+        for (int j = 0; j <= n_tiles; ++j) {
+          if (j < n_tiles) {
+            const int gj = g0 + j;
+            const int s = gj % NS;
+            const int b = gj % NB;
+            const uint32_t bph = (gj / NB) & 1;
+            mbar_wait(k_full + s, (gj / NS) & 1);
+            mbar_wait(s_empty + b, bph ^ 1);                    // S_b of tile gj-NB read
+            // P_b aliases S_b: explicit wait (measured free: the in-order-only variant was no faster)
+            if (gj >= NB) mbar_wait(pv_done + b, bph ^ 1);
             tc_fence_after();
+            const uint32_t k_base = smem_u32(sK + s * L::KV_BYTES);
 #pragma unroll
-            for (int kk = 0; kk < HALF / 16; ++kk) {
-              // V tile: KCH chunks [BN keys x 64 dims], rows of 128 B; MN-major B operand:
-              // LBO = stride between 64-dim chunks, SBO = 8 key rows; K step = 16 rows.
-              const uint64_t bdesc =
-                  smem_desc_sw128(v_base + (h * (HALF / 16) + kk) * 16 * 128, BN * 128, 1024);
-              mma_bf16_ts(tmem + L::TM_O(h), tmem + b * 128 + L::TM_P(h) + kk * 8, bdesc,
-                          idesc_pv, (jp > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < HD / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+              const uint32_t offk = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
+              mma_bf16_ss(tmem + b * 128, smem_desc_sw128(q_base + off, 16, 1024),
+                          smem_desc_sw128(k_base + offk, 16, 1024), idesc_qk, kk > 0);
             }
+            mma_commit(k_empty + s);
+            mma_commit(s_full + b);
           }
-          mma_commit(v_empty + s);
-          mma_commit(pv_done + b);
+          if (k >= 1 && j == (n_tiles > 0 ? 1 : 0)) {
+            // O is overwritten by this item's first PV: the previous item's epilogue must
+            // have read it (this item's first two S tiles, issued above, overlap it)
+            mbar_wait(o_free, (k - 1) & 1);
+          }
+          if (j >= 1) {
+            const int gp = g0 + j - 1;
+            const int s = gp % NS;
+            const int b = gp % NB;
+            mbar_wait(v_full + s, (gp / NS) & 1);
+            const uint32_t v_base = smem_u32(sV + s * L::KV_BYTES);
+            // O_h += P_h V[64h .. 64h+63]: each key half has its own running max, so its own
+            // accumulator; issued as soon as that half's softmax warps published P_h
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              mbar_wait(p_full + 2 * b + h, (gp / NB) & 1);
+              tc_fence_after();
+#pragma unroll
+              for (int kk = 0; kk < HALF / 16; ++kk) {
+                // V tile: KCH chunks [BN keys x 64 dims], rows of 128 B; MN-major B operand:
+                // LBO = stride between 64-dim chunks, SBO = 8 key rows; K step = 16 rows.
+                const uint64_t bdesc =
+                    smem_desc_sw128(v_base + (h * (HALF / 16) + kk) * 16 * 128, BN * 128, 1024);
+                mma_bf16_ts(tmem + L::TM_O(h), tmem + b * 128 + L::TM_P(h) + kk * 8, bdesc,
+                            idesc_pv, (j > 1 || kk > 0) ? 1u : 0u);
+              }
+            }
+            mma_commit(v_empty + s);
+            mma_commit(pv_done + b);
+          }
         }
+        mma_commit(q_empty + ib);  // this item's QK^T MMAs have read its Q buffer
+        g0 += n_tiles;
       }
     }
     __syncwarp();
@@ -377,19 +431,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int half = (warp - 2) >> 2;         // key-column half of every S tile
     const int row = q4 * 32 + lane;           // query row within the tile
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const int grow = q0 + row;
     const float sl2 = a.scale_log2;
     const int pair_bar = 1 + q4;              // named barrier of the two warps of quarter q4
+    int g0 = 0;                               // key tiles of earlier items (S-buffer position)
+    for (int it = blockIdx.x, k = 0; it < n_items; it += gridDim.x, ++k) {
+    const Item im = item_of(a, it, n_total);
+    const int head = im.head, split = im.split, t0 = im.t0, n_tiles = im.n_tiles;
+    const int grow = im.q0 + row;
     float m_run = -INFINITY;                  // running max used for exponents (log2 units)
     float l_half = 0.f;                       // denominator over this warp's columns
     float m_exact = -INFINITY;                // true running max (partial-stats output)
     const uint8_t* mrow = (a.mask != nullptr && grow < a.n_q) ? a.mask + (int64_t)grow * a.mask_ld
                                                               : nullptr;
     for (int j = 0; j < n_tiles; ++j) {
-      const int b = j % NB;
+      const int gj = g0 + j;
+      const int b = gj % NB;
       const Tile t = tile_of(a, t0 + j, n0);
       const int c0 = half * HALF;  // first key column of this warp
-      mbar_wait(s_full + b, (j / NB) & 1);
+      mbar_wait(s_full + b, (gj / NB) & 1);
       tc_fence_after();
       float sv[HALF];
 #pragma unroll
@@ -472,7 +531,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // tcgen05.ld/st are warp-collective: rescale if any row of this warp needs it
       if (__any_sync(0xffffffffu, rescale_o)) {  // O_half *= alpha once PV_{j-1} landed
         const float f = rescale_o ? alpha : 1.f;
-        const int jp = j - 1;
+        const int jp = gj - 1;
         mbar_wait(pv_done + (jp % NB), (jp / NB) & 1);
         tc_fence_after();
 #pragma unroll 1
@@ -500,10 +559,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     // ---------------- epilogue: O / l -> bf16 -> global (this warp's half of O) --------
     if (n_tiles > 0) {
-      const int jl = n_tiles - 1;
+      const int jl = g0 + n_tiles - 1;
       mbar_wait(pv_done + (jl % NB), (jl / NB) & 1);
       tc_fence_after();
     }
+    g0 += n_tiles;
     // merge the two key halves' partials (attention.py:157-180): swap (max, denominator,
     // exact max) with the partner warp, then each warp stores half of the head dims
     float* me = red + half * 3 * BM;
@@ -524,33 +584,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __nv_bfloat16* orow =
         partial ? a.part_o + ((int64_t)split * a.n_q + grow) * a.part_ld + head * HD + half * (HD / 2)
                 : a.o + (int64_t)grow * a.o_ld + head * HD + half * (HD / 2);
-#pragma unroll 1
+    // read and merge all of this warp's O columns first, so the next item's first PV
+    // (waiting on o_free) is not held up by the global stores
+    uint32_t packed[HD / 64][16];
+#pragma unroll
     for (int c = 0; c < HD / 64; ++c) {
       uint32_t r0[32], r1[32];
       const uint32_t col = half * (HD / 2) + c * 32;
       tmem_ld32(tmem + lane_off + L::TM_O(0) + col, r0);
       tmem_ld32(tmem + lane_off + L::TM_O(1) + col, r1);
       tmem_wait_ld();
-      if (grow < a.n_q) {
 #pragma unroll
-        for (int v4 = 0; v4 < 4; ++v4) {
-          float o[8];
+      for (int i = 0; i < 16; ++i) {
+        // a half that saw no key has weight 0 and an undefined accumulator
+        float o2[2];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int i = v4 * 8 + e;
-            // a half that saw no key has weight 0 and an undefined accumulator
-            const float x0 = w_lo != 0.f ? __uint_as_float(r0[i]) * w_lo : 0.f;
-            const float x1 = w_hi != 0.f ? __uint_as_float(r1[i]) * w_hi : 0.f;
-            o[e] = x0 + x1;
-          }
-          uint4 w;
-          w.x = pack_bf16(o[0], o[1]);
-          w.y = pack_bf16(o[2], o[3]);
-          w.z = pack_bf16(o[4], o[5]);
-          w.w = pack_bf16(o[6], o[7]);
-          *reinterpret_cast<uint4*>(orow + c * 32 + v4 * 8) = w;
+        for (int e = 0; e < 2; ++e) {
+          const float x0 = w_lo != 0.f ? __uint_as_float(r0[2 * i + e]) * w_lo : 0.f;
+          const float x1 = w_hi != 0.f ? __uint_as_float(r1[2 * i + e]) * w_hi : 0.f;
+          o2[e] = x0 + x1;
         }
+        packed[c][i] = pack_bf16(o2[0], o2[1]);
       }
+    }
+    tc_fence_before();
+    mbar_arrive(o_free);  // O read: the next item's first PV may overwrite it
+    if (grow < a.n_q) {
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c)
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4)
+          *reinterpret_cast<uint4*>(orow + c * 32 + v4 * 8) =
+              make_uint4(packed[c][4 * v4], packed[c][4 * v4 + 1], packed[c][4 * v4 + 2],
+                         packed[c][4 * v4 + 3]);
     }
     if (partial && grow < a.n_q && half == 0) {  // K4 merges these (attention.py:157-173)
       const int64_t k = ((int64_t)split * a.heads + head) * a.n_q + grow;
@@ -563,6 +629,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const bool live = mx > -INFINITY;
       a.row_max[(int64_t)head * a.n_q + grow] = mx;
       a.row_sum[(int64_t)head * a.n_q + grow] = live ? den * ex2(M - mx) : 0.f;
+    }
+    named_sync(pair_bar, 64);  // the partner has read `red` before the next item rewrites it
     }
   }
 
@@ -624,7 +692,19 @@ int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
     }
     attr_set = true;
   }
-  dim3 grid((n_q + BM - 1) / BM, heads, a.n_splits);
+  // persistent CTAs: at most one per SM, each walking items blockIdx.x + i * gridDim.x
+  // (IFX_K1_GRID=items launches one CTA per item, the pre-persistent schedule, for A/B)
+  static int n_sm = 0;
+  static bool per_item = false;
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const char* env = std::getenv("IFX_K1_GRID");
+    per_item = env != nullptr && std::string(env) == "items";
+  }
+  const int64_t items = (int64_t)((n_q + BM - 1) / BM) * heads * a.n_splits;
+  const int grid = (int)(per_item || items < n_sm ? items : n_sm);
   fn<<<grid, NTHREADS, L::SMEM, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || a.n_splits == 1) return (int)e;
