@@ -99,6 +99,33 @@ def test_attention_large_scores_and_masks():
     assert (out.float() - ref).abs().max().item() < 3e-2
 
 
+@pytest.mark.parametrize("heads,n_q,n", [(5, 4680, 3000), (12, 2000, 1500)])
+def test_attention_persistent_items_rescale_and_mask(heads, n_q, n):
+    """More items than SMs (185 / 192 items on 148 persistent CTAs, uneven items per CTA):
+    every item restarts its online softmax and reuses the TMEM accumulators and S buffers
+    of the previous one; growing logits force O rescales inside each item."""
+    from paper_2511_20714_b200._device import attn_fwd
+
+    hd = 128
+    d = heads * hd
+    g = torch.Generator(device="cuda").manual_seed(heads * 7 + n)
+    q = (torch.randn(n_q, d, device="cuda", generator=g) * 2).bfloat16()
+    k = torch.randn(n, d, device="cuda", generator=g)
+    k = (k * torch.linspace(0.1, 2.5, n, device="cuda")[:, None]).bfloat16()
+    v = torch.randn(n, d, device="cuda", generator=g).bfloat16()
+    out = torch.empty(n_q, d, device="cuda", dtype=torch.bfloat16)
+    attn_fwd(q, heads, hd, out, k, v, 0, n)
+    torch.cuda.synchronize()
+    ref = _ref_attn(q, k, v, heads)
+    assert (out.float() - ref).abs().max().item() < 3e-2
+    mask = torch.rand(n_q, n, device="cuda", generator=g) < 0.5
+    mask[:, n // 2] = True
+    attn_fwd(q, heads, hd, out, k, v, 0, n, mask=mask.to(torch.uint8).contiguous())
+    torch.cuda.synchronize()
+    ref = _ref_attn(q, k, v, heads, mask=mask)
+    assert (out.float() - ref).abs().max().item() < 3e-2
+
+
 def _pool(kd, vd, hk, hv, w, page_len, dt):
     from paper_2511_20714_b200 import _abi
     p = _abi.KvPool()
