@@ -312,7 +312,7 @@ class _CrossFold:
     softmax_per_head(h (cq . K^T)) (V . co): cq . K^T is [D, H*n] and V . co is [H*n, D], so
     the two D x D projections around the attention (cq, co: 2 * 2*T*D*D FLOP per layer-pass)
     and the attention become two GEMMs of width H*n (3 * 12 = 36 at c2: 2 * 2*T*D*36) and a
-    group softmax. Same math, reassociated; built once per block from the cached prompt K/V
+    group softmax. Same math, reassociated; built from the cached prompt K/V when they change
     (fp32 einsum, bf16 GEMM operands, width padded to a multiple of 8 with zero columns)."""
 
     def __init__(self, model: "ToyModel", lw, k: torch.Tensor, v: torch.Tensor):
@@ -769,9 +769,16 @@ def _block_context(model: ToyModel, cache: KvCache | None, prompt_ctx, stager: _
     with cache.batch():
         ctx = _KvContext(model, cache, stager, passes)
         rngs = _touch_cross(model, cache)
-    cross = _gather_cross(cache, rngs) if rngs is not None else _cross_from_cache(model, None, prompt_ctx)
+    if rngs is None:
+        ctx.prepare()
+        return ctx, _fold_cross(model, _cross_from_cache(model, None, prompt_ctx))
+    # the prompt K/V only change with the cache's cross rows: blocks under one prompt reuse
+    # the fold (the fetch bookkeeping above still runs every block, as in the reference)
+    key = (id(model), cache.cross_version, tuple(rngs))
+    if cache.fold_memo is None or cache.fold_memo[0] != key:
+        cache.fold_memo = (key, _fold_cross(model, _gather_cross(cache, rngs)))
     ctx.prepare()
-    return ctx, _fold_cross(model, cross)
+    return ctx, cache.fold_memo[1]
 
 
 def _cross_from_cache(model: ToyModel, cache: KvCache | None, prompt_ctx):
@@ -929,6 +936,10 @@ class Engine:
         reserve = T * request.num_blocks
         if request.kv_window is not None:
             reserve = min(reserve, request.kv_window + 2 * T + c.block_len)
+        # the previous run's page table (~60k pages at c2) is torn down only once this run's
+        # first block is enqueued, so its ~7 ms of host frees overlap GPU work; its HBM
+        # pools go now (the cache object itself is dropped here)
+        retired = self.cache._pt if self.cache is not None else None
         self.cache = KvCache(self.kv_config, dtype=self.cache_dtype, reserve_tokens=reserve,
                              row_width=self.model.attn_width)
         with self._lock:
@@ -968,6 +979,7 @@ class Engine:
                                        to_host=to_host, _ready=ready)
                 if ready:
                     pending.append(ready[0])
+                retired = None
                 torch.cuda.nvtx.range_pop()
                 if span:
                     span.__exit__(None, None, None)

@@ -367,6 +367,10 @@ class KvCache:
                        CROSS_ATTN: _Pool(wc, dtype, config.page_len, cd, ch)}
         self.moved_pages = [0, 0]  # pages copied device->host, host->device (tier moves)
         self._batch = 0  # depth of open batch() contexts
+        # bumped by every call that can change cross-attention rows (append / clear / evict):
+        # the engine reuses its per-block fold of the prompt K/V while it is unchanged
+        self.cross_version = 0
+        self.fold_memo = None
         if reserve_tokens:
             per_layer = -(-reserve_tokens // config.page_len) + 1
             self._pools[SELF_ATTN].ensure(min(config.capacity_pages_device,
@@ -495,6 +499,8 @@ class KvCache:
             k, v = k.contiguous(), v.contiguous()
         with self._lock:
             self._no_batch("append_block")
+            if kind == CROSS_ATTN:
+                self.cross_version += 1
             rc, bid, start, written, pages = self._pt.append(layer, kind, t, chunk_index)
             self._sync(stream)
             if written > 0:  # rows already packed even if allocation then failed (kvcache.py:210-223)
@@ -522,12 +528,14 @@ class KvCache:
         """kvcache.py:258-285 (freed pages return their slots to the pools)."""
         with self._lock:
             self._no_batch("evict_window")
+            self.cross_version += 1
             return self._pt.evict_window(keep_last_n_tokens)
 
     def clear_cross_attention(self) -> int:
         """kvcache.py:287-299."""
         with self._lock:
             self._no_batch("clear_cross_attention")
+            self.cross_version += 1
             return self._pt.clear_cross()
 
     # -- reads ----------------------------------------------------------------------------

@@ -651,6 +651,7 @@ class UlyssesEngine:
         request.validate()
         m, c, r = self.model, self.model.config, self.runner
         T, n, rank = c.block_len, r.n, self.comm.rank
+        retired = self.cache._pt if self.cache is not None else None  # freed after block 0
         self.cache = KvCache(self.kv_config, dtype=torch.bfloat16,
                              reserve_tokens=T * request.num_blocks, row_width=r.wl,
                              cross_row_width=m.attn_width)
@@ -673,6 +674,7 @@ class UlyssesEngine:
                                                    non_blocking=True).clone()
             ctx, cross = _block_context(m, self.cache, None, r.stager, len(request.schedule.steps) + 1)
             r.denoise(lat, request.schedule, ctx, cross, self.cache, chunk)
+            retired = None
             if request.kv_window is not None:
                 self.cache.evict_window(request.kv_window)
             if gather:
