@@ -476,9 +476,11 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     tv, cap = runner._tv, runner._cap
     if ctx is not None:
         ctx.prepare()
-    if not runner._warm and len(steps) > 1:
+    if len(steps) > 1 and (not runner._warm or torch.cuda.current_stream().query()):
         # the runner's first pass runs eagerly: library state (cuBLASLt handle, workspace,
-        # per-shape algorithm choice in ifx_gemm_bf16) is set up outside any capture
+        # per-shape algorithm choice in ifx_gemm_bf16) is set up outside any capture. Also
+        # when the GPU is idle (first block after a sync): capturing first would leave it
+        # idle for the whole capture, eager launches start it at once
         torch.mul(m.time_vec, steps[0], out=tv)
         runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
         latent.add_(eps, alpha=-float(schedule.step_scale))

@@ -466,6 +466,7 @@ def test_graph_replayed_passes_equal_eager():
         try:
             eng = E.Engine(E.build_model(E.ModelConfig(**kw)))
             out[graphs] = (np.stack([b.latent for b in eng.generate(req)]), eng.cache.state())
+            assert (E._runner(eng.model)._graph is not None) == graphs  # graphs really ran
         finally:
             E.GRAPHS = True
     assert np.array_equal(out[True][0], out[False][0])

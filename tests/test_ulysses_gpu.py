@@ -121,6 +121,9 @@ def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad):
         assert ref_eng.cache.memory_stats().host_pages_used > 0
 
 
+GRAPH_STEPS = [1.0, 0.75, 0.5]
+
+
 def _rank_nccl(port, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -131,7 +134,8 @@ def _rank_nccl(port, q):
         from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
 
         eng = UlyssesEngine(E.ToyModel(E.ModelConfig(**CFG)), UlyssesComm())
-        lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
+        # 3 steps: a block's first pass may run eagerly (idle GPU), the rest are captured
+        lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule(GRAPH_STEPS), **REQ))
         q.put(([l.cpu().numpy() for l in lats], eng.cache.state(), eng.runner._graph is not None))
         eng.runner.release_graphs()
         torch.cuda.synchronize()
@@ -146,7 +150,7 @@ def test_ulysses_nccl_graph_capture_world1():
     from paper_2511_20714_b200 import engine as E
 
     ref_eng = E.Engine(E.build_model(E.ModelConfig(**CFG)))
-    ref = ref_eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
+    ref = ref_eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule(GRAPH_STEPS), **REQ))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     p = ctx.Process(target=_rank_nccl, args=(_free_port(), q))
