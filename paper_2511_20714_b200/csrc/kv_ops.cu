@@ -242,7 +242,8 @@ __global__ void rms_bf16_kernel(const float* __restrict__ x, int64_t rows, int64
        r += warps) {
     const float* xr = x + r * width;
     float ss = 0.f;
-    for (int64_t c = lane * 4; c < width; c += 128) {
+#pragma unroll 4  // several row loads in flight per warp
+    for (int c = lane * 4; c < (int)width; c += 128) {
       float4 v = *reinterpret_cast<const float4*>(xr + c);
       if (tvec) {
         const float4 tv = *reinterpret_cast<const float4*>(tvec + c);
@@ -253,7 +254,8 @@ __global__ void rms_bf16_kernel(const float* __restrict__ x, int64_t rows, int64
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     const float inv = rsqrtf(ss / (float)width + 1e-6f);
-    for (int64_t c = lane * 4; c < width; c += 128) {
+#pragma unroll 4
+    for (int c = lane * 4; c < (int)width; c += 128) {
       float4 v = *reinterpret_cast<const float4*>(xr + c);
       if (tvec) {
         const float4 tv = *reinterpret_cast<const float4*>(tvec + c);
@@ -264,6 +266,53 @@ __global__ void rms_bf16_kernel(const float* __restrict__ x, int64_t rows, int64
       o.x = f2_to_bf2(v.x * inv, v.y * inv);
       o.y = f2_to_bf2(v.z * inv, v.w * inv);
       *reinterpret_cast<uint2*>(y + r * width + c) = o;
+    }
+  }
+}
+
+// One CTA of kRmsThreads per row, the row held in registers (x read once): rows up to
+// kRmsThreads * 4 * VPT floats. Block reduction of the sum of squares through shared memory.
+template <int kRmsThreads, int VPT>
+__global__ void __launch_bounds__(kRmsThreads) rms_row_kernel(
+    const float* __restrict__ x, int64_t rows, int width, const float* __restrict__ tvec, float t,
+    float* __restrict__ x_out, __nv_bfloat16* __restrict__ y) {
+  __shared__ float part[kRmsThreads / 32];
+  const int tid = threadIdx.x;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float* xr = x + r * width;
+    float4 v[VPT];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int c = (tid + i * kRmsThreads) * 4;
+      if (c < width) {
+        v[i] = *reinterpret_cast<const float4*>(xr + c);
+        if (tvec) {
+          const float4 tv = *reinterpret_cast<const float4*>(tvec + c);
+          v[i].x += t * tv.x; v[i].y += t * tv.y; v[i].z += t * tv.z; v[i].w += t * tv.w;
+        }
+        ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((tid & 31) == 0) part[tid >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < kRmsThreads / 32; ++w) tot += part[w];
+    __syncthreads();  // part is rewritten by the next row
+    const float inv = rsqrtf(tot / (float)width + 1e-6f);
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int c = (tid + i * kRmsThreads) * 4;
+      if (c < width) {
+        if (tvec && x_out) *reinterpret_cast<float4*>(x_out + r * width + c) = v[i];
+        uint2 o;
+        o.x = f2_to_bf2(v[i].x * inv, v[i].y * inv);
+        o.y = f2_to_bf2(v[i].z * inv, v[i].w * inv);
+        *reinterpret_cast<uint2*>(y + r * width + c) = o;
+      }
     }
   }
 }
@@ -447,11 +496,24 @@ int group_softmax_launch(const float* s, int64_t rows, int groups, int gs, int64
 
 int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
                float* x_out, void* y, cudaStream_t st) {
+  auto* yb = static_cast<__nv_bfloat16*>(y);
+  const int64_t v128 = (width / 4 + 127) / 128;  // float4 per thread at 128 threads
+  const int gr = (int)(rows < (int64_t)kSMs * 64 ? rows : (int64_t)kSMs * 64);
+  if (v128 <= 24 && gr > 0) {  // wider rows: the warp-per-row kernel (two passes)
+    if (v128 <= 3)
+      rms_row_kernel<128, 3><<<gr, 128, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
+    else if (v128 <= 6)
+      rms_row_kernel<128, 6><<<gr, 128, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
+    else if (v128 <= 12)  // e.g. 5,120 (Wan-14B): 256 threads x 5 vectors
+      rms_row_kernel<256, 6><<<gr, 256, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
+    else
+      rms_row_kernel<512, 6><<<gr, 512, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
+    return (int)cudaGetLastError();
+  }
   const int threads = 256;
   const int64_t blocks = (rows + 7) / 8;
   const int g = (int)(blocks < (int64_t)kSMs * 16 ? blocks : (int64_t)kSMs * 16);
-  rms_bf16_kernel<<<g, threads, 0, st>>>(x, rows, width, tvec, t, x_out,
-                                         static_cast<__nv_bfloat16*>(y));
+  rms_bf16_kernel<<<g, threads, 0, st>>>(x, rows, width, tvec, t, x_out, yb);
   return (int)cudaGetLastError();
 }
 

@@ -266,18 +266,24 @@ def test_paged_attention_matches_torch(case):
     assert (out.float() - ref).abs().max().item() < 2e-2
 
 
-def test_rms_matches_torch():
+@pytest.mark.parametrize("width", [1536, 200, 5120])
+def test_rms_matches_torch(width):
+    """Rows up to 1,536 wide stay in registers (one read of x); wider rows take two passes."""
     from paper_2511_20714_b200._device import rms_bf16
 
-    x = torch.randn(777, 1536, device="cuda")
-    tv = torch.randn(1536, device="cuda")
-    y = torch.empty(777, 1536, device="cuda", dtype=torch.bfloat16)
+    x = torch.randn(777, width, device="cuda")
+    tv = torch.randn(width, device="cuda")
+    y = torch.empty(777, width, device="cuda", dtype=torch.bfloat16)
     xo = torch.empty_like(x)
     rms_bf16(x, y, tv, 0.75, xo)
     torch.cuda.synchronize()
     xc = x + 0.75 * tv
     ref = xc / torch.sqrt((xc * xc).mean(-1, keepdim=True) + 1e-6)
     assert torch.allclose(xo, xc, atol=1e-5)
+    assert (y.float() - ref).abs().max().item() < 2e-2
+    rms_bf16(x, y)  # no time conditioning
+    torch.cuda.synchronize()
+    ref = x / torch.sqrt((x * x).mean(-1, keepdim=True) + 1e-6)
     assert (y.float() - ref).abs().max().item() < 2e-2
 
 
