@@ -126,6 +126,26 @@ def test_attention_persistent_items_rescale_and_mask(heads, n_q, n):
     assert (out.float() - ref).abs().max().item() < 3e-2
 
 
+def test_attention_persistent_split_kv():
+    """5 heads x 37 query tiles under-fill 148 SMs, so the key range is split (4 ways here):
+    740 items, 5 per persistent CTA, each writing a partial merged by K4."""
+    from paper_2511_20714_b200._device import attn_fwd
+
+    heads, hd, n_q, n_ctx = 5, 128, 4680, 9000
+    d = heads * hd
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn(n_q, d, device="cuda", generator=g).bfloat16()
+    ks = (torch.randn(n_ctx, d, device="cuda", generator=g)
+          * torch.linspace(0.3, 1.8, n_ctx, device="cuda")[:, None]).bfloat16()
+    vs = torch.randn(n_ctx, d, device="cuda", generator=g).bfloat16()
+    qkv = torch.randn(n_q, 3 * d, device="cuda", generator=g).bfloat16()
+    out = torch.empty(n_q, d, device="cuda", dtype=torch.bfloat16)
+    attn_fwd(q, heads, hd, out, ks, vs, 0, n_ctx, qkv[:, d:2 * d], qkv[:, 2 * d:])
+    torch.cuda.synchronize()
+    ref = _ref_attn(q, torch.cat([ks, qkv[:, d:2 * d]]), torch.cat([vs, qkv[:, 2 * d:]]), heads)
+    assert (out.float() - ref).abs().max().item() < 2e-2
+
+
 def _pool(kd, vd, hk, hv, w, page_len, dt):
     from paper_2511_20714_b200 import _abi
     p = _abi.KvPool()
