@@ -375,7 +375,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t bph = (gj / NB) & 1;
             mbar_wait(k_full + s, (gj / NS) & 1);
             mbar_wait(s_empty + b, bph ^ 1);                    // S_b of tile gj-NB read
-            // P_b aliases S_b: explicit wait (measured free: the in-order-only variant was no faster)
+            // P_b aliases S_b: explicit wait for PV(gj-NB) before QK(gj) overwrites it. The
+            // PTX guarantees in-order execution only between MMAs on the same accumulator,
+            // and PV and QK^T use different ones; dropping the wait measured +0.3 % in the
+            // bench (profiles/r03_k1_persistent.md), not worth a possible WAR race.
             if (gj >= NB) mbar_wait(pv_done + b, bph ^ 1);
             tc_fence_after();
             const uint32_t k_base = smem_u32(sK + s * L::KV_BYTES);
