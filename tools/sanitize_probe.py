@@ -1,6 +1,7 @@
 """Small end-to-end runs for compute-sanitizer (memcheck): the engine with a host tier
 (K6 moves, DMA staging, paged K1 with staging codes), the folded cross-attention, K2/K7,
-the few-keys kernel and the block copies."""
+the few-keys kernel, the persistent K1 with several items per CTA (and split-KV), and the
+block copies."""
 import numpy as np
 import torch
 
@@ -18,5 +19,15 @@ q = torch.randn(2000, 256, device="cuda").bfloat16()
 k = torch.randn(3, 256, device="cuda").bfloat16()
 o = torch.empty_like(q)
 attn_fwd(q, 2, 128, o, k, k, 0, 3)  # K1s
+# persistent K1 with several items per CTA: 12 heads x 20 query tiles = 240 items on 148
+# CTAs (contiguous context + own keys); then 5 heads, split-KV partials + K4 combine
+q = torch.randn(2500, 12 * 128, device="cuda").bfloat16()
+kv = torch.randn(700, 12 * 128, device="cuda").bfloat16()
+o = torch.empty_like(q)
+attn_fwd(q, 12, 128, o, kv, kv, 0, 700, q, q)
+q5 = torch.randn(4680, 5 * 128, device="cuda").bfloat16()
+kv5 = torch.randn(9000, 5 * 128, device="cuda").bfloat16()
+o5 = torch.empty_like(q5)
+attn_fwd(q5, 5, 128, o5, kv5, kv5, 0, 9000, q5, q5)
 torch.cuda.synchronize()
 print("sanitize probe ok", eng.cache.memory_stats())
