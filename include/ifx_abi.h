@@ -156,6 +156,10 @@ int ifx_kv_copy_runs(const ifx_kv_pool* pool, const int64_t* runs, int64_t n, in
  * the device address equals the host address) for the host pools */
 int ifx_host_alloc(int64_t bytes, void** out);
 int ifx_host_free(void* p);
+/* Device buffers outside the caller's caching allocator (the host-tier staging buffers:
+ * tens of GB allocated and grown rarely; cudaFree synchronises the device). */
+int ifx_dev_alloc(int64_t bytes, void** out);
+int ifx_dev_free(void* p);
 
 /* =====================================================================================
  * K1 — fused attention of a block's queries over [cached context ∥ the block's own K/V]

@@ -41,6 +41,7 @@ EXPORTS = (
     "ifx_pt_stats", "ifx_pt_snapshot", "ifx_pt_drain_moves", "ifx_pt_pool_extent", "ifx_pt_slots",
     "ifx_pt_batch_begin", "ifx_pt_batch_end", "ifx_pt_pending",
     "ifx_kv_append", "ifx_kv_gather", "ifx_kv_move_pages", "ifx_kv_copy_runs", "ifx_host_alloc", "ifx_host_free",
+    "ifx_dev_alloc", "ifx_dev_free",
     "ifx_attn_fwd", "ifx_attn_workspace_bytes",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_group_softmax", "ifx_ulysses_pack", "ifx_ulysses_unpack",
     "ifx_copy_blocks", "ifx_gemm_bf16",
@@ -125,6 +126,8 @@ def lib() -> ctypes.CDLL:
             L.ifx_kv_copy_runs.argtypes = [PPOOL, PI64, I64, ctypes.c_int, P]
             L.ifx_host_alloc.argtypes = [I64, ctypes.POINTER(P)]
             L.ifx_host_free.argtypes = [P]
+            L.ifx_dev_alloc.argtypes = [I64, ctypes.POINTER(P)]
+            L.ifx_dev_free.argtypes = [P]
             L.ifx_attn_fwd.argtypes = [ctypes.POINTER(AttnParams), P]
             L.ifx_attn_workspace_bytes.argtypes = [ctypes.POINTER(AttnParams), PI64]
             L.ifx_rms_bf16.argtypes = [P, I64, I64, P, ctypes.c_float, P, P, P]

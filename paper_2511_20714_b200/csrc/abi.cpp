@@ -327,6 +327,17 @@ int ifx_host_free(void* p) {
   return ifx::cuda_fail((int)cudaFreeHost(p), "cudaFreeHost");
 }
 
+int ifx_dev_alloc(int64_t bytes, void** out) {
+  *out = nullptr;
+  if (bytes <= 0) return IFX_OK;
+  return ifx::cuda_fail((int)cudaMalloc(out, (size_t)bytes), "cudaMalloc");
+}
+
+int ifx_dev_free(void* p) {
+  if (p == nullptr) return IFX_OK;
+  return ifx::cuda_fail((int)cudaFree(p), "cudaFree");
+}
+
 int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
                  float* x_out, void* y, void* stream) {
   if (rows < 0 || width <= 0 || width % 4) return ifx::fail(IFX_EDIM, "rms width must be a multiple of 4");

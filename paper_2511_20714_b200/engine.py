@@ -525,6 +525,31 @@ PAGED_K1_PAGE_LENS = (8, 16, 32, 64, 128)  # page boxes that tile K1's 128-key t
 MAX_DMA_RUNS = 256  # staging of a layer with more slot runs goes through K6 instead
 
 
+class _DevBuf:
+    """A device buffer from ifx_dev_alloc (outside torch's caching allocator), exposed as a
+    tensor through __cuda_array_interface__; freed when the last view is gone."""
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _abi.check(_abi.lib().ifx_dev_alloc(int(nbytes), ctypes.byref(p)), "dev_alloc")
+        self.ptr, self.nbytes = p.value or 0, int(nbytes)
+        self.__cuda_array_interface__ = {"shape": (self.nbytes,), "typestr": "|u1",
+                                         "data": (self.ptr, False), "version": 3,
+                                         "strides": None}
+
+    def view(self, rows: int, width: int, dtype) -> torch.Tensor:
+        t = torch.as_tensor(self, device=require_cuda())  # keeps self alive
+        return t.view(dtype)[:rows * width].view(rows, width)
+
+    def __del__(self):
+        if getattr(self, "ptr", 0):
+            try:
+                _abi.lib().ifx_dev_free(ctypes.c_void_p(self.ptr))
+            except Exception:  # interpreter shutdown
+                pass
+            self.ptr = 0
+
+
 class _Stager:
     """HBM staging buffers for host-tier context pages (one per runner, reused by blocks).
 
@@ -551,9 +576,23 @@ class _Stager:
                 and self.k.dtype == dtype:
             return
         self.copy.synchronize()  # no staging copy may still write the old buffers
+        if self.k is not None and self.k.shape[1] == width and self.k.dtype == dtype:
+            # geometric growth capped at the budget: the host tier grows every block, and
+            # re-allocating tens of GB per block would dominate the step
+            esz = torch.finfo(dtype).bits // 8
+            cap = max(rows, self.budget // (width * esz) // page_len * page_len)
+            rows = min(cap, max(rows, -(-self.k.shape[0] * 9 // 8 // page_len) * page_len))
         self.k = self.v = None
-        self.k = torch.zeros(rows, width, device=self.dev, dtype=dtype)
-        self.v = torch.zeros_like(self.k)
+        # staging takes what HBM the device tier leaves (c5: 2 x 23 GB next to a 115 GB
+        # pool). Its buffers bypass torch's caching allocator (ifx_dev_alloc), so a freed
+        # one goes back to the driver instead of being carved up by later small tensors;
+        # segments torch keeps reserved are handed back first. Rare (first block, growth).
+        torch.cuda.empty_cache()
+        esz = torch.finfo(dtype).bits // 8
+        self.k = _DevBuf(rows * width * esz).view(rows, width, dtype)
+        self.v = _DevBuf(rows * width * esz).view(rows, width, dtype)
+        self.k.zero_()
+        self.v.zero_()
 
 
 class _KvContext:
