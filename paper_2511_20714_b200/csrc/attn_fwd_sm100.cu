@@ -446,10 +446,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     float m_exact = -INFINITY;                // true running max (partial-stats output)
     const uint8_t* mrow = (a.mask != nullptr && grow < a.n_q) ? a.mask + (int64_t)grow * a.mask_ld
                                                               : nullptr;
+    // the only tiles with invisible keys: a window start inside the first context tile,
+    // and the ragged last tile of each segment (everything else skips the masking)
+    const int part0 = (n0 > 0 && a.ctx_lo > 0) ? 0 : -1;
+    const int part1 = (a.n_ctx % BN) ? n0 - 1 : -1;
+    const int part2 = (a.n_cur % BN) ? n_total - 1 : -1;
     for (int j = 0; j < n_tiles; ++j) {
       const int gj = g0 + j;
       const int b = gj % NB;
-      const Tile t = tile_of(a, t0 + j, n0);
+      const int jt = t0 + j;
       const int c0 = half * HALF;  // first key column of this warp
       mbar_wait(s_full + b, (gj / NB) & 1);
       tc_fence_after();
@@ -465,8 +470,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_before();
       mbar_arrive(s_empty + b);
 
-      const bool full = (t.valid == BN) && t.lo == 0 && mrow == nullptr;
+      const bool full = mrow == nullptr && jt != part0 && jt != part1 && jt != part2;
       if (!full) {
+        const Tile t = tile_of(a, jt, n0);
 #pragma unroll
         for (int i = 0; i < HALF; ++i) {
           bool ok = c0 + i < t.valid && c0 + i >= t.lo;
