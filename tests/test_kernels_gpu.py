@@ -328,16 +328,6 @@ def test_ulysses_pack_unpack_roundtrip(groups):
     assert torch.equal(back, x[:, :width])
 
 
-def test_addmm_out_dtype_fp32_residual():
-    """The engine keeps the residual stream fp32 with bf16 GEMM inputs."""
-    a = torch.randn(64, 128, device="cuda").bfloat16()
-    b = torch.randn(128, 32, device="cuda").bfloat16()
-    x = torch.randn(64, 32, device="cuda")
-    y = torch.mm(a, b, out_dtype=torch.float32)
-    assert y.dtype == torch.float32
-    assert torch.allclose(y, a.float() @ b.float(), atol=1e-3)
-
-
 @pytest.mark.gpu
 @pytest.mark.parametrize("M,N,K", [(4680, 4608, 1536), (4680, 1536, 3072), (77, 96, 64)])
 def test_gemm_lt_matches_torch(M, N, K):
