@@ -25,6 +25,7 @@ import hashlib
 import math
 import os
 import threading
+import weakref
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Callable
@@ -393,6 +394,7 @@ class BlockRunner:
         self._eps = None
         self._tv = self._gpool = self._cap = self._graph = None  # CUDA-graph state (_euler_steps)
         self._warm = False
+        self._tail = None  # event after the last block's clean pass (_euler_steps: GPU idle?)
 
     def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
                 collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None,
@@ -447,9 +449,12 @@ class BlockRunner:
             self._eps = self.ws.tmp.new_empty(self.ws.tmp.shape)
         eps = self._eps
         rope = rope_tables(self.model.config, chunk_index, self.dev)
-        _euler_steps(self, latent, schedule, ctx, cross, cache, eps, rope)
+        _euler_steps(self, latent, schedule, ctx, cross, cache, eps, rope,
+                     first_block=chunk_index == 0)
         self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
                      chunk_index=chunk_index, rope=rope)
+        self._tail = torch.cuda.Event()
+        self._tail.record()
         return latent
 
 
@@ -457,7 +462,7 @@ GRAPHS = os.environ.get("IFX_CUDA_GRAPHS", "1") != "0"
 
 
 def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, eps, rope,
-                 graphs_ok: bool = True) -> None:
+                 graphs_ok: bool = True, first_block: bool = False) -> None:
     """The S denoise passes of a block (engine.py:299-301). Within a block every pass
     launches the same kernels on the same buffers with the same context, only t differs:
     the first pass is captured once as a CUDA graph (t*time_vec read from a device buffer)
@@ -476,18 +481,22 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     tv, cap = runner._tv, runner._cap
     if ctx is not None:
         ctx.prepare()
-    if len(steps) > 1 and (not runner._warm or torch.cuda.current_stream().query()):
+    if len(steps) > 1 and not runner._warm:
         # the runner's first pass runs eagerly: library state (cuBLASLt handle, workspace,
-        # per-shape algorithm choice in ifx_gemm_bf16) is set up outside any capture. Also
-        # when the GPU is idle (first block after a sync): capturing first would leave it
-        # idle for the whole capture, eager launches start it at once
+        # per-shape algorithm choice in ifx_gemm_bf16) is set up outside any capture
         torch.mul(m.time_vec, steps[0], out=tv)
         runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
         latent.add_(eps, alpha=-float(schedule.step_scale))
         runner._warm = True
         steps = steps[1:]
+    # the first block of a run on a drained GPU runs eagerly: a capture would leave the GPU
+    # idle for its whole duration (in steady state it overlaps the previous block's clean
+    # pass; a host-bound Ulysses rank keeps capturing every later block)
+    eager_block = first_block and (runner._tail is None or runner._tail.query())
     use = (GRAPHS and graphs_ok and len(steps) > 1 and runner.attn_events is None
-           and (ctx is None or (ctx.paged and not ctx.jobs)))
+           and not eager_block and (ctx is None or (ctx.paged and not ctx.jobs)))
+    if use and isinstance(cross, _LazyFold):
+        cross.materialize()  # fold ops (and their allocations) must not enter the graph
     if not use:
         for t in steps:
             torch.mul(m.time_vec, t, out=tv)
@@ -790,6 +799,35 @@ def _touch_cross(model: ToyModel, cache: KvCache | None):
     return rngs
 
 
+class _LazyFold:
+    """Per-layer _CrossFold of the cached prompt K/V, built on first use: the first pass of
+    a run folds layer l right before layer l's cross-attention, so those small host-bound
+    ops interleave with GPU work instead of running while the GPU waits (block 0).
+    `materialize()` builds the rest before a CUDA-graph capture (no fold may be captured)."""
+
+    def __init__(self, model: "ToyModel", cache: KvCache, rngs):
+        # weak: the cache holds this object (fold_memo); a cycle would keep a replaced
+        # cache's HBM pools alive until the next full garbage collection
+        self.model, self.cache_ref, self.rngs = model, weakref.ref(cache), rngs
+        self.folds = [None] * len(rngs)
+
+    def __len__(self):
+        return len(self.folds)
+
+    def __getitem__(self, li: int) -> _CrossFold:
+        f = self.folds[li]
+        if f is None:
+            a, b = self.rngs[li]
+            k, v = self.cache_ref()._gather(li, CROSS_ATTN, None, a, b - a, a, b, raw=True)
+            f = self.folds[li] = _CrossFold(self.model, self.model.layers[li], k, v)
+        return f
+
+    def materialize(self) -> "_LazyFold":
+        for li in range(len(self.folds)):
+            self[li]
+        return self
+
+
 def _gather_cross(cache: KvCache, rngs):
     """Per layer the prompt K/V rows, gathered (K7) into a contiguous buffer (a few rows;
     pages may sit on either tier)."""
@@ -817,7 +855,7 @@ def _block_context(model: ToyModel, cache: KvCache | None, prompt_ctx, stager: _
     # the fold (the fetch bookkeeping above still runs every block, as in the reference)
     key = (id(model), cache.cross_version, tuple(rngs))
     if cache.fold_memo is None or cache.fold_memo[0] != key:
-        cache.fold_memo = (key, _fold_cross(model, _gather_cross(cache, rngs)))
+        cache.fold_memo = (key, _LazyFold(model, cache, rngs))
     ctx.prepare()
     return ctx, cache.fold_memo[1]
 

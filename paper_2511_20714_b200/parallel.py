@@ -530,6 +530,7 @@ class UlyssesRunner:
         self.stager = _Stager(dev)
         self._tv = self._gpool = self._cap = self._graph = None  # CUDA-graph state (_euler_steps)
         self._warm = False
+        self._tail = None  # event after the last block's clean pass (_euler_steps: GPU idle?)
 
     def _balanced_attention(self, li, ctx, sc, ev):
         """BalancedPlan: re-shard (one all-to-all), one K1 per segment (a head's query rows,
@@ -622,9 +623,12 @@ class UlyssesRunner:
         # graph capture needs the all-to-alls on the GPU stream: NCCL only (a gloo group
         # stages them through the host)
         nccl = self.comm.dist.get_backend(self.comm.group) == "nccl"
-        _euler_steps(self, latent, schedule, ctx, cross, cache, self.eps, rope, graphs_ok=nccl)
+        _euler_steps(self, latent, schedule, ctx, cross, cache, self.eps, rope, graphs_ok=nccl,
+                     first_block=chunk_index == 0)
         self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
                      chunk_index=chunk_index, rope=rope)
+        self._tail = torch.cuda.Event()
+        self._tail.record()
         return latent
 
     def release_graphs(self) -> None:
