@@ -102,9 +102,12 @@ extern "C" int ifx_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
                                          sizeof(al_d));
     cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_D_BYTES, &al_d,
                                          sizeof(al_d));
-    std::vector<cublasLtMatmulHeuristicResult_t> res(8);
+#ifndef IFX_LT_CANDIDATES
+#define IFX_LT_CANDIDATES 8
+#endif
+    std::vector<cublasLtMatmulHeuristicResult_t> res(IFX_LT_CANDIDATES);
     int got = 0;
-    int s = cublasLtMatmulAlgoGetHeuristic(L.h, p.op, p.la, p.lb, p.lc, p.lc, pref, 8, res.data(), &got);
+    int s = cublasLtMatmulAlgoGetHeuristic(L.h, p.op, p.la, p.lb, p.lc, p.lc, pref, IFX_LT_CANDIDATES, res.data(), &got);
     cublasLtMatmulPreferenceDestroy(pref);
     if (s || got == 0) return lt_fail("cublasLtMatmulAlgoGetHeuristic", s);
     p.algo = res[0].algo;
