@@ -479,8 +479,8 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
         roll()
     torch.cuda.synchronize()
     dist.barrier()
-    # K1 roofline from one extra rollout with per-launch CUDA events (these force the eager
-    # path); the timed region below runs as in production (denoise passes as CUDA graphs)
+    # K1 roofline from one extra rollout with per-launch CUDA events (external event nodes
+    # inside the pass graphs); the timed region below runs without them
     eng.runner.attn_events = []
     roll()
     torch.cuda.synchronize()

@@ -33,7 +33,7 @@ from typing import Callable
 import numpy as np
 import torch
 
-from . import _abi
+from . import _abi, _device
 from ._device import (attn_fwd, count_launch, gemm, require_cuda, rms_bf16, rope_qk,
                       stream_ptr, tile_run_codes)
 from .errors import ConfigError, DimensionError
@@ -419,14 +419,14 @@ class BlockRunner:
                 rope_qk(ws.qkv, H, dhp, c.head_dim // 2, 0, Dp, rope[0], rope[1])
             ev = self.attn_events
             if ev is not None:
-                e0 = torch.cuda.Event(enable_timing=True)
+                e0 = timing_event()
                 e0.record()
             if ctx is not None:
                 ctx.attend(li, q, H, dhp, ws.attn, kc, vc, sc)
             else:
                 attn_fwd(q, H, dhp, ws.attn, cur_k=kc, cur_v=vc, scale=sc)
             if ev is not None:
-                e1 = torch.cuda.Event(enable_timing=True)
+                e1 = timing_event()
                 e1.record()
                 ev.append((e0, e1))
             _residual(ws.x, ws.attn, lw.wo, ws.tmp)
@@ -461,6 +461,13 @@ class BlockRunner:
 GRAPHS = os.environ.get("IFX_CUDA_GRAPHS", "1") != "0"
 
 
+def timing_event() -> torch.cuda.Event:
+    """A timing event for K1 launch windows; inside a CUDA-graph capture it is recorded as
+    an external event node, so every replay re-records it (read after the last replay)."""
+    return torch.cuda.Event(enable_timing=True,
+                            external=torch.cuda.is_current_stream_capturing())
+
+
 def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, eps, rope,
                  graphs_ok: bool = True, first_block: bool = False) -> None:
     """The S denoise passes of a block (engine.py:299-301). Within a block every pass
@@ -493,8 +500,8 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     # idle for its whole duration (in steady state it overlaps the previous block's clean
     # pass; a host-bound Ulysses rank keeps capturing every later block)
     eager_block = first_block and (runner._tail is None or runner._tail.query())
-    use = (GRAPHS and graphs_ok and len(steps) > 1 and runner.attn_events is None
-           and not eager_block and (ctx is None or (ctx.paged and not ctx.jobs)))
+    use = (GRAPHS and graphs_ok and len(steps) > 1 and not eager_block
+           and (ctx is None or (ctx.paged and not ctx.jobs)))
     if use and isinstance(cross, _LazyFold):
         cross.materialize()  # fold ops (and their allocations) must not enter the graph
     if not use:
@@ -503,6 +510,9 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
             runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
             latent.add_(eps, alpha=-float(schedule.step_scale))
         return
+    ev = runner.attn_events
+    n_ev = len(ev) if ev is not None else 0
+    n_launch = _device.LAUNCHES[0]
     g = torch.cuda.CUDAGraph()
     cap.wait_stream(torch.cuda.current_stream())
     try:
@@ -515,6 +525,9 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
                 g.capture_end()
     except RuntimeError as err:  # capture refused (driver / library): run eagerly from now on
         globals()["GRAPHS"] = False
+        if ev is not None:
+            del ev[n_ev:]  # events of the failed capture never complete
+        _device.LAUNCHES[0] = n_launch  # nor do its kernels
         import warnings
         warnings.warn(f"CUDA graph capture failed ({err}); denoise passes run eagerly")
         torch.cuda.current_stream().wait_stream(cap)
@@ -527,6 +540,10 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     for t in steps:
         torch.mul(m.time_vec, t, out=tv)
         g.replay()
+    if ev is not None:  # the captured K1 windows hold the last replay's times: one entry
+        ev.extend(ev[n_ev:] * (len(steps) - 1))  # per replayed launch (same context each pass)
+    # our kernels in the graph run once per replay (the launch counter saw the capture)
+    _device.LAUNCHES[0] += (_device.LAUNCHES[0] - n_launch) * (len(steps) - 1)
     runner._graph = g  # kept until the next block (its kernels may still be running)
 
 

@@ -545,7 +545,8 @@ class UlyssesRunner:
         kc, vc = kv[0], kv[1]
         qreg = self.b_region[:pl.qr * dhp].view(pl.qr, dhp)
         if ev is not None:
-            e0 = torch.cuda.Event(enable_timing=True)
+            from .engine import timing_event
+            e0 = timing_event()
             e0.record()
         last = len(pl.segs) - 1
         for si, (h, r0, r1) in enumerate(pl.segs):
@@ -555,7 +556,7 @@ class UlyssesRunner:
             ctx.attend(li, qreg[b:b + m], 1, dhp, self.b_o[b:b + m], kc[:, c0:c1], vc[:, c0:c1], sc,
                        attn=self._attn, cols=(c0, c1), first=si == 0, last=si == last)
         if ev is not None:
-            e1 = torch.cuda.Event(enable_timing=True)
+            e1 = timing_event()
             e1.record()
             ev.append((e0, e1))
         _copy_blocks(self.b_o, self.b_osend, pl.opack)
@@ -570,7 +571,7 @@ class UlyssesRunner:
     def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None,
                 rope=None):
         from ._device import gemm
-        from .engine import _cross_attend, _ffn_up, _residual
+        from .engine import _cross_attend, _ffn_up, _residual, timing_event
         from .kvcache import SELF_ATTN
         m = self.model
         c = m.config
@@ -594,11 +595,11 @@ class UlyssesRunner:
                 qkv_h = self.comm.seq_to_head(self.qkv, 3)          # [T, 3*wl] local heads
                 q, kc, vc = qkv_h[:, :wl], qkv_h[:, wl:2 * wl], qkv_h[:, 2 * wl:]
                 if ev is not None:
-                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0 = timing_event()
                     e0.record()
                 ctx.attend(li, q, self.hl, dhp, self.attn_h, kc, vc, sc, attn=self._attn)
                 if ev is not None:
-                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1 = timing_event()
                     e1.record()
                     ev.append((e0, e1))
                 self.comm.head_to_seq(self.attn_h, self.attn_s)      # [n, Dp]
