@@ -93,7 +93,8 @@ int ifx_pt_snapshot(const ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t*
 /* Drain the logged page moves as records of 5 int64 (epoch, kind, dir, device slot, host
  * slot); dir 0 = device -> host, 1 = host -> device. Records are in execution order: per
  * logging call, all dir-0 moves then all dir-1 moves (each group is hazard-free, so it is
- * one ifx_kv_move_pages launch). out == NULL: only *n_records is set, nothing drained. */
+ * one ifx_kv_move_pages launch). out == NULL: only *n_records is set, nothing drained.
+ * Fails with IFX_ECONFIG while a batch is open (its pages still index the move log). */
 int ifx_pt_drain_moves(ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* n_records);
 /* Group the following calls into one move batch (one epoch): a page restored by one call
  * and demoted again by a later one before the drain (the LRU churn of fetching a whole

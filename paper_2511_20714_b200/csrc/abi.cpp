@@ -13,6 +13,7 @@
 #include "../../include/ifx_abi.h"
 #include "attn_kernel.h"
 #include "common_host.h"
+#include "device_state.h"
 #include "kv_kernels.h"
 
 namespace ifx {
@@ -174,15 +175,10 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   return cuda_fail(e, "attn_fwd launch");
 }
 
-int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
-      n = 148;
-  }
-  return n;
+int num_sms() {  // of the CURRENT device (a process may drive several)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return device_sms(dev);
 }
 
 int64_t split_workspace_bytes(const ifx_attn_params* p, int splits) {

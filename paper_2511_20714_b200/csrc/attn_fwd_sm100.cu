@@ -39,6 +39,7 @@
 #include <string>
 
 #include "attn_kernel.h"
+#include "device_state.h"
 #include "sm100_ptx.cuh"
 
 namespace ifx {
@@ -693,32 +694,29 @@ template <int HD>
 int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
   using L = Layout<HD>;
   auto* fn = a.ctx_slots != nullptr ? attn_fwd_kernel<HD, true> : attn_fwd_kernel<HD, false>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceFlags attr_set;  // the smem attribute is per device context
+  const int dev = current_device();
+  if (attr_set.first(dev)) {
     for (auto* f : {attn_fwd_kernel<HD, true>, attn_fwd_kernel<HD, false>}) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
       if (e != cudaSuccess) return (int)e;
     }
-    attr_set = true;
+    attr_set.set(dev);
   }
   // persistent CTAs: at most one per SM, each walking items blockIdx.x + i * gridDim.x
   // (IFX_K1_GRID=items launches one CTA per item, the pre-persistent schedule, for A/B)
-  static int n_sm = 0;
-  static bool per_item = false;
-  if (n_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int n_sm = device_sms(dev);
+  static const bool per_item = [] {
     const char* env = std::getenv("IFX_K1_GRID");
-    per_item = env != nullptr && std::string(env) == "items";
-  }
+    return env != nullptr && std::string(env) == "items";
+  }();
   const int64_t items = (int64_t)((n_q + BM - 1) / BM) * heads * a.n_splits;
   const int grid = (int)(per_item || items < n_sm ? items : n_sm);
   fn<<<grid, NTHREADS, L::SMEM, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || a.n_splits == 1) return (int)e;
   const int64_t warps = (int64_t)n_q * heads;
-  const int blocks = (int)((warps + 7) / 8 < 148 * 16 ? (warps + 7) / 8 : 148 * 16);
+  const int blocks = (int)((warps + 7) / 8 < n_sm * 16 ? (warps + 7) / 8 : n_sm * 16);
   attn_combine_kernel<HD><<<blocks, 256, 0, st>>>(a);
   return (int)cudaGetLastError();
 }

@@ -5,7 +5,9 @@
 // bf16. cuBLASLt's first heuristic is not always its fastest algorithm on these shapes
 // (tools/lt_algo_probe: w2 4680x1536x3072 runs 19 % faster with the 7th candidate), so the
 // first call of each shape outside a CUDA-graph capture times the top candidates on scratch
-// outputs and keeps the fastest; calls during a capture use the first heuristic until then.
+// outputs and keeps the fastest. A shape first seen inside a capture keeps the first
+// heuristic for good, so captured and later eager calls of one shape run the same algorithm
+// (bit-identical results). Handles, workspaces and plans are per device.
 #include <cublasLt.h>
 #include <cuda_runtime.h>
 
@@ -39,9 +41,11 @@ struct Lt {
   std::mutex mu;
 };
 
-Lt& lt() {
-  static Lt s;
-  return s;
+constexpr int kMaxDevices = 64;
+
+Lt& lt(int dev) {
+  static Lt s[kMaxDevices];
+  return s[dev];
 }
 
 int lt_fail(const char* what, int st) {
@@ -56,7 +60,10 @@ extern "C" int ifx_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
   if (M < 0 || N < 0 || K < 1 || lda < K || ldb < N || ldd < N)
     return ifx::fail(IFX_EDIM, "bad gemm sizes");
   if (M == 0 || N == 0) return IFX_OK;
-  Lt& L = lt();
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return ifx::fail(IFX_ECUDA, "gemm: no current CUDA device");
+  Lt& L = lt(dev);
   std::lock_guard<std::mutex> g(L.mu);
   auto st = static_cast<cudaStream_t>(stream);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -111,7 +118,8 @@ extern "C" int ifx_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
     cublasLtMatmulPreferenceDestroy(pref);
     if (s || got == 0) return lt_fail("cublasLtMatmulAlgoGetHeuristic", s);
     p.algo = res[0].algo;
-    if (cap == cudaStreamCaptureStatusNone && got > 1) {
+    if (cap != cudaStreamCaptureStatusNone || got == 1) p.tuned = true;  // frozen (see top)
+    if (!p.tuned) {
       // time the candidates on a scratch output (the real D may be the residual C)
       const size_t esz = d_type == IFX_F32 ? 4 : 2;
       void* scratch = nullptr;

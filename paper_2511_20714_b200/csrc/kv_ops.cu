@@ -7,12 +7,14 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "device_state.h"
 #include "kv_kernels.h"
 
 namespace ifx {
 namespace {
 
-constexpr int kSMs = 148;
+// grid caps scale with the SM count of the current device (148 on B200)
+inline int kSMs_now() { return ifx::device_sms(ifx::current_device()); }
 
 __device__ __forceinline__ uint4 ld_nc(const void* p) {
   uint4 r;
@@ -406,7 +408,7 @@ __global__ void group_softmax_kernel(const float* __restrict__ s, int64_t rows, 
 
 int grid_for(int64_t work, int threads) {
   int64_t blocks = (work + threads - 1) / threads;
-  const int64_t cap = (int64_t)kSMs * 8;
+  const int64_t cap = (int64_t)kSMs_now() * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   return (int)blocks;
@@ -432,14 +434,15 @@ int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf1
   } else if ((width * (pool_bf16 ? 2 : 4)) <= kBulkMaxRowBytes && !std::getenv("IFX_K2_SIMT")) {
     const int row_b = (int)(width * (pool_bf16 ? 2 : 4));
     const size_t smem = (size_t)16 * row_b;  // 8 warps x 2 buffers
-    static bool attr = false;
-    if (!attr) {
+    static DeviceFlags attr;  // per device context
+    const int dev = current_device();
+    if (attr.first(dev)) {
       cudaFuncSetAttribute(append_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            16 * kBulkMaxRowBytes);
-      attr = true;
+      attr.set(dev);
     }
     int blocks = (int)((2 * t + 7) / 8);
-    const int cap = kSMs * (row_b <= 4096 ? 4 : 1);
+    const int cap = kSMs_now() * (row_b <= 4096 ? 4 : 1);
     if (blocks > cap) blocks = cap;
     append_bulk<<<blocks, threads, smem, st>>>(static_cast<const uint8_t*>(ks),
                                                static_cast<const uint8_t*>(vs),
@@ -498,7 +501,7 @@ int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, f
                float* x_out, void* y, cudaStream_t st) {
   auto* yb = static_cast<__nv_bfloat16*>(y);
   const int64_t v128 = (width / 4 + 127) / 128;  // float4 per thread at 128 threads
-  const int gr = (int)(rows < (int64_t)kSMs * 64 ? rows : (int64_t)kSMs * 64);
+  const int gr = (int)(rows < (int64_t)kSMs_now() * 64 ? rows : (int64_t)kSMs_now() * 64);
   if (v128 <= 24 && gr > 0) {  // wider rows: the warp-per-row kernel (two passes)
     if (v128 <= 3)
       rms_row_kernel<128, 3><<<gr, 128, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
@@ -512,7 +515,7 @@ int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, f
   }
   const int threads = 256;
   const int64_t blocks = (rows + 7) / 8;
-  const int g = (int)(blocks < (int64_t)kSMs * 16 ? blocks : (int64_t)kSMs * 16);
+  const int g = (int)(blocks < (int64_t)kSMs_now() * 16 ? blocks : (int64_t)kSMs_now() * 16);
   rms_bf16_kernel<<<g, threads, 0, st>>>(x, rows, width, tvec, t, x_out, yb);
   return (int)cudaGetLastError();
 }

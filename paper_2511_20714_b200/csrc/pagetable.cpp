@@ -594,6 +594,9 @@ int ifx_pt_pending(const ifx_pagetable* pt, int64_t max_layer, int64_t* out3) {
 
 int ifx_pt_drain_moves(ifx_pagetable* pt, int64_t* out, int64_t cap, int64_t* n_records) {
   std::lock_guard<std::mutex> g(pt->mu);
+  // a drain clears the move log, but pages of an open batch still index it (pending):
+  // later restores / demotions of the batch would then retarget or cancel the wrong move
+  if (pt->batch_depth > 0) return ifx::fail(IFX_ECONFIG, "drain_moves inside an open batch");
   pt->finalize_epoch();
   std::vector<const Move*> live;
   for (const Move& m : pt->moves)

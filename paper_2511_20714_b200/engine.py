@@ -171,6 +171,72 @@ def _pad_rows(w: torch.Tensor, heads: int, heads_pad: int, dh: int, dhp: int) ->
     return out.view(heads_pad * dhp, w.shape[1])
 
 
+def _unpad_heads(x: torch.Tensor, heads: int, heads_pad: int, dh: int, dhp: int) -> torch.Tensor:
+    """[n, heads_pad*dhp] (engine layout) -> [n, heads*dh] fp32 (the reference's layout)."""
+    n = x.shape[0]
+    return x.reshape(n, heads_pad, dhp)[:, :heads, :dh].reshape(n, heads * dh).float()
+
+
+def _pad_heads(x: torch.Tensor, heads: int, heads_pad: int, dh: int, dhp: int, out: torch.Tensor):
+    """[n, heads*dh] -> out [n, heads_pad*dhp] (zero padding, out's dtype)."""
+    n = x.shape[0]
+    o = out.view(n, heads_pad, dhp)
+    if dh != dhp or heads != heads_pad:
+        o.zero_()
+    o[:, :heads, :dh] = torch.as_tensor(x, device=out.device).reshape(n, heads, dh)
+    return out
+
+
+def _mha(q, k, v, heads: int, mask):
+    """engine.py:176-182 — the attention-processor hook: per head h, scaled_dot_attention
+    of columns h*dh:(h+1)*dh of q [T, D] over k / v [m, D] under mask [T, m], concatenated
+    to [T, D]. Here all heads run in ONE K1 launch (bf16 operands, fp32 softmax and
+    accumulation); an all-true mask takes the unmasked fast path, anything else goes in as
+    a dense mask. numpy in -> numpy out (like the reference); CUDA tensors in -> CUDA out.
+
+    The engine's passes call the fused paged path directly (the context is read in place,
+    never concatenated); if this module attribute is REPLACED (e.g. monkeypatched by a
+    user processor), BlockRunner routes every self- and cross-attention through the
+    replacement with the reference's arguments instead (eager, context gathered)."""
+    from ._device import to_device
+    from .errors import MaskError
+    as_np = not isinstance(q, torch.Tensor)
+    qt, kt, vt = (to_device(x, torch.float32) for x in (q, k, v))
+    if qt.dim() != 2 or kt.dim() != 2 or vt.dim() != 2 or qt.shape[1] % heads or \
+            kt.shape[1] != qt.shape[1] or vt.shape != kt.shape:
+        raise DimensionError("_mha expects q [T, D], k / v [m, D] with D % heads == 0")
+    for x, name in ((qt, "q"), (kt, "k"), (vt, "v")):
+        if not bool(torch.isfinite(x).all()):
+            raise DimensionError(f"{name} contains non-finite values")
+    T, D = qt.shape
+    m = kt.shape[0]
+    dh = D // heads
+    dhp = padded_head_dim(dh)
+    mt = torch.as_tensor(np.asarray(mask, dtype=bool) if not isinstance(mask, torch.Tensor)
+                         else mask, device=qt.device).bool()
+    if tuple(mt.shape) != (T, m):
+        raise DimensionError(f"mask shape {tuple(mt.shape)} != ({T}, {m})")
+    if not bool(mt.any(dim=1).all()):
+        raise MaskError("query row with no allowed key")
+    bf = lambda x, n: _pad_heads(x, heads, heads, dh, dhp, torch.empty(  # noqa: E731
+        n, heads * dhp, device=qt.device, dtype=torch.bfloat16))
+    qp, kp, vp = bf(qt, T), bf(kt, m), bf(vt, m)
+    out = torch.empty(T, heads * dhp, device=qt.device, dtype=torch.bfloat16)
+    m8 = None if bool(mt.all()) else mt.to(torch.uint8).contiguous()
+    attn_fwd(qp, heads, dhp, out, kp, vp, 0, m, scale=1.0 / math.sqrt(dh), mask=m8)
+    res = _unpad_heads(out, heads, heads, dh, dhp)
+    return res.cpu().numpy() if as_np else res
+
+
+_MHA_DEFAULT = _mha
+
+
+def _mha_hook():
+    """The user's replacement of `_mha`, or None while the built-in one is in place."""
+    h = globals()["_mha"]
+    return None if h is _MHA_DEFAULT else h
+
+
 class _LayerWeights:
     """Device weights of one layer: fused [D, 3Dp] QKV, bf16 GEMM operands (Dp = padded
     heads x padded head width; padding is exact zeros); the prompt projections ck/cv
@@ -323,6 +389,7 @@ class _CrossFold:
         vv = v.float().reshape(n, H, dhp)
         wqk = torch.einsum("dhe,jhe->dhj", lw.cq.float().reshape(D, H, dhp), kk).reshape(D, H * n)
         wvo = torch.einsum("jhe,hed->hjd", vv, lw.co.float().reshape(H, dhp, D)).reshape(H * n, D)
+        self.k, self.v = k, v  # prompt K/V rows (the `_mha` hook path attends them directly)
         self.n, self.groups, self.width = n, H, -(-(H * n) // 8) * 8
         pad = self.width - H * n
         self.wqk = torch.nn.functional.pad(wqk, (0, pad)).to(torch.bfloat16).contiguous()
@@ -367,7 +434,7 @@ class _Workspace:
         self.cross_bufs = {}
 
 
-def _residual(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor, tmp: torch.Tensor = None):
+def _residual(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor):
     """x += a @ w with bf16 operands, fp32 accumulation and fp32 in-place epilogue (one
     cuBLASLt call with beta = 1, per-shape algorithm, `ifx_gemm_bf16`)."""
     gemm(a, w, x, beta=1.0)
@@ -417,11 +484,14 @@ class BlockRunner:
             gemm(ws.h, lw.wqkv, ws.qkv)
             if rope is not None:  # Q and the block's own K, before K1 and the page write
                 rope_qk(ws.qkv, H, dhp, c.head_dim // 2, 0, Dp, rope[0], rope[1])
-            ev = self.attn_events
+            hook = _mha_hook()
+            ev = self.attn_events if hook is None else None
             if ev is not None:
                 e0 = timing_event()
                 e0.record()
-            if ctx is not None:
+            if hook is not None:  # a user attention processor (reference signature)
+                self._hooked_self(hook, li, ctx, q, kc, vc)
+            elif ctx is not None:
                 ctx.attend(li, q, H, dhp, ws.attn, kc, vc, sc)
             else:
                 attn_fwd(q, H, dhp, ws.attn, cur_k=kc, cur_v=vc, scale=sc)
@@ -429,18 +499,52 @@ class BlockRunner:
                 e1 = timing_event()
                 e1.record()
                 ev.append((e0, e1))
-            _residual(ws.x, ws.attn, lw.wo, ws.tmp)
+            _residual(ws.x, ws.attn, lw.wo)
             if cross is not None:  # folded through the prompt's few keys (_CrossFold)
                 rms_bf16(ws.x, ws.h)
-                _cross_attend(ws, cross[li], ws.x, ws.h, sc)
+                if hook is not None:
+                    self._hooked_cross(hook, lw, cross[li])
+                else:
+                    _cross_attend(ws, cross[li], ws.x, ws.h, sc)
             rms_bf16(ws.x, ws.h)
             _ffn_up(ws.h, lw.w1, ws.ffn)
-            _residual(ws.x, ws.ffn, lw.w2, ws.tmp)
+            _residual(ws.x, ws.ffn, lw.w2)
             if collect_kv:  # clean pass: page write of this layer's K/V (engine.py:303-306)
                 cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
         if eps_out is not None:
             rms_bf16(ws.x, ws.h)
             gemm(ws.h, m.w_out, eps_out)
+
+    def _hooked_self(self, hook, li: int, ctx, q, kc, vc) -> None:
+        """engine.py:202-210 through a replaced `_mha`: k / v = [cached context ∥ block],
+        all-true mask, the hook's [T, D] output written back into the padded layout."""
+        m = self.model
+        c = m.config
+        un = lambda x: _unpad_heads(x, c.heads, m.heads_pad, c.head_dim, m.dh_pad)  # noqa: E731
+        k, v = kc, vc
+        if ctx is not None:
+            lo, hi = ctx.ranges[li]
+            if hi > lo:
+                ck, cv = ctx.cache._gather(li, SELF_ATTN, None, lo, hi - lo, lo, hi, raw=True)
+                k, v = torch.cat([ck, kc]), torch.cat([cv, vc])
+        T = q.shape[0]
+        mask = torch.ones(T, k.shape[0], dtype=torch.bool, device=q.device)
+        out = hook(un(q), un(k), un(v), c.heads, mask)
+        _pad_heads(torch.as_tensor(out, dtype=torch.float32), c.heads, m.heads_pad, c.head_dim,
+                   m.dh_pad, self.ws.attn)
+
+    def _hooked_cross(self, hook, lw, fold: "_CrossFold") -> None:
+        """engine.py:211-215 through a replaced `_mha`: q = h2 @ cq over the prompt K/V."""
+        m, ws = self.model, self.ws
+        c = m.config
+        un = lambda x: _unpad_heads(x, c.heads, m.heads_pad, c.head_dim, m.dh_pad)  # noqa: E731
+        q2 = torch.empty_like(ws.attn)
+        gemm(ws.h, lw.cq, q2)
+        mask = torch.ones(q2.shape[0], fold.k.shape[0], dtype=torch.bool, device=q2.device)
+        out = hook(un(q2), un(fold.k), un(fold.v), c.heads, mask)
+        _pad_heads(torch.as_tensor(out, dtype=torch.float32), c.heads, m.heads_pad, c.head_dim,
+                   m.dh_pad, q2)
+        gemm(q2, lw.co, ws.x, beta=1.0)
 
     def denoise(self, latent: torch.Tensor, schedule: DenoiseSchedule, ctx, cross,
                 cache: KvCache | None, chunk_index: int) -> torch.Tensor:
@@ -475,10 +579,11 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     the first pass is captured once as a CUDA graph (t*time_vec read from a device buffer)
     and replayed S times, so the host enqueues one pass per block instead of S (what keeps
     a Ulysses rank, whose GPU share of a pass shrinks with the world size, GPU-bound).
-    Eager when capture is off (IFX_CUDA_GRAPHS=0), when K1 launches are being timed
-    (attn_events), when host-tier pages are staged on the side stream, or when the page
-    length forces the K7-gather path; both modes compute t*time_vec the same way, so they
-    are bit-identical."""
+    K1 launches stay timed inside a capture (attn_events: external event nodes, re-recorded
+    by every replay). Eager when capture is off (IFX_CUDA_GRAPHS=0), for the first block of
+    a run on an idle GPU, when host-tier pages are staged on the side stream, when the
+    page length forces the K7-gather path, or when `_mha` is replaced by a user hook; both
+    modes compute t*time_vec the same way, so they are bit-identical."""
     steps = [float(t) for t in schedule.steps]
     m = runner.model
     if runner._tv is None:
@@ -500,7 +605,7 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     # idle for its whole duration (in steady state it overlaps the previous block's clean
     # pass; a host-bound Ulysses rank keeps capturing every later block)
     eager_block = first_block and (runner._tail is None or runner._tail.query())
-    use = (GRAPHS and graphs_ok and len(steps) > 1 and not eager_block
+    use = (GRAPHS and graphs_ok and len(steps) > 1 and not eager_block and _mha_hook() is None
            and (ctx is None or (ctx.paged and not ctx.jobs)))
     if use and isinstance(cross, _LazyFold):
         cross.materialize()  # fold ops (and their allocations) must not enter the graph
@@ -779,6 +884,8 @@ class _KvContext:
                 torch.cuda.current_stream().wait_event(self.staged[j])
         sk, sv = self._stage_views(self._buf(j)) if j is not None else (None, None)
         pool = self.pool
+        if pool.dev_k is None:  # capacity_pages_device=0: every page is staged, but K1 still
+            pool.ensure(1, 0)   # takes the (unused) device pool as its base
         attn(q, heads, dhp, out, sl(pool.dev_k), sl(pool.dev_v), lo, hi - lo, cur_k, cur_v,
              scale=scale, ctx_slots=self.tables[li], page_len=self.P, first_token=self.first[li],
              stage_k=sl(sk) if sk is not None else None, stage_v=sl(sv) if sv is not None else None,
@@ -892,13 +999,13 @@ def _cross_from_cache(model: ToyModel, cache: KvCache | None, prompt_ctx):
     return out
 
 
-_RUNNERS: dict = {}
-
-
 def _runner(model: ToyModel) -> BlockRunner:
-    r = _RUNNERS.get(id(model))
-    if r is None or r.model is not model:
-        r = _RUNNERS[id(model)] = BlockRunner(model)
+    """The model's BlockRunner (workspaces, staging buffers, graph state). Stored ON the
+    model and holding it only through a weak proxy, so the runner and its device buffers
+    are freed together with the model (no process-global registry keeps either alive)."""
+    r = model.__dict__.get("_b200_runner")
+    if r is None:
+        r = model._b200_runner = BlockRunner(weakref.proxy(model))
     return r
 
 

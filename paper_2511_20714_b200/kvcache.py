@@ -359,9 +359,15 @@ class KvCache:
         self._pt = PageTable(config)
         if row_width is not None and config.latent is not None:
             raise ConfigError("row_width override is not supported in latent mode")
-        w = row_width or config.stored_width
+        # pool rows are a multiple of 16 bytes (K2/K7 move rows in 16-byte vectors): widths
+        # the reference accepts but that do not align are zero-padded in the pool and
+        # trimmed on every read, so no call fails after its bookkeeping is recorded
+        esz = torch.finfo(dtype).bits // 8
+        w = row_width or -(-config.stored_width * esz // 16) * 16 // esz
         wc = cross_row_width or w
         self._row_width = {SELF_ATTN: w, CROSS_ATTN: wc}
+        self._logical_width = {SELF_ATTN: config.stored_width if row_width is None else w,
+                               CROSS_ATTN: config.stored_width if row_width is None else wc}
         cd, ch = config.capacity_pages_device, config.capacity_pages_host
         self._pools = {SELF_ATTN: _Pool(w, dtype, config.page_len, cd, ch),
                        CROSS_ATTN: _Pool(wc, dtype, config.page_len, cd, ch)}
@@ -450,7 +456,7 @@ class KvCache:
         fresh one. Bounds the host footprint of a fetch whose tiers change a lot (e.g. the
         first fetch after a long prefill) without splitting the steady-state fetch, whose
         mid-fetch demotions of later layers are all undone."""
-        if not self._batch:
+        if self._batch != 1:  # nested batches: only the outermost may run its moves
             return
         _, _, lazy = self._pt.pending(fetched_layer)
         ext = self._pt.pool_extent()
@@ -495,6 +501,10 @@ class KvCache:
         if self._latent_down is not None:
             k = (k.float() @ self._latent_down).contiguous()
             v = (v.float() @ self._latent_down).contiguous()
+        pad = self._row_width[kind] - k.shape[1]
+        if pad > 0 and k.shape[1] == self._logical_width[kind]:  # unaligned width: zero-pad rows
+            k = torch.nn.functional.pad(k, (0, pad))
+            v = torch.nn.functional.pad(v, (0, pad))
         if k.stride(1) != 1 or v.stride(1) != 1 or k.stride(0) != v.stride(0):
             k, v = k.contiguous(), v.contiguous()
         with self._lock:
@@ -522,7 +532,8 @@ class KvCache:
             try:
                 return self._pt.offload(block_ids)
             finally:
-                self._sync()
+                if not self._batch:  # inside batch(): the moves run when the batch ends
+                    self._sync()
 
     def evict_window(self, keep_last_n_tokens: int) -> int:
         """kvcache.py:258-285 (freed pages return their slots to the pools)."""
@@ -566,6 +577,9 @@ class KvCache:
                 None if tokens is None else tokens.data_ptr(), first, n,
                 ko.data_ptr(), vo.data_ptr(), stream_ptr()), "kv_gather")
             count_launch()
+        lw = self._logical_width[kind]
+        if p.width != lw:  # padded pool rows (alignment)
+            ko, vo = ko[:, :lw].contiguous(), vo[:, :lw].contiguous()
         if self._latent_up is not None and not raw:
             ko, vo = ko.float() @ self._latent_up, vo.float() @ self._latent_up
         return ko, vo
@@ -585,6 +599,7 @@ class KvCache:
         if not 0 <= layer < self.config.num_layers:
             raise OutOfRangeError(f"layer {layer} out of range")
         with self._lock:
+            self._no_batch("a fetch")
             try:
                 self._pt.touch_indices(layer, kind, idx)
             finally:

@@ -172,3 +172,62 @@ def test_batched_context_fetch_cancels_lru_churn():
     assert total_pages > 2 * cap
     assert sum(per_call[-3:]) > 6 * sum(batched[-3:])
     assert max(batched[-3:]) <= 2 * L * per_block  # ~ the pages whose tier really changes
+
+
+def test_drain_refused_inside_open_batch():
+    """A drain inside an open batch would clear the move log while the batch's pages still
+    index it (a later restore in the batch would retarget an unrelated move): refused."""
+    from paper_2511_20714_b200.errors import ConfigError
+
+    pt = PageTable(KvConfig(num_layers=1, head_dim=4, page_len=1, capacity_pages_device=1,
+                            capacity_pages_host=8))
+    for _ in range(4):
+        pt.append(0, "self_attn", 1, 0)
+    pt.drain_moves()
+    pt.batch_begin()
+    pt.touch_indices(0, "self_attn", [1])
+    with pytest.raises(ConfigError):
+        pt.drain_moves()
+    pt.touch_indices(0, "self_attn", [2])
+    pt.touch_indices(0, "self_attn", [0])
+    pt.batch_end()
+    mv = pt.drain_moves()
+    _check_batches(mv)
+    # the churn cancels inside the batch: page 0 is back on the device tier in its own slot
+    # (whose data never left), pages 1-3 stay on the host tier, and no move is left to run
+    st = pt.state()
+    assert [p[1] for p in st["streams"][0][4]] == [0, 1, 1, 1]
+    assert pt.slots(0, "self_attn", 0, 1)[0].tolist() == [0]
+    assert len(mv) == 0
+
+
+def test_cache_calls_inside_batch_keep_the_move_log():
+    """KvCache.fetch_indices inside batch() raises (data only consistent after the batch)
+    and offload_blocks inside batch() defers its moves to the batch's end."""
+    from paper_2511_20714_b200.kvcache import KvCache
+
+    cache = KvCache(KvConfig(num_layers=1, head_dim=4, page_len=1, capacity_pages_device=2,
+                             capacity_pages_host=8))
+    pt = cache.page_table
+    with _nullbatch(cache):
+        with pytest.raises(RuntimeError):
+            cache.fetch_indices(0, [])
+        cache.offload_blocks([])  # no drain inside the open batch
+        assert cache._batch == 1
+    assert cache._batch == 0
+    del pt
+
+
+class _nullbatch:
+    """Opens the cache's batch bookkeeping without executing moves on exit (no GPU here)."""
+
+    def __init__(self, cache):
+        self.cache = cache
+
+    def __enter__(self):
+        self.cache._pt.batch_begin()
+        self.cache._batch += 1
+
+    def __exit__(self, *exc):
+        self.cache._batch -= 1
+        self.cache._pt.batch_end()
