@@ -207,6 +207,21 @@ def run_reference(args):
     return 0
 
 
+def attn_traffic(cfgname, world):
+    """DRAM bytes of one K1 launch of this workload (rank shape at `world` ranks) from an
+    ncu --set full capture committed in profiles/attn_traffic.json, or (None, None)."""
+    tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if not os.path.exists(tpath):
+        return None, None
+    with open(tpath) as f:
+        recs = json.load(f)
+    t_rec = recs.get(cfgname if world == 1 else f"{cfgname}@w{world}")
+    if not t_rec:
+        return None, None
+    return t_rec["dram_bytes_per_launch"], (
+        f"{t_rec['launch']}; algorithmic {t_rec['algorithmic_bytes_per_launch']} B; {t_rec['source']}")
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_ours(args):
     import numpy as np
@@ -306,15 +321,7 @@ def run_ours(args):
     assert all(np.isfinite(b.latent).all() for b in blocks)
 
     cpu = None if args.no_cpu_baseline else cpu_baseline(c, cfgname)
-    traffic, traffic_note = None, None
-    tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            t_rec = json.load(f).get(cfgname)
-        if t_rec:  # DRAM bytes of one K1 launch from an ncu --set full capture
-            traffic = t_rec["dram_bytes_per_launch"]
-            traffic_note = (f"{t_rec['launch']}; algorithmic {t_rec['algorithmic_bytes_per_launch']} B; "
-                            f"{t_rec['source']}")
+    traffic, traffic_note = attn_traffic(cfgname, 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -466,13 +473,15 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
     mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
                        block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
                        weight_seed=0)
-    model = E.ToyModel(mc, weights="device")  # heads % N != 0: balanced query split, no padding
+    # the same model as the N = 1 line (reference PCG64 weights for c1-c3); heads % N != 0
+    # use the balanced query split, no padding
+    model = E.ToyModel(mc, weights=c["weights"])
     comm = UlyssesComm()
     nb = c["blocks"]
     kvc = E.default_kv_config(mc, capacity_pages_device=10**8, capacity_pages_host=4096)
     req = E.GenerationRequest(nb, E.DenoiseSchedule(STEPS), seed=0)
-    g = torch.Generator(device="cuda").manual_seed(0)
-    noise = [torch.randn(mc.block_len, mc.model_dim, device="cuda", generator=g) for _ in range(nb)]
+    # the reference's seeded noise (engine.py:280-282), resident in HBM for `value`
+    noise = [torch.from_numpy(E._init_noise(mc, 0, ch)).cuda() for ch in range(nb)]
     eng = UlyssesEngine(model, comm, kvc)
     roll = lambda: eng.generate(req, noise_provider=lambda ch: noise[ch], gather=False)  # noqa: E731
     for _ in range(args.warmup):
@@ -515,25 +524,31 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
     e2e = torch.tensor([(time.perf_counter() - t0) / args.steps], device="cuda")
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     clocks = clk.summary()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(c, cfgname)  # host cores of rank 0's node; other ranks wait
+    traffic, traffic_note = attn_traffic(cfgname, world)
     if rank == 0:
         T, D = mc.block_len, mc.model_dim
         line = {"metric": METRIC, "value": nb * FRAMES_PER_BLOCK / (ms / 1e3), "unit": UNIT,
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (device-seeded noise, random-init weights)",
+                "data": ("synthetic (reference-seeded noise, PCG64 random-init weights)"
+                         if c["weights"] == "reference" else "synthetic (reference-seeded noise, "
+                         "torch-seeded random-init weights)"),
                 "config": {"workload": c["desc"], "parallelism": f"ulysses{world}",
                            "head_split": "whole heads" if eng.runner.plan is None else
                            f"balanced: {eng.runner.plan.hl} heads / {len(eng.runner.plan.segs)} "
                            f"segments on rank 0", "l2": "inputs larger than L2"},
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                             "frac": achieved / peak if achieved else None, "traffic": None,
-                             "peak_source": peak_src,
+                             "frac": achieved / peak if achieved else None, "traffic": traffic,
+                             "traffic_launch": traffic_note, "peak_source": peak_src,
                              "scope": "rank 0's K1 launches, one eager rollout with per-launch events"},
                 "e2e": {"value": nb * FRAMES_PER_BLOCK / float(e2e.item()), "unit": UNIT,
                         "h2d_bytes_per_step": nb * T * D * 4 // world,
                         "d2h_bytes_per_step": nb * T * D * 4},
                 "comm": {"a2a_messages": comm.messages, "a2a_bytes": comm.bytes},
-                "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None,
+                "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
                 "cuda_graphs": "denoise passes captured once per block, replayed (IFX_CUDA_GRAPHS=0: eager)"}
         print(json.dumps(line), flush=True)
     dist.barrier()
