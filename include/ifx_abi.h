@@ -274,6 +274,42 @@ int ifx_copy_blocks(const void* src, void* dst, const int64_t* desc, int64_t n_b
 int ifx_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
                   int d_type, int64_t M, int64_t N, int64_t K, float beta, int relu, void* stream);
 
+/* G1 — the dense projections as a hand-written persistent tcgen05/TMA GEMM with fused
+ * epilogues (engine.py:202-205 h @ wq/wk/wv, :210 @ wo, :215 cross, :217-218 FFN, :220
+ * eps; the page write of kvcache.py:179-234 on the clean pass, engine.py:303-306):
+ *   C[m, n] = f(A[m, :] . B[:, n]) with A bf16 [M, K] (row stride lda), B bf16 [K, N]
+ *   (ldb), fp32 accumulation; C bf16, or fp32 with C = beta * C + f(.) (the residual).
+ * f, in order: row scale (rs_part != NULL: x rsqrt(sum_p rs_part[m * rs_ld + p] / rs_dim +
+ * rs_eps), the RMS norm of the fp32 row A was copied from, engine.py:171-173), ReLU, 3D RoPE
+ * (rope_cos != NULL: pairs (2i, 2i+1), i < rope_pairs, of each head (stride rope_hs) of
+ * the column blocks at rope_q0 and rope_k0, rotated by row m's angle i, tables
+ * [(rope_row0 + m) * rope_pairs + i]). With fp32 C and emit_b != NULL the new row is also
+ * written as bf16 to emit_b and partial sums of its squares (one per half column tile) to
+ * emit_ss[m * emit_ss_ld + part] (*out_tiles_n = parts per row: the consumer's rs_parts).
+ * page_pool != NULL (bf16 C only): columns [page_k_col0, +pool width) of row m are also
+ * written to token page_token0 + m of the K stream whose pages start at page_first_token
+ * with slot codes page_slots (device int32, as ifx_kv_append), [page_v_col0, ...) to V.
+ * N % 8 == 0; 16-byte aligned operands. */
+typedef struct ifx_gemm_params {
+  const void* a; int64_t lda;
+  const void* b; int64_t ldb;
+  void* c; int64_t ldc; int c_type;
+  int relu;
+  int64_t m, n, k;
+  float beta;
+  float rs_eps;
+  const float* rs_part; int64_t rs_ld; int64_t rs_parts; int64_t rs_dim;
+  void* emit_b; int64_t emit_ld;
+  float* emit_ss; int64_t emit_ss_ld;
+  const float* rope_cos; const float* rope_sin;
+  int64_t rope_row0, rope_q0, rope_k0, rope_pairs, rope_hs, rope_heads;
+  const ifx_kv_pool* page_pool; const int32_t* page_slots;
+  int64_t page_first_token, page_token0, page_k_col0, page_v_col0;
+} ifx_gemm_params;
+int ifx_gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream);
+/* sum-of-squares parts per row G1 emits for an [M, N] output (the emit_ss width needed) */
+int ifx_gemm_tiles_n(int64_t m, int64_t n, int64_t* out_tiles_n);
+
 /* Initial block noise, host side (engine.py:280-282): writes the first n values of
  * np.random.default_rng([seed, chunk]).standard_normal(...).astype(float32) into `out`
  * (host memory, e.g. pinned), bit-identically, using `threads` host threads (0 = all).

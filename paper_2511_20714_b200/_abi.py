@@ -44,7 +44,7 @@ EXPORTS = (
     "ifx_dev_alloc", "ifx_dev_free",
     "ifx_attn_fwd", "ifx_attn_workspace_bytes",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_group_softmax", "ifx_ulysses_pack", "ifx_ulysses_unpack",
-    "ifx_copy_blocks", "ifx_gemm_bf16",
+    "ifx_copy_blocks", "ifx_gemm_bf16", "ifx_gemm_fused", "ifx_gemm_tiles_n",
     "ifx_noise_normal_f32",
 )
 
@@ -77,6 +77,29 @@ class AttnParams(ctypes.Structure):
         ("k_stage", ctypes.c_void_p), ("v_stage", ctypes.c_void_p), ("stage_rows", ctypes.c_int64),
         ("ctx_tile_runs", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_int64),
+    ]
+
+
+class GemmParams(ctypes.Structure):
+    """Mirror of `ifx_gemm_params` (include/ifx_abi.h)."""
+
+    _fields_ = [
+        ("a", ctypes.c_void_p), ("lda", ctypes.c_int64),
+        ("b", ctypes.c_void_p), ("ldb", ctypes.c_int64),
+        ("c", ctypes.c_void_p), ("ldc", ctypes.c_int64), ("c_type", ctypes.c_int),
+        ("relu", ctypes.c_int),
+        ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("k", ctypes.c_int64),
+        ("beta", ctypes.c_float), ("rs_eps", ctypes.c_float),
+        ("rs_part", ctypes.c_void_p), ("rs_ld", ctypes.c_int64), ("rs_parts", ctypes.c_int64),
+        ("rs_dim", ctypes.c_int64),
+        ("emit_b", ctypes.c_void_p), ("emit_ld", ctypes.c_int64),
+        ("emit_ss", ctypes.c_void_p), ("emit_ss_ld", ctypes.c_int64),
+        ("rope_cos", ctypes.c_void_p), ("rope_sin", ctypes.c_void_p),
+        ("rope_row0", ctypes.c_int64), ("rope_q0", ctypes.c_int64), ("rope_k0", ctypes.c_int64),
+        ("rope_pairs", ctypes.c_int64), ("rope_hs", ctypes.c_int64), ("rope_heads", ctypes.c_int64),
+        ("page_pool", ctypes.c_void_p), ("page_slots", ctypes.c_void_p),
+        ("page_first_token", ctypes.c_int64), ("page_token0", ctypes.c_int64),
+        ("page_k_col0", ctypes.c_int64), ("page_v_col0", ctypes.c_int64),
     ]
 
 
@@ -134,6 +157,8 @@ def lib() -> ctypes.CDLL:
             L.ifx_copy_blocks.argtypes = [P, P, P, I64, I64, P]
             L.ifx_gemm_bf16.argtypes = [P, I64, P, I64, P, I64, ctypes.c_int, I64, I64, I64,
                                         ctypes.c_float, ctypes.c_int, P]
+            L.ifx_gemm_fused.argtypes = [ctypes.POINTER(GemmParams), PI64, P]
+            L.ifx_gemm_tiles_n.argtypes = [I64, I64, PI64]
             L.ifx_group_softmax.argtypes = [P, I64, I64, I64, I64, ctypes.c_float, P, I64, P]
             L.ifx_rope_qk.argtypes = [P, I64, I64, I64, I64, I64, I64, I64, P, P, I64, P]
             L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]

@@ -138,6 +138,74 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, beta: float = 0.0,
     return out
 
 
+RMS_EPS = 1e-6  # engine.py:26
+
+
+class RowNorm:
+    """RMS statistics a G1 producer leaves for its consumer: the bf16 copy of the fp32 rows
+    (the consumer's A) and per-column-tile sums of squares [rows, parts] (its row scale)."""
+
+    __slots__ = ("rows_bf16", "ss", "parts", "dim")
+
+    def __init__(self, rows_bf16: torch.Tensor, ss: torch.Tensor, parts: int, dim: int):
+        self.rows_bf16, self.ss, self.parts, self.dim = rows_bf16, ss, parts, dim
+
+
+def gemm_tiles_n(m: int, n: int) -> int:
+    out = ctypes.c_int64()
+    _abi.check(_abi.lib().ifx_gemm_tiles_n(m, n, ctypes.byref(out)), "gemm_tiles_n")
+    return out.value
+
+
+def gemm_fused(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, beta: float = 0.0,
+               relu: bool = False, norm_in: RowNorm | None = None, norm_out: RowNorm | None = None,
+               rope=None, page=None, stream=None) -> int:
+    """G1 (gemm_sm100.cu): out = f(a @ b) on tcgen05, bf16 a [M, K] / b [K, N], fp32
+    accumulate; out bf16, or fp32 with out = beta * out + f(.).
+
+    norm_in:  a holds bf16 copies of fp32 rows whose RMS statistics are norm_in.ss: the
+              product is scaled by rsqrt(mean(row^2) + 1e-6) (engine.py:171-173).
+    norm_out: (fp32 out) also write the new rows as bf16 to norm_out.rows_bf16 and their
+              per-tile sums of squares to norm_out.ss (norm_out.parts is set).
+    rope:     (cos, sin, row0, pairs, head_stride, heads, q_col0, k_col0) 3D RoPE tables.
+    page:     (pool abi, slots tensor, first_token, token0, k_col0, v_col0) page write.
+    Returns the column tile count (norm_out.parts)."""
+    M, K = a.shape
+    N = b.shape[1]
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or b.shape[0] != K or \
+            tuple(out.shape) != (M, N):
+        raise DimensionError("gemm expects bf16 a [M, K], b [K, N] and out [M, N]")
+    p = _abi.GemmParams()
+    p.a, p.lda, p.b, p.ldb = a.data_ptr(), row_ld(a), b.data_ptr(), row_ld(b)
+    p.c, p.ldc, p.c_type = out.data_ptr(), row_ld(out), dtype_code(out.dtype)
+    p.m, p.n, p.k, p.beta, p.relu = M, N, K, float(beta), int(relu)
+    if norm_in is not None:
+        p.rs_part, p.rs_ld, p.rs_parts = norm_in.ss.data_ptr(), norm_in.ss.stride(0), norm_in.parts
+        p.rs_dim, p.rs_eps = norm_in.dim, RMS_EPS
+    if norm_out is not None:
+        p.emit_b, p.emit_ld = norm_out.rows_bf16.data_ptr(), row_ld(norm_out.rows_bf16)
+        p.emit_ss, p.emit_ss_ld = norm_out.ss.data_ptr(), norm_out.ss.stride(0)
+    if rope is not None:
+        cos, sin, row0, pairs, hs, heads, q0, k0 = rope
+        p.rope_cos, p.rope_sin, p.rope_row0 = cos.data_ptr(), sin.data_ptr(), row0
+        p.rope_pairs, p.rope_hs, p.rope_heads, p.rope_q0, p.rope_k0 = pairs, hs, heads, q0, k0
+    keep = None
+    if page is not None:
+        pool, slots, first, token0, kc0, vc0 = page
+        keep = pool
+        p.page_pool = ctypes.addressof(pool)
+        p.page_slots, p.page_first_token, p.page_token0 = slots.data_ptr(), first, token0
+        p.page_k_col0, p.page_v_col0 = kc0, vc0
+    tn = ctypes.c_int64()
+    _abi.check(_abi.lib().ifx_gemm_fused(ctypes.byref(p), ctypes.byref(tn), stream_ptr(stream)),
+               "gemm_fused")
+    del keep
+    LAUNCHES[0] += 1
+    if norm_out is not None:
+        norm_out.parts, norm_out.dim = tn.value, N
+    return tn.value
+
+
 def tile_run_codes(codes: np.ndarray, page_len: int) -> np.ndarray:
     """Per 128-key tile of a paged context (K1's ctx_tile_runs): the first page's slot code
     when the tile's pages are one consecutive run of one pool, else INT32_MIN. The last

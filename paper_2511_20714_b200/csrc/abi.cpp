@@ -14,6 +14,7 @@
 #include "attn_kernel.h"
 #include "common_host.h"
 #include "device_state.h"
+#include "gemm_kernel.h"
 #include "kv_kernels.h"
 
 namespace ifx {
@@ -28,6 +29,16 @@ int fail(int code, const std::string& msg) {
 static int cuda_fail(int err, const char* what) {
   if (err == 0) return IFX_OK;
   return fail(IFX_ECUDA, std::string(what) + ": " + cudaGetErrorString((cudaError_t)err));
+}
+
+static int check_pool(const ifx_kv_pool* p) {
+  if (p == nullptr || p->width <= 0 || p->page_len <= 0) return fail(IFX_EDIM, "bad pool");
+  const int esz = p->type == IFX_BF16 ? 2 : 4;
+  if ((p->width * esz) % 16) return fail(IFX_EDIM, "row width must be a multiple of 16 bytes");
+  if ((reinterpret_cast<uintptr_t>(p->dev_k) | reinterpret_cast<uintptr_t>(p->dev_v) |
+       reinterpret_cast<uintptr_t>(p->host_k) | reinterpret_cast<uintptr_t>(p->host_v)) & 15)
+    return fail(IFX_EDIM, "pools must be 16-byte aligned");
+  return IFX_OK;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -212,6 +223,95 @@ int choose_splits(const ifx_attn_params* p) {
   return best;
 }
 
+// G1 (gemm_sm100.cu): validation + tensor maps; the epilogue options are documented at
+// ifx_gemm_params in include/ifx_abi.h.
+int gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
+  if (p->m < 0 || p->n < 1 || p->k < 1 || p->lda < p->k || p->ldb < p->n || p->ldc < p->n)
+    return fail(IFX_EDIM, "bad GEMM sizes");
+  if (p->n % 8) return fail(IFX_EDIM, "GEMM N must be a multiple of 8");
+  if (p->m > INT32_MAX || p->n > INT32_MAX || p->k > INT32_MAX)
+    return fail(IFX_EDIM, "GEMM extents must fit int32");
+  const bool f32 = p->c_type == IFX_F32;
+  if (!f32 && p->c_type != IFX_BF16) return fail(IFX_EUNSUPPORTED, "C must be fp32 or bf16");
+  const int esz = f32 ? 4 : 2;
+  auto mis = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) != 0; };
+  if (mis(p->c) || (p->ldc * esz) % 16) return fail(IFX_EDIM, "C must be 16-byte aligned");
+  if (!f32 && (p->beta != 0.f || p->emit_b != nullptr))
+    return fail(IFX_EUNSUPPORTED, "beta / emit need an fp32 C");
+  if (p->emit_b != nullptr && (mis(p->emit_b) || (p->emit_ld * 2) % 16 || p->emit_ss == nullptr))
+    return fail(IFX_EDIM, "emit needs a 16-byte aligned bf16 row buffer and a sum-of-squares buffer");
+  const int n_sm = num_sms();
+  const int bn = gemm_pick_bn(p->m, p->n, n_sm);
+  GemmArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.M = (int)p->m;
+  a.N = (int)p->n;
+  a.K = (int)p->k;
+  a.tiles_m = (int)((p->m + 127) / 128);
+  a.tiles_n = (int)((p->n + bn - 1) / bn);
+  // sums of squares per row: one per (column tile, epilogue half)
+  if (out_tiles_n) *out_tiles_n = 2 * a.tiles_n;
+  if (p->emit_b != nullptr && p->emit_ss_ld < 2 * a.tiles_n)
+    return fail(IFX_EDIM, "emit_ss_ld smaller than the sum-of-squares part count");
+  if (p->m == 0) return IFX_OK;
+  int rc;
+  if ((rc = make_map(&a.tm_a, p->a, p->m, p->k, p->lda, 128))) return rc;
+  if ((rc = make_map(&a.tm_b, p->b, p->k, p->n, p->ldb, 64))) return rc;
+  a.c = p->c;
+  a.ldc = p->ldc;
+  a.c_f32 = f32;
+  a.beta = p->beta;
+  a.relu = p->relu;
+  if (p->rs_part != nullptr) {
+    if (p->rs_parts < 1 || p->rs_ld < p->rs_parts || p->rs_dim < 1)
+      return fail(IFX_EDIM, "bad row-scale statistics");
+    a.rs_part = p->rs_part;
+    a.rs_parts = (int)p->rs_parts;
+    a.rs_ld = p->rs_ld;
+    a.rs_inv_d = 1.f / (float)p->rs_dim;
+    a.rs_eps = p->rs_eps;
+  }
+  a.emit_b = static_cast<__nv_bfloat16*>(p->emit_b);
+  a.emit_ld = p->emit_ld;
+  a.emit_ss = p->emit_b != nullptr ? p->emit_ss : nullptr;
+  a.emit_ss_ld = p->emit_ss_ld;
+  if (p->rope_cos != nullptr) {
+    if (p->rope_hs % 32 || p->rope_q0 % 32 || p->rope_k0 % 32 || p->rope_pairs * 2 > p->rope_hs ||
+        p->rope_heads < 1 || p->rope_sin == nullptr)
+      return fail(IFX_EDIM, "RoPE heads must be 32-column aligned");
+    a.rope_cos = p->rope_cos;
+    a.rope_sin = p->rope_sin;
+    a.rope_row0 = p->rope_row0;
+    a.rope_q0 = p->rope_q0;
+    a.rope_k0 = p->rope_k0;
+    a.rope_pairs = (int)p->rope_pairs;
+    a.rope_hs = (int)p->rope_hs;
+    a.rope_heads = (int)p->rope_heads;
+  }
+  if (p->page_pool != nullptr) {
+    const ifx_kv_pool* pool = p->page_pool;
+    if (int r2 = check_pool(pool)) return r2;
+    if (f32 || pool->type != IFX_BF16) return fail(IFX_EUNSUPPORTED, "fused page write is bf16 -> bf16");
+    if (pool->width % 32 || p->page_k_col0 % 32 || p->page_v_col0 % 32 ||
+        p->page_k_col0 + pool->width > p->n || p->page_v_col0 + pool->width > p->n)
+      return fail(IFX_EDIM, "page-write columns must be 32-aligned blocks inside C");
+    if (p->page_token0 < p->page_first_token || p->page_slots == nullptr)
+      return fail(IFX_EDIM, "bad page-write tokens");
+    a.slots = p->page_slots;
+    a.pk_dev = static_cast<uint8_t*>(pool->dev_k);
+    a.pv_dev = static_cast<uint8_t*>(pool->dev_v);
+    a.pk_host = static_cast<uint8_t*>(pool->host_k);
+    a.pv_host = static_cast<uint8_t*>(pool->host_v);
+    a.prow_b = pool->width * 2;
+    a.rel0 = p->page_token0 - p->page_first_token;
+    a.pk_col0 = p->page_k_col0;
+    a.pv_col0 = p->page_v_col0;
+    a.pwidth = pool->width;
+    a.page_len = (int)pool->page_len;
+  }
+  return cuda_fail(gemm_launch(a, bn, static_cast<cudaStream_t>(stream)), "gemm launch");
+}
+
 }  // namespace ifx
 
 extern "C" {
@@ -226,20 +326,11 @@ int ifx_attn_workspace_bytes(const ifx_attn_params* p, int64_t* bytes) {
   return IFX_OK;
 }
 
-static int check_pool(const ifx_kv_pool* p) {
-  if (p == nullptr || p->width <= 0 || p->page_len <= 0) return ifx::fail(IFX_EDIM, "bad pool");
-  const int esz = p->type == IFX_BF16 ? 2 : 4;
-  if ((p->width * esz) % 16) return ifx::fail(IFX_EDIM, "row width must be a multiple of 16 bytes");
-  if ((reinterpret_cast<uintptr_t>(p->dev_k) | reinterpret_cast<uintptr_t>(p->dev_v) |
-       reinterpret_cast<uintptr_t>(p->host_k) | reinterpret_cast<uintptr_t>(p->host_v)) & 15)
-    return ifx::fail(IFX_EDIM, "pools must be 16-byte aligned");
-  return IFX_OK;
-}
 
 int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_type,
                   const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
                   int64_t token0, int64_t t, void* stream) {
-  if (int rc = check_pool(pool)) return rc;
+  if (int rc = ifx::check_pool(pool)) return rc;
   if (t < 0 || token0 < first_token) return ifx::fail(IFX_EDIM, "bad append sizes");
   if (t == 0) return IFX_OK;
   if (src_type == IFX_BF16 && pool->type == IFX_F32)
@@ -258,7 +349,7 @@ int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_
 int ifx_kv_gather(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
                   const int64_t* tokens, int64_t token0, int64_t n, void* k_out, void* v_out,
                   void* stream) {
-  if (int rc = check_pool(pool)) return rc;
+  if (int rc = ifx::check_pool(pool)) return rc;
   if (n < 0) return ifx::fail(IFX_EDIM, "bad gather sizes");
   if (n == 0) return IFX_OK;
   const int esz = pool->type == IFX_BF16 ? 2 : 4;
@@ -271,7 +362,7 @@ int ifx_kv_gather(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_t
 
 int ifx_kv_move_pages(const ifx_kv_pool* pool, const int64_t* moves, int64_t n, int dir,
                       void* stream) {
-  if (int rc = check_pool(pool)) return rc;
+  if (int rc = ifx::check_pool(pool)) return rc;
   if (n < 0 || (dir != 0 && dir != 1)) return ifx::fail(IFX_EDIM, "bad page move batch");
   if (n == 0) return IFX_OK;
   const int esz = pool->type == IFX_BF16 ? 2 : 4;
@@ -283,7 +374,7 @@ int ifx_kv_move_pages(const ifx_kv_pool* pool, const int64_t* moves, int64_t n, 
 
 int ifx_kv_copy_runs(const ifx_kv_pool* pool, const int64_t* runs, int64_t n, int dir,
                      void* stream) {
-  if (int rc = check_pool(pool)) return rc;
+  if (int rc = ifx::check_pool(pool)) return rc;
   if (n < 0 || (dir != 0 && dir != 1)) return ifx::fail(IFX_EDIM, "bad page run batch");
   const int esz = pool->type == IFX_BF16 ? 2 : 4;
   const int64_t slot_b = pool->page_len * pool->width * esz;
@@ -397,6 +488,17 @@ int ifx_ulysses_unpack(const void* src, int64_t n, int64_t groups, int64_t world
   int e = ifx::ulysses_launch(src, dst, n, groups, world, chunk * esz, dst_ld * esz, false,
                               static_cast<cudaStream_t>(stream));
   return ifx::cuda_fail(e, "ulysses unpack");
+}
+
+int ifx_gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
+  return ifx::gemm_fused(p, out_tiles_n, stream);
+}
+
+int ifx_gemm_tiles_n(int64_t m, int64_t n, int64_t* out_tiles_n) {
+  if (m < 0 || n < 1 || out_tiles_n == nullptr) return ifx::fail(IFX_EDIM, "bad GEMM sizes");
+  const int bn = ifx::gemm_pick_bn(m, n, ifx::num_sms());
+  *out_tiles_n = 2 * ((n + bn - 1) / bn);
+  return IFX_OK;
 }
 
 }  // extern "C"
