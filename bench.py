@@ -207,6 +207,24 @@ def run_reference(args):
     return 0
 
 
+def _gemm_path(runner) -> str:
+    if runner.g1:
+        return "G1 (tcgen05, norms / RoPE / page write fused) for every projection"
+    if runner.g1_qkv:
+        return "QKV on G1 (RoPE + page write fused), others cuBLASLt + RMS kernel"
+    return "cuBLASLt + RMS kernel"
+
+
+def rope_grid(args, c):
+    """--rope: 3D RoPE over (frames, latent rows, latent columns) of a block, Wan2.1 480p:
+    3 frames x 30 x 52 = 4,680 tokens (the north_star's fused RoPE; the reference has none)."""
+    if not args.rope:
+        return None
+    if c["block_len"] != 4680:
+        raise SystemExit("--rope is defined for the 4,680-token (3 x 30 x 52) blocks")
+    return (3, 30, 52)
+
+
 def attn_traffic(cfgname, world):
     """DRAM bytes of one K1 launch of this workload (rank shape at `world` ranks) from an
     ncu --set full capture committed in profiles/attn_traffic.json, or (None, None)."""
@@ -254,7 +272,7 @@ def run_ours(args):
     torch.backends.cuda.matmul.allow_tf32 = False
     mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
                        block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
-                       weight_seed=0)
+                       weight_seed=0, rope_grid=rope_grid(args, c))
     model = E.build_model(mc, weights=c["weights"])
     T, D = mc.block_len, mc.model_dim
     nb = c["blocks"]
@@ -326,7 +344,10 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (reference-seeded noise, PCG64 random-init weights)",
-        "config": {"workload": c["desc"], "layers": mc.layers, "heads": mc.heads,
+        "config": {"workload": c["desc"] + (", 3D RoPE (3 x 30 x 52) fused into the QKV GEMM"
+                                            if mc.rope_grid else ""),
+                   "rope_grid": mc.rope_grid, "gemm": _gemm_path(runner),
+                   "layers": mc.layers, "heads": mc.heads,
                    "head_dim": mc.head_dim, "tokens_per_block": T, "blocks": nb,
                    "denoise_steps": len(STEPS), "kv_cache": "bf16 paged (page_len 16): HBM slot pool + pinned host tier",
                    "l2": "inputs larger than L2 (weights 1.4 GB, KV pool up to 6 GB)",
@@ -367,7 +388,7 @@ def run_host_tier_bench(args, c, cfgname, local):
     torch.backends.cuda.matmul.allow_tf32 = False
     mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
                        block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
-                       weight_seed=0)
+                       weight_seed=0, rope_grid=rope_grid(args, c))
     model = E.build_model(mc, weights=c["weights"])
     T, L, W = mc.block_len, mc.layers, model.attn_width
     pages_blk = -(-T // 16)
@@ -472,7 +493,7 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
     torch.backends.cuda.matmul.allow_tf32 = False
     mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
                        block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
-                       weight_seed=0)
+                       weight_seed=0, rope_grid=rope_grid(args, c))
     # the same model as the N = 1 line (reference PCG64 weights for c1-c3); heads % N != 0
     # use the balanced query split, no padding
     model = E.ToyModel(mc, weights=c["weights"])
@@ -566,6 +587,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rope", action="store_true",
+                    help="3D RoPE on Q/K (3 x 30 x 52 grid), fused into the QKV GEMM epilogue")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -241,6 +241,12 @@ int ifx_rms_bf16(const float* x, int64_t rows, int64_t width, const float* tvec,
  * (row stride p_ld), which then meets (V . co) in one more GEMM. */
 int ifx_group_softmax(const float* s, int64_t rows, int64_t groups, int64_t group_size,
                       int64_t ld, float scale, void* p, int64_t p_ld, void* stream);
+/* The same with the logits' RMS row scale still to apply (s = bf16(x) . W rather than
+ * rms(x) . W): row r's logits are scaled by rsqrt(sum_p rs_part[r * rs_ld + p] / rs_dim +
+ * 1e-6) first (the statistics G1's residual epilogue emitted, engine.py:171-173). */
+int ifx_group_softmax_rs(const float* s, int64_t rows, int64_t groups, int64_t group_size,
+                         int64_t ld, float scale, void* p, int64_t p_ld, const float* rs_part,
+                         int64_t rs_ld, int64_t rs_parts, int64_t rs_dim, void* stream);
 
 /* 3D RoPE (B200 extension; the reference has no positional encoding, attention.py:6):
  * rotate, in place, the interleaved pairs (2k, 2k+1), k < pairs, of every head of the Q
@@ -307,8 +313,9 @@ typedef struct ifx_gemm_params {
   int64_t page_first_token, page_token0, page_k_col0, page_v_col0;
 } ifx_gemm_params;
 int ifx_gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream);
-/* sum-of-squares parts per row G1 emits for an [M, N] output (the emit_ss width needed) */
-int ifx_gemm_tiles_n(int64_t m, int64_t n, int64_t* out_tiles_n);
+/* sum-of-squares parts per row G1 emits for an [M, N] = [M, K] . [K, N] output (the
+ * emit_ss width needed) */
+int ifx_gemm_tiles_n(int64_t m, int64_t n, int64_t k, int64_t* out_tiles_n);
 
 /* Initial block noise, host side (engine.py:280-282): writes the first n values of
  * np.random.default_rng([seed, chunk]).standard_normal(...).astype(float32) into `out`

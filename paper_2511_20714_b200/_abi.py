@@ -43,7 +43,7 @@ EXPORTS = (
     "ifx_kv_append", "ifx_kv_gather", "ifx_kv_move_pages", "ifx_kv_copy_runs", "ifx_host_alloc", "ifx_host_free",
     "ifx_dev_alloc", "ifx_dev_free",
     "ifx_attn_fwd", "ifx_attn_workspace_bytes",
-    "ifx_rms_bf16", "ifx_rope_qk", "ifx_group_softmax", "ifx_ulysses_pack", "ifx_ulysses_unpack",
+    "ifx_rms_bf16", "ifx_rope_qk", "ifx_group_softmax", "ifx_group_softmax_rs", "ifx_ulysses_pack", "ifx_ulysses_unpack",
     "ifx_copy_blocks", "ifx_gemm_bf16", "ifx_gemm_fused", "ifx_gemm_tiles_n",
     "ifx_noise_normal_f32",
 )
@@ -158,8 +158,10 @@ def lib() -> ctypes.CDLL:
             L.ifx_gemm_bf16.argtypes = [P, I64, P, I64, P, I64, ctypes.c_int, I64, I64, I64,
                                         ctypes.c_float, ctypes.c_int, P]
             L.ifx_gemm_fused.argtypes = [ctypes.POINTER(GemmParams), PI64, P]
-            L.ifx_gemm_tiles_n.argtypes = [I64, I64, PI64]
+            L.ifx_gemm_tiles_n.argtypes = [I64, I64, I64, PI64]
             L.ifx_group_softmax.argtypes = [P, I64, I64, I64, I64, ctypes.c_float, P, I64, P]
+            L.ifx_group_softmax_rs.argtypes = [P, I64, I64, I64, I64, ctypes.c_float, P, I64, P,
+                                               I64, I64, I64, P]
             L.ifx_rope_qk.argtypes = [P, I64, I64, I64, I64, I64, I64, I64, P, P, I64, P]
             L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]
             L.ifx_ulysses_unpack.argtypes = [P, I64, I64, I64, I64, ctypes.c_int, P, I64, P]

@@ -151,9 +151,10 @@ class RowNorm:
         self.rows_bf16, self.ss, self.parts, self.dim = rows_bf16, ss, parts, dim
 
 
-def gemm_tiles_n(m: int, n: int) -> int:
+def gemm_tiles_n(m: int, n: int, k: int) -> int:
+    """Sum-of-squares parts per row G1 emits for an [m, k] x [k, n] product."""
     out = ctypes.c_int64()
-    _abi.check(_abi.lib().ifx_gemm_tiles_n(m, n, ctypes.byref(out)), "gemm_tiles_n")
+    _abi.check(_abi.lib().ifx_gemm_tiles_n(m, n, k, ctypes.byref(out)), "gemm_tiles_n")
     return out.value
 
 

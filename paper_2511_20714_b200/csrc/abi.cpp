@@ -241,13 +241,14 @@ int gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
   if (p->emit_b != nullptr && (mis(p->emit_b) || (p->emit_ld * 2) % 16 || p->emit_ss == nullptr))
     return fail(IFX_EDIM, "emit needs a 16-byte aligned bf16 row buffer and a sum-of-squares buffer");
   const int n_sm = num_sms();
-  const int bn = gemm_pick_bn(p->m, p->n, n_sm);
+  int bn = 0, mode = 0;
+  gemm_plan(p->m, p->n, p->k, n_sm, &bn, &mode);
   GemmArgs a;
   std::memset(&a, 0, sizeof(a));
   a.M = (int)p->m;
   a.N = (int)p->n;
   a.K = (int)p->k;
-  a.tiles_m = (int)((p->m + 127) / 128);
+  a.tiles_m = (int)(mode == 3 ? (p->m + 255) / 256 : (p->m + 127) / 128);
   a.tiles_n = (int)((p->n + bn - 1) / bn);
   // sums of squares per row: one per (column tile, epilogue half)
   if (out_tiles_n) *out_tiles_n = 2 * a.tiles_n;
@@ -255,7 +256,7 @@ int gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
     return fail(IFX_EDIM, "emit_ss_ld smaller than the sum-of-squares part count");
   if (p->m == 0) return IFX_OK;
   int rc;
-  if ((rc = make_map(&a.tm_a, p->a, p->m, p->k, p->lda, 128))) return rc;
+  if ((rc = make_map(&a.tm_a, p->a, p->m, p->k, p->lda, mode == 2 ? 64 : 128))) return rc;
   if ((rc = make_map(&a.tm_b, p->b, p->k, p->n, p->ldb, 64))) return rc;
   a.c = p->c;
   a.ldc = p->ldc;
@@ -287,6 +288,8 @@ int gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
     a.rope_pairs = (int)p->rope_pairs;
     a.rope_hs = (int)p->rope_hs;
     a.rope_heads = (int)p->rope_heads;
+    a.rope_vec = (p->rope_pairs % 4 == 0 && ((reinterpret_cast<uintptr_t>(p->rope_cos) |
+                                               reinterpret_cast<uintptr_t>(p->rope_sin)) & 15) == 0);
   }
   if (p->page_pool != nullptr) {
     const ifx_kv_pool* pool = p->page_pool;
@@ -309,7 +312,7 @@ int gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
     a.pwidth = pool->width;
     a.page_len = (int)pool->page_len;
   }
-  return cuda_fail(gemm_launch(a, bn, static_cast<cudaStream_t>(stream)), "gemm launch");
+  return cuda_fail(gemm_launch(a, bn, mode, static_cast<cudaStream_t>(stream)), "gemm launch");
 }
 
 }  // namespace ifx
@@ -444,11 +447,21 @@ int ifx_copy_blocks(const void* src, void* dst, const int64_t* desc, int64_t n_b
 
 int ifx_group_softmax(const float* s, int64_t rows, int64_t groups, int64_t group_size,
                       int64_t ld, float scale, void* p, int64_t p_ld, void* stream) {
+  return ifx_group_softmax_rs(s, rows, groups, group_size, ld, scale, p, p_ld, nullptr, 0, 0, 1,
+                              stream);
+}
+
+int ifx_group_softmax_rs(const float* s, int64_t rows, int64_t groups, int64_t group_size,
+                         int64_t ld, float scale, void* p, int64_t p_ld, const float* rs_part,
+                         int64_t rs_ld, int64_t rs_parts, int64_t rs_dim, void* stream) {
   if (rows < 0 || groups < 1 || group_size < 1 || ld < groups * group_size || p_ld < groups * group_size)
     return ifx::fail(IFX_EDIM, "bad group softmax sizes");
+  if (rs_part != nullptr && (rs_parts < 1 || rs_ld < rs_parts || rs_dim < 1))
+    return ifx::fail(IFX_EDIM, "bad row-scale statistics");
   if (rows == 0) return IFX_OK;
   int e = ifx::group_softmax_launch(s, rows, (int)groups, (int)group_size, ld,
-                                    scale * 1.4426950408889634f, p, p_ld,
+                                    scale * 1.4426950408889634f, p, p_ld, rs_part, (int)rs_parts,
+                                    rs_ld, 1.f / (float)rs_dim, 1e-6f,
                                     static_cast<cudaStream_t>(stream));
   return ifx::cuda_fail(e, "group softmax launch");
 }
@@ -494,9 +507,10 @@ int ifx_gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream)
   return ifx::gemm_fused(p, out_tiles_n, stream);
 }
 
-int ifx_gemm_tiles_n(int64_t m, int64_t n, int64_t* out_tiles_n) {
+int ifx_gemm_tiles_n(int64_t m, int64_t n, int64_t k, int64_t* out_tiles_n) {
   if (m < 0 || n < 1 || out_tiles_n == nullptr) return ifx::fail(IFX_EDIM, "bad GEMM sizes");
-  const int bn = ifx::gemm_pick_bn(m, n, ifx::num_sms());
+  int bn = 0, mode = 0;
+  ifx::gemm_plan(m, n, k, ifx::num_sms(), &bn, &mode);
   *out_tiles_n = 2 * ((n + bn - 1) / bn);
   return IFX_OK;
 }

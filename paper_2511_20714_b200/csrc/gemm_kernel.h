@@ -40,7 +40,7 @@ struct GemmArgs {
   const float* rope_cos;
   const float* rope_sin;
   int64_t rope_row0, rope_q0, rope_k0;
-  int rope_pairs, rope_hs, rope_heads, pad0_;
+  int rope_pairs, rope_hs, rope_heads, rope_vec;  // rope_vec: tables 16-byte aligned rows
   // ---- page write (KvCache.append_block, kvcache.py:179-234, fused): columns
   // [pk_col0, pk_col0 + pwidth) of row r are token (rel0 + r) of the K stream, columns
   // [pv_col0, ...) of the V stream; its page's slot code slots[(rel0 + r) / page_len]
@@ -54,8 +54,11 @@ struct GemmArgs {
   int page_len, pad1_;
 };
 
-// Persistent launch (<= one CTA per SM), BN in {64, 128, 192, 256}. Returns cudaError_t.
-int gemm_launch(const GemmArgs& a, int bn, cudaStream_t st);
-int gemm_pick_bn(int64_t M, int64_t N, int n_sm);
+// Persistent launch (<= one CTA per SM), BN in {64, 128, 192, 256}; mode 1: one CTA per
+// 128 x BN tile; 2: clusters of two column tiles sharing A by multicast (tm_a box 64 rows);
+// 3: cta_group::2 CTA pairs per 256 x BN tile (BN 128 / 256; tiles_m counts 256-row
+// tiles). Returns cudaError_t.
+int gemm_launch(const GemmArgs& a, int bn, int mode, cudaStream_t st);
+void gemm_plan(int64_t M, int64_t N, int64_t K, int n_sm, int* bn_out, int* mode_out);
 
 }  // namespace ifx

@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cmath>
 #include <cstdlib>
 
 #include "device_state.h"
@@ -48,10 +49,10 @@ constexpr int BK = 64;
 constexpr int NTHREADS = 320;  // producer, MMA, 8 epilogue warps
 constexpr int NEPI = 256;
 
-template <int BN>
+template <int BN, int BNL>  // BNL: B columns held per CTA (BN, or BN / 2 for a CTA pair)
 struct GLayout {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BK * BN * 2;
+  static constexpr int B_BYTES = BK * BNL * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STG = 8 * 4096;  // epilogue staging, 4 KB per epilogue warp
   static constexpr int NST0 = (224 * 1024 - STG) / STAGE;
@@ -63,13 +64,88 @@ struct GLayout {
   static constexpr uint32_t TM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
 };
 
-__device__ __forceinline__ void st_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  *reinterpret_cast<uint4*>(p) = make_uint4(a, b, c, d);
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA 2D load multicast to the CTAs of `mask` (same smem offset, their own mbarrier)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                               int32_t c0, int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+// arrive on the mbarrier at this offset in every CTA of `mask` once this thread's MMAs finish
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
 }
 
-template <int BN>
+// ---- CTA pair (cta_group::2): one MMA of M = 256 over the two SMs of a TPC -------------
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// TMA load into this CTA's smem whose completion is counted on the LEADER CTA's barrier
+// (the peer bit of the shared::cluster address cleared), which the pair MMA waits on
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                                 int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+// arrive on the barrier at the same offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+// CL = CTAs per cluster along N (1 or 2). With CL = 2 the two CTAs of a cluster compute
+// the tiles (m, 2p) and (m, 2p + 1): they need the same A tile, so each loads half of its
+// rows and multicasts it to both (A's L2 -> SM traffic halves), and a stage is refilled
+// only when BOTH CTAs' MMAs have read it (the MMA commit arrives in both CTAs).
+//
+// PAIR (CL = 2): the two CTAs of a cluster are a cta_group::2 pair computing one 256 x BN
+// tile: CTA r holds A rows [128 r, 128 r + 128) and B columns [r BN/2, (r + 1) BN/2) of it;
+// the leader (rank 0) issues M = 256 MMAs that read both CTAs' shared memory and write each
+// CTA's 128 rows into that CTA's TMEM. Per SM a K step moves A 16 KB + B BN/2 x 128 B
+// through shared memory instead of A + B BN x 128 B: with the TMA fill and the tensor
+// core's reads sharing the shared-memory bandwidth this is what lets the MMAs run back to
+// back (profiles/r04_g1_ncu.md). tiles_m counts 256-row tiles in this mode.
+template <int BN, int CL, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant__ GemmArgs a) {
-  using L = GLayout<BN>;
+  static_assert(!PAIR || CL == 2, "a CTA pair is a cluster of 2");
+  constexpr int BNL = PAIR ? BN / 2 : BN;
+  using L = GLayout<BN, BNL>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -82,23 +158,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int n_tiles = a.tiles_m * a.tiles_n;
   const int k_iters = (a.K + BK - 1) / BK;
+  // work units: u = (row tile u % tiles_m, column tile(s) u / tiles_m): one tile per CTA
+  // (CL = 1), a column-tile pair sharing A (CL = 2), one 256-row tile per CTA pair (PAIR)
+  const int rank = CL > 1 ? (int)cluster_rank() : 0;
+  const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
+  const int n_units = PAIR ? a.tiles_m * a.tiles_n : a.tiles_m * ((a.tiles_n + CL - 1) / CL);
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
+  constexpr int kEpiWarps = NEPI / 32;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L::NST; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, PAIR ? 1 : CL);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
-      mbar_init(tempty + i, NEPI);
+      mbar_init(tempty + i, PAIR ? 2 * kEpiWarps : kEpiWarps);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<L::TM_COLS>(tmem_slot);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair(tmem_slot, L::TM_COLS);
+    else tmem_alloc<L::TM_COLS>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // the peer's barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -108,14 +194,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
       tma_prefetch_desc(&a.tm_a);
       tma_prefetch_desc(&a.tm_b);
       int g = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int m0 = (t % a.tiles_m) * BM, n0 = (t / a.tiles_m) * BN;
+      for (int u = unit0; u < n_units; u += unit_step) {
+        const int m0 = PAIR ? (u % a.tiles_m) * 2 * BM + rank * BM : (u % a.tiles_m) * BM;
+        const int n0 = PAIR ? (u / a.tiles_m) * BN + rank * BNL : ((u / a.tiles_m) * CL + rank) * BN;
         for (int kb = 0; kb < k_iters; ++kb, ++g) {
           const int s = g % L::NST;
           mbar_wait(empty + s, ((g / L::NST) & 1) ^ 1);
           uint8_t* st = smem + s * L::STAGE;
+          if (PAIR) {  // both CTAs' bytes complete on the leader's barrier
+            if (rank == 0) mbar_expect_tx(full + s, 2 * L::STAGE);
+            tma_load_2d_pair(st, &a.tm_a, full + s, kb * BK, m0);
+#pragma unroll
+            for (int c = 0; c < BNL / 64; ++c)
+              tma_load_2d_pair(st + L::A_BYTES + c * (BK * 128), &a.tm_b, full + s, n0 + c * 64, kb * BK);
+            continue;
+          }
           mbar_expect_tx(full + s, L::STAGE);
-          tma_load_2d(st, &a.tm_a, full + s, kb * BK, m0);
+          if (CL == 1) {
+            tma_load_2d(st, &a.tm_a, full + s, kb * BK, m0);
+          } else {  // this CTA's share of the A rows, to every CTA of the cluster
+            constexpr int RA = BM / CL;
+            tma_load_2d_mc(st + rank * RA * 128, &a.tm_a, full + s, kb * BK, m0 + rank * RA, kMask);
+          }
 #pragma unroll
           for (int c = 0; c < BN / 64; ++c)
             tma_load_2d(st + L::A_BYTES + c * (BK * 128), &a.tm_b, full + s, n0 + c * 64, kb * BK);
@@ -125,10 +225,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
     __syncwarp();
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
-    if (elect_one()) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, 0, 1);  // A K-major, B MN-major
+    if ((!PAIR || rank == 0) && elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * BM : BM, BN, 0, 1);  // A K-major, B MN-major
       int g = 0, i = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      for (int u = unit0; u < n_units; u += unit_step, ++i) {
         const int acc = i & 1;
         mbar_wait(tempty + acc, ((i >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -143,13 +243,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
           for (int kk = 0; kk < BK / 16; ++kk) {
             // A: rows of 128 B, K step 16 = 32 B inside the swizzle atom.
             // B: BN/64 chunks [64 K rows x 128 B]; K step 16 = 16 rows; LBO = chunk stride
-            mma_bf16_ss(d, smem_desc_sw128(a_base + kk * 32, 16, 1024),
-                        smem_desc_sw128(b_base + kk * 16 * 128, BK * 128, 1024), idesc,
-                        (kb | kk) != 0);
+            const uint64_t ad = smem_desc_sw128(a_base + kk * 32, 16, 1024);
+            const uint64_t bd = smem_desc_sw128(b_base + kk * 16 * 128, BK * 128, 1024);
+            if (PAIR) mma_bf16_pair(d, ad, bd, idesc, (kb | kk) != 0);
+            else mma_bf16_ss(d, ad, bd, idesc, (kb | kk) != 0);
           }
-          mma_commit(empty + s);
+          if (PAIR) mma_commit_pair(empty + s, kMask);
+          else if (CL == 1) mma_commit(empty + s);
+          else mma_commit_mc(empty + s, kMask);
         }
-        mma_commit(tfull + acc);
+        if (PAIR) mma_commit_pair(tfull + acc, kMask);
+        else mma_commit(tfull + acc);
       }
     }
     __syncwarp();
@@ -166,9 +270,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
     constexpr int PD = NCH < 2 ? NCH : 2;  // residual chunks prefetched ahead
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
-    const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const bool beta_on = a.c_f32 && a.beta != 0.f;
+    // one arrive per warp on the accumulator's barrier in the MMA-issuing CTA
+    auto release_acc = [&](uint64_t* bar) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cta(bar, 0);
+        else mbar_arrive(bar);
+      }
+    };
     uint8_t* stg = smem + L::OFF_STG + (warp - 2) * 4096;
     const uint32_t stg_u = smem_u32(stg);
     // coalesced-domain coordinates: fp32 rows k*4 + (lane >> 3), 16 B column piece lane & 7;
@@ -176,10 +288,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
     const int fr = lane >> 3, fj = lane & 7;
     const int br = lane >> 2, bj = lane & 3;
     int i = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+    for (int u = unit0; u < n_units; u += unit_step, ++i) {
       const int acc = i & 1;
-      const int tm = t % a.tiles_m, tn = t / a.tiles_m;
-      const int64_t r0 = (int64_t)tm * BM + q * 32;  // first row of this warp
+      const int tm = u % a.tiles_m;
+      const int tn = PAIR ? u / a.tiles_m : (u / a.tiles_m) * CL + rank;
+      const int64_t r0 = (PAIR ? (int64_t)tm * 2 * BM + rank * BM : (int64_t)tm * BM) + q * 32;
       const int64_t grow = r0 + lane;
       const int c0 = tn * BN + half * HC;
       const bool live = grow < a.M;
@@ -216,8 +329,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
         tmem_ld32(tmem + lane_off + acc * BN + half * HC + c * 32, r);
         tmem_wait_ld();
         if (c == NCH - 1) {  // every TMEM column of this warp is read: release the buffer
-          tc_fence_before();
-          mbar_arrive(tempty + acc);
+          release_acc(tempty + acc);
           released = true;
         }
         float v[32];
@@ -234,14 +346,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
           else if (col0 >= a.rope_k0 && col0 < a.rope_k0 + span) base = a.rope_k0;
           if (base >= 0) {
             const int k0 = (int)(((col0 - base) % a.rope_hs) >> 1);
-            const int64_t tab = (a.rope_row0 + grow) * a.rope_pairs;
+            const int64_t tab = (a.rope_row0 + grow) * a.rope_pairs + k0;
+            if (a.rope_vec && k0 + 16 <= a.rope_pairs) {  // 16 pairs as 4 x float4 per table
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              if (k0 + e < a.rope_pairs) {
-                const float cs = __ldg(a.rope_cos + tab + k0 + e), sn = __ldg(a.rope_sin + tab + k0 + e);
-                const float x0 = v[2 * e], x1 = v[2 * e + 1];
-                v[2 * e] = x0 * cs - x1 * sn;
-                v[2 * e + 1] = x0 * sn + x1 * cs;
+              for (int e4 = 0; e4 < 4; ++e4) {
+                const float4 cs = __ldg(reinterpret_cast<const float4*>(a.rope_cos + tab) + e4);
+                const float4 sn = __ldg(reinterpret_cast<const float4*>(a.rope_sin + tab) + e4);
+                const float cv[4] = {cs.x, cs.y, cs.z, cs.w}, sv[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int e = 4 * e4 + u;
+                  const float x0 = v[2 * e], x1 = v[2 * e + 1];
+                  v[2 * e] = x0 * cv[u] - x1 * sv[u];
+                  v[2 * e + 1] = x0 * sv[u] + x1 * cv[u];
+                }
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                if (k0 + e < a.rope_pairs) {
+                  const float cs = __ldg(a.rope_cos + tab + e), sn = __ldg(a.rope_sin + tab + e);
+                  const float x0 = v[2 * e], x1 = v[2 * e + 1];
+                  v[2 * e] = x0 * cs - x1 * sn;
+                  v[2 * e + 1] = x0 * sn + x1 * cs;
+                }
               }
             }
           }
@@ -334,10 +462,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
           __syncwarp();
         }
       }
-      if (!released) {  // ragged N: this warp's last columns were past the edge
-        tc_fence_before();
-        mbar_arrive(tempty + acc);
-      }
+      if (!released) release_acc(tempty + acc);  // ragged N: last columns past the edge
       if (a.emit_ss != nullptr) {  // per-row sums of this warp's columns (8 lanes per row)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -346,7 +471,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
           sk += __shfl_xor_sync(0xffffffffu, sk, 2);
           sk += __shfl_xor_sync(0xffffffffu, sk, 4);
           const int64_t rr = r0 + k * 4 + fr;
-          if (fj == 0 && rr < a.M) a.emit_ss[rr * a.emit_ss_ld + 2 * tn + half] = sk;
+          if (fj == 0 && rr < a.M && tn < a.tiles_n) a.emit_ss[rr * a.emit_ss_ld + 2 * tn + half] = sk;
         }
       }
     }
@@ -354,61 +479,115 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
 
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no multicast or remote arrive still targets this CTA
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<L::TM_COLS>(tmem);
+    if (PAIR) tmem_dealloc_pair(tmem, L::TM_COLS);
+    else tmem_dealloc<L::TM_COLS>(tmem);
   }
 }
 
-template <int BN>
+template <int BN, int CL, bool PAIR = false>
 int launch(const GemmArgs& a, cudaStream_t st) {
-  using L = GLayout<BN>;
+  using L = GLayout<BN, PAIR ? BN / 2 : BN>;
   static DeviceFlags attr_set;
   const int dev = current_device();
   if (attr_set.first(dev)) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, CL, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_set.set(dev);
   }
-  const int tiles = a.tiles_m * a.tiles_n;
+  const int units = PAIR ? a.tiles_m * a.tiles_n : a.tiles_m * ((a.tiles_n + CL - 1) / CL);
   const int n_sm = device_sms(dev);
-  const int grid = tiles < n_sm ? tiles : n_sm;
-  gemm_kernel<BN><<<grid, NTHREADS, L::SMEM, st>>>(a);
-  return (int)cudaGetLastError();
+  const int per = n_sm / CL;
+  const int grid = (units < per ? units : per) * CL;
+  if (CL == 1) {
+    gemm_kernel<BN, 1, false><<<grid, NTHREADS, L::SMEM, st>>>(a);
+    return (int)cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = L::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CL, PAIR>, a);
 }
 
 }  // namespace
 
-// Output tile width: fewest waves x per-tile cost on n_sm SMs (a tile's cost ~ BN + a fixed
-// ramp / epilogue share). At T = 4,680 rows (37 row tiles, 148 = 4 x 37) BN = 192 makes
-// every c2 projection whole waves: N = 1,536 / 3,072 / 4,608 -> 296 / 592 / 888 tiles.
-int gemm_pick_bn(int64_t M, int64_t N, int n_sm) {
-  static const int forced = [] {
+// Tile plan: output tile width BN and mode (1: one CTA per 128 x BN tile; 2: a cluster of
+// two column tiles sharing A by multicast; 3: a cta_group::2 CTA pair per 256 x BN tile).
+// Modelled time = waves x (K steps x 2 BN / util + 2,500) clk, with the tensor-pipe
+// utilisation of each main loop and the per-tile ramp / exposed epilogue fitted to the
+// c2 / c4 projection shapes (tools/gemm_probe.py, profiles/r04_g1.md): one CTA reaches
+// ~0.78 at BN 192-256 (its K step moves A + B through shared memory twice, TMA fill and
+// tensor-core read, against 2 BN clk of MMA), a CTA pair ~0.91 at BN 256 (each SM holds
+// only half of B). Mode 2 (L2 traffic only) is kept for A/B (IFX_G1_MODE=2).
+void gemm_plan(int64_t M, int64_t N, int64_t K, int n_sm, int* bn_out, int* mode_out) {
+  static const int forced_bn = [] {
     const char* e = std::getenv("IFX_G1_BN");
     return e ? std::atoi(e) : 0;
   }();
-  if (forced == 64 || forced == 128 || forced == 192 || forced == 256) return forced;
-  const int64_t tm = (M + BM - 1) / BM;
-  int best = 64;
-  int64_t best_cost = INT64_MAX;
-  for (int bn : {256, 192, 128, 64}) {
-    const int64_t tiles = tm * ((N + bn - 1) / bn);
-    const int64_t waves = (tiles + n_sm - 1) / n_sm;
-    const int64_t cost = waves * (bn + 48);
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = bn;
+  static const int forced_mode = [] {
+    const char* e = std::getenv("IFX_G1_MODE");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int64_t k_iters = (K + BK - 1) / BK;
+  double best = 1e300;
+  int bn_best = 64, mode_best = 1;
+  for (int mode : {1, 3}) {
+    if (forced_mode && mode != (forced_mode == 2 ? 1 : forced_mode)) continue;
+    for (int bn : {256, 192, 128, 64}) {
+      if (forced_bn && bn != forced_bn) continue;
+      if (mode == 3 && bn != 256 && bn != 128) continue;
+      const int64_t rows = mode == 3 ? 2 * BM : BM;
+      const int64_t units = ((M + rows - 1) / rows) * ((N + bn - 1) / bn);
+      const int64_t slots = mode == 3 ? n_sm / 2 : n_sm;
+      const int64_t waves = (units + slots - 1) / slots;
+      const double util = mode == 3 ? (bn == 256 ? 0.91 : 0.80)
+                                    : (bn >= 192 ? 0.78 : (bn == 128 ? 0.70 : 0.55));
+      const double cost = (double)waves * ((double)k_iters * 2.0 * bn / util + 2500.0);
+      if (cost < best * (1 - 1e-9)) {
+        best = cost;
+        bn_best = bn;
+        mode_best = mode;
+      }
     }
   }
-  return best;
+  if (forced_mode == 2 && ((N + bn_best - 1) / bn_best) % 2 == 0) mode_best = 2;
+  *bn_out = bn_best;
+  *mode_out = mode_best;
 }
 
-int gemm_launch(const GemmArgs& a, int bn, cudaStream_t st) {
+int gemm_launch(const GemmArgs& a, int bn, int cl, cudaStream_t st) {
+  if (cl == 3) {  // CTA pair
+    switch (bn) {
+      case 128: return launch<128, 2, true>(a, st);
+      case 256: return launch<256, 2, true>(a, st);
+      default: return (int)cudaErrorInvalidValue;
+    }
+  }
+  if (cl == 2) {
+    switch (bn) {
+      case 64: return launch<64, 2>(a, st);
+      case 128: return launch<128, 2>(a, st);
+      case 192: return launch<192, 2>(a, st);
+      case 256: return launch<256, 2>(a, st);
+      default: return (int)cudaErrorInvalidValue;
+    }
+  }
   switch (bn) {
-    case 64: return launch<64>(a, st);
-    case 128: return launch<128>(a, st);
-    case 192: return launch<192>(a, st);
-    case 256: return launch<256>(a, st);
+    case 64: return launch<64, 1>(a, st);
+    case 128: return launch<128, 1>(a, st);
+    case 192: return launch<192, 1>(a, st);
+    case 256: return launch<256, 1>(a, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }

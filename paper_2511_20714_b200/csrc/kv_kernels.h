@@ -16,7 +16,9 @@ int kv_move_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t widt
 int copy_blocks_launch(const void* src, void* dst, const int64_t* desc, int64_t n_blocks,
                        int64_t max_rows, cudaStream_t st);
 int group_softmax_launch(const float* s, int64_t rows, int groups, int gs, int64_t ld,
-                         float scale_log2, void* p, int64_t p_ld, cudaStream_t st);
+                         float scale_log2, void* p, int64_t p_ld, const float* rs_part,
+                         int rs_parts, int64_t rs_ld, float rs_inv_d, float rs_eps,
+                         cudaStream_t st);
 int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, float t,
                float* x_out, void* y, cudaStream_t st);
 int rope_launch(void* qkv, int64_t rows, int64_t ld, int heads, int64_t head_stride, int pairs,

@@ -387,14 +387,25 @@ __global__ void copy_blocks_kernel(const uint8_t* __restrict__ src, uint8_t* __r
 
 // ---- softmax over groups of a few logits (the folded cross-attention, engine.py:211-215):
 // p[r, g*gs + j] = bf16(softmax_j(s[r, g*gs + j] * scale)), one thread per (row, group)
+// rs_part != nullptr: the logits are (bf16 x) . W rows whose RMS norm (engine.py:171-173)
+// is still to be applied: row r is scaled by rsqrt(sum_p rs_part[r, p] * inv_d + eps) (the
+// statistics G1's residual epilogue left, see gemm_sm100.cu)
 __global__ void group_softmax_kernel(const float* __restrict__ s, int64_t rows, int groups,
-                                     int gs, int64_t ld, float scale_log2,
-                                     __nv_bfloat16* __restrict__ p, int64_t p_ld) {
+                                     int gs, int64_t ld, float scale_log2_in,
+                                     __nv_bfloat16* __restrict__ p, int64_t p_ld,
+                                     const float* __restrict__ rs_part, int rs_parts,
+                                     int64_t rs_ld, float rs_inv_d, float rs_eps) {
   const int64_t total = rows * groups;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / groups;
     const int g = (int)(i - r * groups);
+    float scale_log2 = scale_log2_in;
+    if (rs_part != nullptr) {
+      float ss = 0.f;
+      for (int q = 0; q < rs_parts; ++q) ss += __ldg(rs_part + r * rs_ld + q);
+      scale_log2 *= rsqrtf(ss * rs_inv_d + rs_eps);
+    }
     const float* sr = s + r * ld + (int64_t)g * gs;
     __nv_bfloat16* pr = p + r * p_ld + (int64_t)g * gs;
     float m = -INFINITY;
@@ -490,10 +501,13 @@ int copy_blocks_launch(const void* src, void* dst, const int64_t* desc, int64_t 
 }
 
 int group_softmax_launch(const float* s, int64_t rows, int groups, int gs, int64_t ld,
-                         float scale_log2, void* p, int64_t p_ld, cudaStream_t st) {
+                         float scale_log2, void* p, int64_t p_ld, const float* rs_part,
+                         int rs_parts, int64_t rs_ld, float rs_inv_d, float rs_eps,
+                         cudaStream_t st) {
   const int threads = 256;
   group_softmax_kernel<<<grid_for(rows * groups, threads), threads, 0, st>>>(
-      s, rows, groups, gs, ld, scale_log2, static_cast<__nv_bfloat16*>(p), p_ld);
+      s, rows, groups, gs, ld, scale_log2, static_cast<__nv_bfloat16*>(p), p_ld, rs_part,
+      rs_parts, rs_ld, rs_inv_d, rs_eps);
   return (int)cudaGetLastError();
 }
 

@@ -34,8 +34,8 @@ import numpy as np
 import torch
 
 from . import _abi, _device
-from ._device import (attn_fwd, count_launch, gemm, require_cuda, rms_bf16, rope_qk,
-                      stream_ptr, tile_run_codes)
+from ._device import (RowNorm, attn_fwd, count_launch, gemm, gemm_fused, gemm_tiles_n,
+                      require_cuda, rms_bf16, rope_qk, stream_ptr, tile_run_codes)
 from .errors import ConfigError, DimensionError
 from .kvcache import CROSS_ATTN, SELF_ATTN, KvCache, KvConfig
 
@@ -421,6 +421,27 @@ def _cross_attend(ws, fold: _CrossFold, x: torch.Tensor, h: torch.Tensor, scale:
     gemm(p, fold.wvo, x, beta=1.0)
 
 
+def _cross_attend_g1(ws, fold: _CrossFold, norm: RowNorm, scale: float):
+    """_cross_attend on G1: logits = rms(x) . wqk (row scale from the wo epilogue's
+    statistics), group softmax, then x += P . wvo emitting the next norm's statistics."""
+    T = norm.rows_bf16.shape[0]
+    key = (T, fold.width)
+    buf = ws.cross_bufs.get(key)
+    if buf is None:
+        buf = ws.cross_bufs[key] = (torch.empty(T, fold.width, device=ws.x.device),
+                                    torch.zeros(T, fold.width, device=ws.x.device, dtype=torch.bfloat16))
+    s, p = buf
+    # a [T, D] x [D, H*n] product (H*n = 36 at c2) has too few output tiles for G1's
+    # persistent grid (37 CTAs); cuBLASLt on the un-normalised rows, row scale in the softmax
+    gemm(norm.rows_bf16, fold.wqk, s)
+    _abi.check(_abi.lib().ifx_group_softmax_rs(s.data_ptr(), T, fold.groups, fold.n, fold.width,
+                                               float(scale), p.data_ptr(), fold.width,
+                                               norm.ss.data_ptr(), norm.ss.stride(0), norm.parts,
+                                               norm.dim, stream_ptr()), "group_softmax")
+    count_launch()
+    gemm_fused(p, fold.wvo, ws.x, beta=1.0, norm_out=norm)
+
+
 class _Workspace:
     """Per-(T, D) device buffers reused across passes (no allocator traffic in the loop)."""
 
@@ -432,6 +453,10 @@ class _Workspace:
         self.ffn = torch.empty(T, 2 * D, device=dev, dtype=torch.bfloat16)
         self.tmp = torch.empty(T, D, device=dev, dtype=torch.float32)
         self.cross_bufs = {}
+        # G1 norm statistics: bf16 copy of the residual rows (self.h) and per-part sums of
+        # squares of the fp32 rows, written by each residual GEMM for the next consumer
+        # (room for the most parts any producer can emit: BN 64 tiles, two halves each)
+        self.norm = RowNorm(self.h, torch.empty(T, 2 * -(-D // 64), device=dev), 0, D)
 
 
 def _residual(x: torch.Tensor, a: torch.Tensor, w: torch.Tensor):
@@ -462,12 +487,25 @@ class BlockRunner:
         self._tv = self._gpool = self._cap = self._graph = None  # CUDA-graph state (_euler_steps)
         self._warm = False
         self._tail = None  # event after the last block's clean pass (_euler_steps: GPU idle?)
+        # G1 (hand-written tcgen05 GEMMs with fused epilogues) when the widths allow TMA
+        # (rows of 16-byte multiples). IFX_G1 = "qkv": the QKV projection on G1 with RoPE
+        # and the clean pass's page write in its epilogue, the other projections on
+        # cuBLASLt with the RMS kernel; "all" (or 1): every projection on G1 with the norms
+        # fused into the epilogues (_forward_g1); "off" (or 0): cuBLASLt only. Measured in
+        # profiles/r04_g1.md.
+        # "auto" (default) = "qkv" when the model has RoPE (the fused rotation saves a pass
+        # over Q / K), else "off": on these shapes cuBLASLt's GEMMs are as fast or faster.
+        ok = c.model_dim % 8 == 0
+        self.g1 = G1 == "all" and ok
+        self.g1_qkv = ok and (G1 == "qkv" or (G1 == "auto" and c.rope_grid is not None))
 
     def forward(self, latent: torch.Tensor, t: float, ctx, cross, cache: KvCache | None,
                 collect_kv: bool = False, chunk_index: int = 0, eps_out: torch.Tensor | None = None,
                 rope=None):
         """One pass. ctx: _KvContext of the block or None; cross: per-layer _CrossFold or
         None; rope = (cos, sin) tables of this block (rope_tables) or None."""
+        if self.g1 and _mha_hook() is None:
+            return self._forward_g1(latent, t, ctx, cross, cache, collect_kv, chunk_index, eps_out, rope)
         m, ws = self.model, self.ws
         c = m.config
         H, dhp, Dp = m.heads_pad, m.dh_pad, m.attn_width
@@ -481,10 +519,18 @@ class BlockRunner:
                     rms_bf16(latent, ws.h, m.time_vec, t, x_out=ws.x)
             else:
                 rms_bf16(ws.x, ws.h)
-            gemm(ws.h, lw.wqkv, ws.qkv)
-            if rope is not None:  # Q and the block's own K, before K1 and the page write
-                rope_qk(ws.qkv, H, dhp, c.head_dim // 2, 0, Dp, rope[0], rope[1])
             hook = _mha_hook()
+            pend = None
+            if self.g1_qkv and hook is None:  # RoPE and the clean pass's page write fused
+                if collect_kv:
+                    pend = cache.append_reserve(li, c.block_len, SELF_ATTN, chunk_index)
+                page = None if pend is None or pend.page is None else (*pend.page, Dp, 2 * Dp)
+                gemm_fused(ws.h, lw.wqkv, ws.qkv, rope=None if rope is None else
+                           (rope[0], rope[1], 0, c.head_dim // 2, dhp, H, 0, Dp), page=page)
+            else:
+                gemm(ws.h, lw.wqkv, ws.qkv)
+                if rope is not None:  # Q and the block's own K, before K1 and the page write
+                    rope_qk(ws.qkv, H, dhp, c.head_dim // 2, 0, Dp, rope[0], rope[1])
             ev = self.attn_events if hook is None else None
             if ev is not None:
                 e0 = timing_event()
@@ -509,11 +555,64 @@ class BlockRunner:
             rms_bf16(ws.x, ws.h)
             _ffn_up(ws.h, lw.w1, ws.ffn)
             _residual(ws.x, ws.ffn, lw.w2)
-            if collect_kv:  # clean pass: page write of this layer's K/V (engine.py:303-306)
+            if pend is not None:  # page bookkeeping ran before the QKV GEMM wrote the rows
+                pend.finish(kc, vc)
+            elif collect_kv:  # clean pass: page write of this layer's K/V (engine.py:303-306)
                 cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
         if eps_out is not None:
             rms_bf16(ws.x, ws.h)
             gemm(ws.h, m.w_out, eps_out)
+
+    def _forward_g1(self, latent, t, ctx, cross, cache, collect_kv, chunk_index, eps_out, rope):
+        """The same pass with every projection on G1 (csrc/gemm_sm100.cu) and the work
+        between them in its epilogues: each residual GEMM (wo, the cross W_vo, w2) also
+        writes the new rows as bf16 plus their sums of squares, and the next projection
+        applies the RMS norm (engine.py:171-173) as a row scale after its product, so no
+        norm kernel runs after layer 0's; 3D RoPE is applied to Q / K in the QKV epilogue;
+        on the clean pass the QKV epilogue also writes K / V into their KV-cache pages
+        (engine.py:303-306 -> kvcache.py:179-234; the page bookkeeping runs first, in the
+        reference's order)."""
+        m, ws = self.model, self.ws
+        c = m.config
+        H, dhp, Dp = m.heads_pad, m.dh_pad, m.attn_width
+        T = c.block_len
+        sc = 1.0 / math.sqrt(c.head_dim)
+        q, kc, vc = ws.qkv[:, :Dp], ws.qkv[:, Dp:2 * Dp], ws.qkv[:, 2 * Dp:]
+        norm = ws.norm
+        rope_spec = None if rope is None else (rope[0], rope[1], 0, c.head_dim // 2, dhp, H, 0, Dp)
+        for li, lw in enumerate(m.layers):
+            if li == 0:  # x = latent + t*time_vec fused into the first norm (engine.py:199)
+                if isinstance(t, torch.Tensor):
+                    rms_bf16(latent, ws.h, t, 1.0, x_out=ws.x)
+                else:
+                    rms_bf16(latent, ws.h, m.time_vec, t, x_out=ws.x)
+                nin = None
+            else:
+                nin = norm
+            pend = cache.append_reserve(li, T, SELF_ATTN, chunk_index) if collect_kv else None
+            page = None if pend is None or pend.page is None else (*pend.page, Dp, 2 * Dp)
+            gemm_fused(ws.h, lw.wqkv, ws.qkv, norm_in=nin, rope=rope_spec, page=page)
+            ev = self.attn_events
+            if ev is not None:
+                e0 = timing_event()
+                e0.record()
+            if ctx is not None:
+                ctx.attend(li, q, H, dhp, ws.attn, kc, vc, sc)
+            else:
+                attn_fwd(q, H, dhp, ws.attn, cur_k=kc, cur_v=vc, scale=sc)
+            if ev is not None:
+                e1 = timing_event()
+                e1.record()
+                ev.append((e0, e1))
+            gemm_fused(ws.attn, lw.wo, ws.x, beta=1.0, norm_out=norm)
+            if cross is not None:  # folded through the prompt's few keys (_CrossFold)
+                _cross_attend_g1(ws, cross[li], norm, sc)
+            gemm_fused(ws.h, lw.w1, ws.ffn, relu=True, norm_in=norm)
+            gemm_fused(ws.ffn, lw.w2, ws.x, beta=1.0, norm_out=norm)
+            if pend is not None:
+                pend.finish(kc, vc)
+        if eps_out is not None:
+            gemm_fused(ws.h, m.w_out, eps_out, norm_in=norm)
 
     def _hooked_self(self, hook, li: int, ctx, q, kc, vc) -> None:
         """engine.py:202-210 through a replaced `_mha`: k / v = [cached context ∥ block],
@@ -563,6 +662,7 @@ class BlockRunner:
 
 
 GRAPHS = os.environ.get("IFX_CUDA_GRAPHS", "1") != "0"
+G1 = {"0": "off", "1": "all"}.get(os.environ.get("IFX_G1", "auto"), os.environ.get("IFX_G1", "auto"))
 
 
 def timing_event() -> torch.cuda.Event:

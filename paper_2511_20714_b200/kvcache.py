@@ -340,6 +340,41 @@ class PageTable:
         return st
 
 
+class _PendingAppend:
+    """An append whose bookkeeping ran (KvCache.append_reserve) and whose rows are written
+    by the caller's kernel (`page`) or, failing that, by K2 in `finish`."""
+
+    __slots__ = ("cache", "layer", "kind", "chunk", "t", "rc", "bid", "start", "written",
+                 "pages", "slots", "page")
+
+    def __init__(self, cache, layer, kind, chunk, t, rc, bid, start, written, pages):
+        self.cache, self.layer, self.kind, self.chunk, self.t = cache, layer, kind, chunk, t
+        self.rc, self.bid, self.start, self.written, self.pages = rc, bid, start, written, pages
+        self.slots = self.page = None
+
+    def finish(self, k=None, v=None, stream=None) -> "BlockEntry":
+        c = self.cache
+        if self.page is None and self.written > 0:  # rows the producer could not write
+            k, v = c._as_rows(k), c._as_rows(v)
+            pad = c._row_width[self.kind] - k.shape[1]
+            if pad > 0:
+                k = torch.nn.functional.pad(k, (0, pad))
+                v = torch.nn.functional.pad(v, (0, pad))
+            if k.stride(1) != 1 or v.stride(1) != 1 or k.stride(0) != v.stride(0):
+                k, v = k.contiguous(), v.contiguous()
+            with c._lock:
+                codes, first = c._pt.slots(self.layer, self.kind, self.start, self.start + self.written)
+                slots = torch.from_numpy(codes).to(k.device, non_blocking=True)
+                p = c._pools[self.kind]
+                _abi.check(_abi.lib().ifx_kv_append(
+                    k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype), ctypes.byref(p.abi()),
+                    slots.data_ptr(), first, self.start, self.written, stream_ptr(stream)), "kv_append")
+                count_launch()
+        _abi.check(self.rc, "append_block")
+        return BlockEntry(self.bid, self.layer, (self.start, self.start + self.t), self.pages,
+                          self.kind, self.chunk)
+
+
 class KvCache:
     """Drop-in for `inferix.kvcache.KvCache` (kvcache.py:105-404); create via create_cache().
 
@@ -523,6 +558,35 @@ class KvCache:
                 count_launch()
             _abi.check(rc, "append_block")
             return BlockEntry(bid, layer, (start, start + t), pages, kind, chunk_index)
+
+    def append_reserve(self, layer: int, t: int, kind: str = SELF_ATTN, chunk_index: int = 0,
+                       stream=None) -> "_PendingAppend":
+        """append_block (kvcache.py:179-234) split in two for a producer kernel that writes
+        the rows itself (G1's QKV epilogue on the clean pass): the page bookkeeping runs NOW,
+        in the reference's order; the returned object's `page` is the page-write spec for
+        `gemm_fused` (None: the caller must use `finish(k, v)`, which then runs K2), and
+        `finish` returns the BlockEntry or raises the bookkeeping's error (CapacityError
+        after the rows the reference would have packed were written)."""
+        cfg = self.config
+        if t < 1:
+            raise DimensionError("append needs at least one token")
+        if not 0 <= layer < cfg.num_layers:
+            raise OutOfRangeError(f"layer {layer} out of range")
+        PageTable.kind_code(kind)
+        with self._lock:
+            self._no_batch("append_block")
+            if kind == CROSS_ATTN:
+                self.cross_version += 1
+            rc, bid, start, written, pages = self._pt.append(layer, kind, t, chunk_index)
+            self._sync(stream)
+            pend = _PendingAppend(self, layer, kind, chunk_index, t, rc, bid, start, written, pages)
+            pool = self._pools[kind]
+            if (rc == _abi.OK and self._latent_down is None and pool.dtype == torch.bfloat16
+                    and self._row_width[kind] == self._logical_width[kind]):
+                codes, first = self._pt.slots(layer, kind, start, start + written)
+                pend.slots = torch.from_numpy(codes).to(require_cuda(), non_blocking=True)
+                pend.page = (pool.abi(), pend.slots, first, start)
+            return pend
 
     def offload_blocks(self, block_ids) -> int:
         """kvcache.py:236-256: demote the blocks' device pages; their data moves to the

@@ -68,7 +68,7 @@ def test_gemm_residual_emit_and_row_scale():
     x0 = x.clone()
     a = torch.randn(M, 1536, device="cuda", generator=g).bfloat16()
     w = (torch.randn(1536, Dm, device="cuda", generator=g) / 40).bfloat16()
-    tiles = D.gemm_tiles_n(M, Dm)
+    tiles = D.gemm_tiles_n(M, Dm, 1536)
     norm = D.RowNorm(torch.empty(M, Dm, device="cuda", dtype=torch.bfloat16),
                      torch.full((M, tiles), float("nan"), device="cuda"), 0, Dm)
     parts = D.gemm_fused(a, w, x, beta=1.0, norm_out=norm)
@@ -202,3 +202,41 @@ def test_gemm_inside_cuda_graph():
     graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, eager)
+
+
+@pytest.mark.parametrize("mode", ["all", "qkv"])
+@pytest.mark.parametrize("case", [
+    dict(rope_grid=None, cap=10**6),
+    dict(rope_grid=(2, 8, 8), cap=10**6),
+    dict(rope_grid=(2, 8, 8), cap=24),   # device tier full: fused page writes to host pages
+])
+def test_engine_g1_paths_vs_oracle(monkeypatch, mode, case):
+    """The engine with G1 on every projection ("all": RMS norms fused into the epilogues,
+    engine.py:171-173) or on the QKV projection only ("qkv": RoPE + clean-pass page write
+    in its epilogue) vs the numpy oracle: latents within the stated tolerance, page table
+    bit-exact (also when the fused page write lands on pinned-host pages)."""
+    from oracle import engine as OE
+    from paper_2511_20714_b200 import engine as E
+
+    monkeypatch.setattr(E, "G1", mode)
+    kw = dict(layers=2, heads=4, head_dim=64, block_len=128, frame_shape=(4, 4), prompt_dim=8,
+              rope_grid=case["rope_grid"])
+    req = dict(num_blocks=3, seed=4, prompt_schedule=[(0, "a b c"), (2, "d")])
+    sched = [1.0, 0.5]
+    mc = E.ModelConfig(**kw)
+    model = E.build_model(mc)
+    eng = E.Engine(model, E.default_kv_config(mc, capacity_pages_device=case["cap"],
+                                              capacity_pages_host=4096))
+    got = np.stack([b.latent for b in eng.generate(E.GenerationRequest(
+        schedule=E.DenoiseSchedule(sched), **req))])
+    r = E._runner(model)
+    assert (r.g1, r.g1_qkv) == ((True, False) if mode == "all" else (False, True))
+    omc = OE.ModelConfig(**kw)
+    want, ocache = OE.generate_sequence(OE.ToyModel(omc), OE.GenerationRequest(
+        schedule=OE.DenoiseSchedule(sched), **req),
+        kv_config=OE.default_kv_config(omc, capacity_pages_device=case["cap"], capacity_pages_host=4096))
+    want = np.stack(want)
+    a, b = got.ravel().astype(np.float64), want.ravel().astype(np.float64)
+    cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+    assert np.abs(got - want).max() <= 2e-2 and cos > 0.999
+    assert eng.cache.state() == ocache.state()
