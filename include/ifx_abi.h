@@ -142,6 +142,19 @@ int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_
 int ifx_kv_gather(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
                   const int64_t* tokens, int64_t token0, int64_t n, void* k_out, void* v_out,
                   void* stream);
+/* K2L / K7L — latent mode (kvcache.py:26-31,201-203,323-325, MLA-style): the page write
+ * stores row . down (down fp32 [d_in, latent_dim] row-major; pool width >= latent_dim, the
+ * rest zero) and the gather returns stored_row . up (up fp32 [latent_dim, d_out]) into
+ * k_out / v_out (row stride out_ld, IFX_F32 or IFX_BF16), both in fp32 arithmetic inside the
+ * copy kernels. Tokens / slots as ifx_kv_append / ifx_kv_gather. */
+int ifx_kv_append_latent(const void* k_src, const void* v_src, int64_t src_ld, int src_type,
+                         int64_t d_in, const float* down, int64_t latent_dim,
+                         const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
+                         int64_t token0, int64_t t, void* stream);
+int ifx_kv_gather_latent(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
+                         const int64_t* tokens, int64_t token0, int64_t n, int64_t latent_dim,
+                         const float* up, int64_t d_out, void* k_out, void* v_out, int64_t out_ld,
+                         int out_type, void* stream);
 /* K6 — whole-page copies between the pools (tier moves of ifx_pt_drain_moves, staging of
  * host pages for attention): moves = device int64 [n][2] (device slot, host slot);
  * dir 0 device -> host, 1 host -> device. */

@@ -40,7 +40,7 @@ EXPORTS = (
     "ifx_pt_clear_cross", "ifx_pt_touch_range", "ifx_pt_touch_indices", "ifx_pt_range",
     "ifx_pt_stats", "ifx_pt_snapshot", "ifx_pt_drain_moves", "ifx_pt_pool_extent", "ifx_pt_slots",
     "ifx_pt_batch_begin", "ifx_pt_batch_end", "ifx_pt_pending",
-    "ifx_kv_append", "ifx_kv_gather", "ifx_kv_move_pages", "ifx_kv_copy_runs", "ifx_host_alloc", "ifx_host_free",
+    "ifx_kv_append", "ifx_kv_gather", "ifx_kv_append_latent", "ifx_kv_gather_latent", "ifx_kv_move_pages", "ifx_kv_copy_runs", "ifx_host_alloc", "ifx_host_free",
     "ifx_dev_alloc", "ifx_dev_free",
     "ifx_attn_fwd", "ifx_attn_workspace_bytes",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_group_softmax", "ifx_group_softmax_rs", "ifx_ulysses_pack", "ifx_ulysses_unpack",
@@ -145,6 +145,10 @@ def lib() -> ctypes.CDLL:
             PPOOL = ctypes.POINTER(KvPool)
             L.ifx_kv_append.argtypes = [P, P, I64, ctypes.c_int, PPOOL, P, I64, I64, I64, P]
             L.ifx_kv_gather.argtypes = [PPOOL, P, I64, P, I64, I64, P, P, P]
+            L.ifx_kv_append_latent.argtypes = [P, P, I64, ctypes.c_int, I64, P, I64, PPOOL, P, I64,
+                                               I64, I64, P]
+            L.ifx_kv_gather_latent.argtypes = [PPOOL, P, I64, P, I64, I64, I64, P, I64, P, P, I64,
+                                               ctypes.c_int, P]
             L.ifx_kv_move_pages.argtypes = [PPOOL, P, I64, ctypes.c_int, P]
             L.ifx_kv_copy_runs.argtypes = [PPOOL, PI64, I64, ctypes.c_int, P]
             L.ifx_host_alloc.argtypes = [I64, ctypes.POINTER(P)]

@@ -349,6 +349,40 @@ int ifx_kv_append(const void* k_src, const void* v_src, int64_t src_ld, int src_
   return ifx::cuda_fail(e, "kv_append launch");
 }
 
+int ifx_kv_append_latent(const void* k_src, const void* v_src, int64_t src_ld, int src_type,
+                         int64_t d_in, const float* down, int64_t latent_dim,
+                         const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
+                         int64_t token0, int64_t t, void* stream) {
+  if (int rc = ifx::check_pool(pool)) return rc;
+  if (t < 0 || token0 < first_token || d_in < 1 || latent_dim < 1 || latent_dim > pool->width ||
+      src_ld < d_in || down == nullptr)
+    return ifx::fail(IFX_EDIM, "bad latent append sizes");
+  if (t == 0) return IFX_OK;
+  int e = ifx::kv_append_latent_launch(k_src, v_src, src_ld, src_type == IFX_BF16, d_in, down,
+                                       latent_dim, pool->dev_k, pool->dev_v, pool->host_k,
+                                       pool->host_v, pool->type == IFX_BF16, pool->width,
+                                       pool->page_len, slots, token0 - first_token, t,
+                                       static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "kv_append_latent launch");
+}
+
+int ifx_kv_gather_latent(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
+                         const int64_t* tokens, int64_t token0, int64_t n, int64_t latent_dim,
+                         const float* up, int64_t d_out, void* k_out, void* v_out, int64_t out_ld,
+                         int out_type, void* stream) {
+  if (int rc = ifx::check_pool(pool)) return rc;
+  if (n < 0 || latent_dim < 1 || latent_dim > pool->width || d_out < 1 || out_ld < d_out ||
+      up == nullptr)
+    return ifx::fail(IFX_EDIM, "bad latent gather sizes");
+  if (n == 0) return IFX_OK;
+  int e = ifx::kv_gather_latent_launch(pool->dev_k, pool->dev_v, pool->host_k, pool->host_v,
+                                       pool->type == IFX_BF16, pool->width, pool->page_len, slots,
+                                       tokens, tokens ? first_token : token0 - first_token, n,
+                                       latent_dim, up, d_out, k_out, v_out, out_ld,
+                                       out_type == IFX_BF16, static_cast<cudaStream_t>(stream));
+  return ifx::cuda_fail(e, "kv_gather_latent launch");
+}
+
 int ifx_kv_gather(const ifx_kv_pool* pool, const int32_t* slots, int64_t first_token,
                   const int64_t* tokens, int64_t token0, int64_t n, void* k_out, void* v_out,
                   void* stream) {

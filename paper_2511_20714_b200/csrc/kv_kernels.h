@@ -11,6 +11,14 @@ int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf1
 int kv_gather_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t width,
                      int64_t page_len, const int32_t* slots, const int64_t* tokens, int64_t rel0,
                      int64_t n, void* ko, void* vo, cudaStream_t st);
+int kv_append_latent_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf16,
+                            int64_t d_in, const float* down, int64_t L, void* dk, void* dv,
+                            void* hk, void* hv, int pool_bf16, int64_t width, int64_t page_len,
+                            const int32_t* slots, int64_t rel0, int64_t t, cudaStream_t st);
+int kv_gather_latent_launch(void* dk, void* dv, void* hk, void* hv, int pool_bf16, int64_t width,
+                            int64_t page_len, const int32_t* slots, const int64_t* tokens,
+                            int64_t rel0, int64_t n, int64_t L, const float* up, int64_t d_out,
+                            void* ko, void* vo, int64_t out_ld, int out_bf16, cudaStream_t st);
 int kv_move_launch(void* dk, void* dv, void* hk, void* hv, int esz, int64_t width,
                    int64_t page_len, const int64_t* moves, int64_t n, int dir, cudaStream_t st);
 int copy_blocks_launch(const void* src, void* dst, const int64_t* desc, int64_t n_blocks,

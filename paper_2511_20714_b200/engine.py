@@ -624,7 +624,7 @@ class BlockRunner:
         if ctx is not None:
             lo, hi = ctx.ranges[li]
             if hi > lo:
-                ck, cv = ctx.cache._gather(li, SELF_ATTN, None, lo, hi - lo, lo, hi, raw=True)
+                ck, cv = ctx.cache.gather_expanded(li, SELF_ATTN, lo, hi)
                 k, v = torch.cat([ck, kc]), torch.cat([cv, vc])
         T = q.shape[0]
         mask = torch.ones(T, k.shape[0], dtype=torch.bool, device=q.device)
@@ -842,7 +842,11 @@ class _KvContext:
         L = model.config.layers
         self.L, self.P = L, cfg.page_len
         self.pool = cache.pool(SELF_ATTN)
-        self.paged = cfg.page_len in PAGED_K1_PAGE_LENS
+        # latent mode: the stored rows are expanded (K7 gather + up-projection GEMM) once
+        # per block and layer into a contiguous context, reused by the block's passes
+        self.latent = cfg.latent is not None
+        self.expanded = {}
+        self.paged = cfg.page_len in PAGED_K1_PAGE_LENS and not self.latent
         self.stager = stager
         self.calls = 0
         self.passes = passes
@@ -973,6 +977,11 @@ class _KvContext:
         sl = (lambda t: t) if cols is None else (lambda t: t[:, cols[0]:cols[1]])  # noqa: E731
         if hi <= lo:
             return attn(q, heads, dhp, out, cur_k=cur_k, cur_v=cur_v, scale=scale)
+        if self.latent:
+            if li not in self.expanded:
+                self.expanded[li] = self.cache.gather_expanded(li, SELF_ATTN, lo, hi)
+            k, v = self.expanded[li]
+            return attn(q, heads, dhp, out, sl(k), sl(v), 0, hi - lo, cur_k, cur_v, scale=scale)
         if not self.paged:  # K7 gather of the context (host pages read over PCIe in place)
             k, v = self.cache._gather(li, SELF_ATTN, None, lo, hi - lo, lo, hi, raw=True)
             return attn(q, heads, dhp, out, sl(k), sl(v), 0, hi - lo, cur_k, cur_v, scale=scale)
@@ -1042,7 +1051,7 @@ class _LazyFold:
         f = self.folds[li]
         if f is None:
             a, b = self.rngs[li]
-            k, v = self.cache_ref()._gather(li, CROSS_ATTN, None, a, b - a, a, b, raw=True)
+            k, v = self.cache_ref().gather_expanded(li, CROSS_ATTN, a, b)
             f = self.folds[li] = _CrossFold(self.model, self.model.layers[li], k, v)
         return f
 
@@ -1052,12 +1061,23 @@ class _LazyFold:
         return self
 
 
+def _engine_row_width(model: "ToyModel", kv_config: KvConfig):
+    """Pool row width of the engine's cache: the padded attention width (zero head padding
+    rides along into the pages), or in latent mode (kvcache.py:26-31) the stored latent
+    rows, which the down-projection of unpadded rows produces."""
+    if kv_config.latent is None:
+        return model.attn_width
+    if model.attn_width != model.config.model_dim:
+        raise ConfigError("latent KV needs head_dim >= 64 (no zero-padded heads in the rows)")
+    return None
+
+
 def _gather_cross(cache: KvCache, rngs):
     """Per layer the prompt K/V rows, gathered (K7) into a contiguous buffer (a few rows;
     pages may sit on either tier)."""
     out = []
     for li, (a, b) in enumerate(rngs):
-        k, v = cache._gather(li, CROSS_ATTN, None, a, b - a, a, b, raw=True)
+        k, v = cache.gather_expanded(li, CROSS_ATTN, a, b)
         out.append((k, v, 0, b - a))
     return out
 
@@ -1244,7 +1264,7 @@ class Engine:
         # pools go now (the cache object itself is dropped here)
         retired = self.cache._pt if self.cache is not None else None
         self.cache = KvCache(self.kv_config, dtype=self.cache_dtype, reserve_tokens=reserve,
-                             row_width=self.model.attn_width)
+                             row_width=_engine_row_width(self.model, self.kv_config))
         with self._lock:
             self._schedule = list(request.prompt_schedule)
             self._generating_chunk = -1

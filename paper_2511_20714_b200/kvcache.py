@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._device import count_launch, dtype_code, require_cuda, row_ld, stream_ptr
+from ._device import count_launch, dtype_code, gemm, require_cuda, row_ld, stream_ptr
 from .errors import ConfigError, DimensionError, OutOfRangeError
 
 DUMP_MAGIC = b"INFKV1"  # kvcache.py:22
@@ -356,20 +356,10 @@ class _PendingAppend:
         c = self.cache
         if self.page is None and self.written > 0:  # rows the producer could not write
             k, v = c._as_rows(k), c._as_rows(v)
-            pad = c._row_width[self.kind] - k.shape[1]
-            if pad > 0:
-                k = torch.nn.functional.pad(k, (0, pad))
-                v = torch.nn.functional.pad(v, (0, pad))
-            if k.stride(1) != 1 or v.stride(1) != 1 or k.stride(0) != v.stride(0):
-                k, v = k.contiguous(), v.contiguous()
+            if c._latent_down is None:
+                k, v = c._pad_rows(self.kind, k, v)
             with c._lock:
-                codes, first = c._pt.slots(self.layer, self.kind, self.start, self.start + self.written)
-                slots = torch.from_numpy(codes).to(k.device, non_blocking=True)
-                p = c._pools[self.kind]
-                _abi.check(_abi.lib().ifx_kv_append(
-                    k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype), ctypes.byref(p.abi()),
-                    slots.data_ptr(), first, self.start, self.written, stream_ptr(stream)), "kv_append")
-                count_launch()
+                c._write_rows(self.layer, self.kind, self.start, self.written, k, v, stream)
         _abi.check(self.rc, "append_block")
         return BlockEntry(self.bid, self.layer, (self.start, self.start + self.t), self.pages,
                           self.kind, self.chunk)
@@ -416,11 +406,12 @@ class KvCache:
             per_layer = -(-reserve_tokens // config.page_len) + 1
             self._pools[SELF_ATTN].ensure(min(config.capacity_pages_device,
                                               per_layer * config.num_layers), 0)
-        self._latent_down = self._latent_up = None
+        self._latent_down = self._latent_up = self._latent_up_bf16 = None
         if config.latent is not None:
             dev = require_cuda()
-            self._latent_down = torch.as_tensor(np.asarray(config.latent.down_proj, np.float32)).to(dev)
-            self._latent_up = torch.as_tensor(np.asarray(config.latent.up_proj, np.float32)).to(dev)
+            # row-major fp32 on the device (K2L / K7L index them as [rows, cols])
+            self._latent_down = torch.as_tensor(np.ascontiguousarray(config.latent.down_proj, np.float32)).to(dev)
+            self._latent_up = torch.as_tensor(np.ascontiguousarray(config.latent.up_proj, np.float32)).to(dev)
 
     @property
     def page_table(self) -> PageTable:
@@ -533,15 +524,8 @@ class KvCache:
         if not 0 <= layer < cfg.num_layers:
             raise OutOfRangeError(f"layer {layer} out of range")
         PageTable.kind_code(kind)
-        if self._latent_down is not None:
-            k = (k.float() @ self._latent_down).contiguous()
-            v = (v.float() @ self._latent_down).contiguous()
-        pad = self._row_width[kind] - k.shape[1]
-        if pad > 0 and k.shape[1] == self._logical_width[kind]:  # unaligned width: zero-pad rows
-            k = torch.nn.functional.pad(k, (0, pad))
-            v = torch.nn.functional.pad(v, (0, pad))
-        if k.stride(1) != 1 or v.stride(1) != 1 or k.stride(0) != v.stride(0):
-            k, v = k.contiguous(), v.contiguous()
+        if self._latent_down is None:
+            k, v = self._pad_rows(kind, k, v)
         with self._lock:
             self._no_batch("append_block")
             if kind == CROSS_ATTN:
@@ -549,15 +533,39 @@ class KvCache:
             rc, bid, start, written, pages = self._pt.append(layer, kind, t, chunk_index)
             self._sync(stream)
             if written > 0:  # rows already packed even if allocation then failed (kvcache.py:210-223)
-                codes, first = self._pt.slots(layer, kind, start, start + written)
-                slots = torch.from_numpy(codes).to(k.device, non_blocking=True)
-                p = self._pools[kind]
-                _abi.check(_abi.lib().ifx_kv_append(
-                    k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype), ctypes.byref(p.abi()),
-                    slots.data_ptr(), first, start, written, stream_ptr(stream)), "kv_append")
-                count_launch()
+                self._write_rows(layer, kind, start, written, k, v, stream)
             _abi.check(rc, "append_block")
             return BlockEntry(bid, layer, (start, start + t), pages, kind, chunk_index)
+
+    def _pad_rows(self, kind: str, k, v):
+        """Rows as the pool stores them: zero-padded to the pool width (16-byte rows)."""
+        pad = self._row_width[kind] - k.shape[1]
+        if pad > 0 and k.shape[1] == self._logical_width[kind]:  # unaligned width: zero-pad rows
+            k = torch.nn.functional.pad(k, (0, pad))
+            v = torch.nn.functional.pad(v, (0, pad))
+        if k.stride(1) != 1 or v.stride(1) != 1 or k.stride(0) != v.stride(0):
+            k, v = k.contiguous(), v.contiguous()
+        return k, v
+
+    def _write_rows(self, layer: int, kind: str, start: int, n: int, k, v, stream=None) -> None:
+        """The page write of tokens [start, start + n): K2, or in latent mode K2L (the rows
+        down-projected inside the page-write kernel, kvcache.py:201-203)."""
+        codes, first = self._pt.slots(layer, kind, start, start + n)
+        slots = torch.from_numpy(codes).to(k.device, non_blocking=True)
+        p = self._pools[kind]
+        if self._latent_down is not None:
+            if k.stride(1) != 1 or v.stride(1) != 1 or k.stride(0) != v.stride(0):
+                k, v = k.contiguous(), v.contiguous()
+            lat = self.config.latent
+            _abi.check(_abi.lib().ifx_kv_append_latent(
+                k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype), k.shape[1],
+                self._latent_down.data_ptr(), lat.latent_dim, ctypes.byref(p.abi()),
+                slots.data_ptr(), first, start, n, stream_ptr(stream)), "kv_append_latent")
+        else:
+            _abi.check(_abi.lib().ifx_kv_append(
+                k.data_ptr(), v.data_ptr(), row_ld(k), dtype_code(k.dtype), ctypes.byref(p.abi()),
+                slots.data_ptr(), first, start, n, stream_ptr(stream)), "kv_append")
+        count_launch()
 
     def append_reserve(self, layer: int, t: int, kind: str = SELF_ATTN, chunk_index: int = 0,
                        stream=None) -> "_PendingAppend":
@@ -631,6 +639,21 @@ class KvCache:
         self._no_batch("a fetch")
         p = self._pools[kind]
         dev = require_cuda()
+        if self._latent_up is not None and not raw:  # K7L: gather + up-projection, fp32
+            lat = self.config.latent
+            d = self.config.head_dim
+            ko = torch.empty(n, d, device=dev, dtype=torch.float32)
+            vo = torch.empty_like(ko)
+            if n:
+                codes, first_tok = self._pt.slots(layer, kind, lo, hi)
+                slots = torch.from_numpy(codes).to(dev, non_blocking=True)
+                _abi.check(_abi.lib().ifx_kv_gather_latent(
+                    ctypes.byref(p.abi()), slots.data_ptr(), first_tok,
+                    None if tokens is None else tokens.data_ptr(), first, n, lat.latent_dim,
+                    self._latent_up.data_ptr(), d, ko.data_ptr(), vo.data_ptr(), d, _abi.F32,
+                    stream_ptr()), "kv_gather_latent")
+                count_launch()
+            return ko, vo
         ko = torch.empty(n, p.width, device=dev, dtype=p.dtype)
         vo = torch.empty_like(ko)
         if n:
@@ -644,9 +667,26 @@ class KvCache:
         lw = self._logical_width[kind]
         if p.width != lw:  # padded pool rows (alignment)
             ko, vo = ko[:, :lw].contiguous(), vo[:, :lw].contiguous()
-        if self._latent_up is not None and not raw:
-            ko, vo = ko.float() @ self._latent_up, vo.float() @ self._latent_up
         return ko, vo
+
+    def gather_expanded(self, layer: int, kind: str, lo: int, hi: int):
+        """Rows [lo, hi) as bf16 [n, head_dim] for attention (no access-clock tick: the
+        caller did the fetch bookkeeping). In latent mode the stored rows are gathered (K7)
+        and up-projected on the tensor cores (one bf16 GEMM each for K and V, fp32
+        accumulation); otherwise the rows themselves."""
+        ko, vo = self._gather(layer, kind, None, lo, hi - lo, lo, hi, raw=True)
+        if self._latent_up is None:
+            return ko, vo
+        if self._latent_up_bf16 is None:
+            self._latent_up_bf16 = self._latent_up.to(torch.bfloat16).contiguous()
+        d = self.config.head_dim
+        outs = []
+        for x in (ko, vo):
+            y = torch.empty(x.shape[0], d, device=x.device, dtype=torch.bfloat16)
+            if x.shape[0]:
+                gemm(x.to(torch.bfloat16).contiguous(), self._latent_up_bf16, y)
+            outs.append(y)
+        return outs[0], outs[1]
 
     def fetch_range(self, layer: int, token_range, kind: str = SELF_ATTN):
         """kvcache.py:328-339 -> (k, v) new CUDA tensors [end-start, head_dim]."""

@@ -29,7 +29,7 @@ import torch
 from . import _abi
 from .attention import (AttentionPartial, attention_partial, empty_partial, finalize_partial, merge_partials,
                         scaled_dot_attention)
-from .errors import DimensionError
+from .errors import ConfigError, DimensionError
 
 FLOAT_BYTES = 4  # parallel.py:38 — the reference's cost model counts fp32 elements
 
@@ -645,6 +645,8 @@ class UlyssesEngine:
         from .engine import default_kv_config
         self.model, self.comm = model, comm
         self.kv_config = kv_config or default_kv_config(model.config)
+        if self.kv_config.latent is not None:  # the up-projection mixes every head's columns
+            raise ConfigError("latent KV mode is not supported with head-sharded (Ulysses) caches")
         self.runner = UlyssesRunner(model, comm, attn)
         self.cache = None
 

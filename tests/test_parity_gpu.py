@@ -681,3 +681,85 @@ def test_engine_all_pages_on_host_tier():
         kv_config=OE.default_kv_config(OE.ModelConfig(**kw), capacity_pages_device=0,
                                        capacity_pages_host=4096))
     assert eng.cache.state() == ocache.state()
+
+
+# ---------------------------------------------------------------- latent KV mode (§8 f4)
+def _latent_cfg(head_dim, latent_dim, seed=0):
+    g = np.random.default_rng(seed)
+    down = g.standard_normal((head_dim, latent_dim)).astype(np.float32)
+    up = g.standard_normal((latent_dim, head_dim)).astype(np.float32)
+    return down, up
+
+
+@pytest.mark.parametrize("head_dim,latent_dim,cap", [(16, 4, 100), (16, 8, 2), (64, 30, 3), (1536, 512, 50)])
+def test_kv_latent_mode_vs_oracle(head_dim, latent_dim, cap):
+    """Latent KV (kvcache.py:26-31,201-203,323-325) through K2L / K7L (the down- and
+    up-projections inside the page-write and gather kernels, fp32): fetched rows equal the
+    oracle's (k . down) . up within fp32 summation-order noise, across both tiers, with
+    bit-exact bookkeeping; the reference's orthonormal round trip (test_kvcache.py:130-143)
+    holds to 1e-6."""
+    from oracle import kvcache as OK
+    from paper_2511_20714_b200 import kvcache as K
+
+    down, up = _latent_cfg(head_dim, latent_dim)
+    mk = lambda mod: mod.create_cache(mod.KvConfig(  # noqa: E731
+        num_layers=2, head_dim=head_dim, page_len=8, capacity_pages_device=cap,
+        capacity_pages_host=4096, latent=mod.LatentConfig(latent_dim, down, up)))
+    ours, ref = mk(K), mk(OK)
+    g = np.random.default_rng(head_dim)
+    for i in range(5):
+        t = int(g.integers(1, 40))
+        k, v = (g.standard_normal((t, head_dim)).astype(np.float32) for _ in range(2))
+        a, b = ours.append_block(i % 2, k, v), ref.append_block(i % 2, k, v)
+        assert (a.block_id, a.token_range, a.page_list) == (b.block_id, b.token_range, b.page_list)
+    for layer in (0, 1):
+        lo, hi = ref.addressable_range(layer)
+        fk, fv = ours.fetch_range(layer, (lo, hi))
+        rk, rv = ref.fetch_range(layer, (lo, hi))
+        assert fk.shape == (hi - lo, head_dim) and fk.dtype == torch.float32
+        scale = np.abs(rk).max()
+        assert np.abs(_np(fk) - rk).max() <= 1e-5 * scale * np.sqrt(head_dim)
+        assert np.abs(_np(fv) - rv).max() <= 1e-5 * scale * np.sqrt(head_dim)
+        idx = [hi - 1, lo, lo + 2, lo]
+        gk, _ = ours.fetch_indices(layer, idx)
+        wk, _ = ref.fetch_indices(layer, idx)
+        assert np.abs(_np(gk) - wk).max() <= 1e-5 * scale * np.sqrt(head_dim)
+    assert ours.state() == ref.state()
+    # orthonormal round trip
+    q, _ = np.linalg.qr(np.random.default_rng(2).standard_normal((8, 8)))
+    c = K.create_cache(K.KvConfig(num_layers=1, head_dim=8,
+                                  latent=K.LatentConfig(8, q.astype(np.float32), q.T.astype(np.float32))))
+    k = np.random.default_rng(3).standard_normal((5, 8)).astype(np.float32)
+    c.append_block(0, k, k)
+    fk, _ = c.fetch_range(0, (0, 5))
+    assert np.abs(_np(fk) - k).max() <= 1e-6
+
+
+@pytest.mark.parametrize("win", [None, 64])
+def test_engine_latent_kv_vs_oracle(win):
+    """The engine over a latent-mode cache (the reference engine accepts any KvConfig,
+    engine.py:335-346): appends down-projected in K2L, each block's context expanded once
+    per layer (K7 gather + up-projection GEMM) and attended by K1; latents vs the oracle
+    engine on the same latent cache within tolerance, page table bit-exact."""
+    from oracle import engine as OE
+    from oracle import kvcache as OK
+    from paper_2511_20714_b200 import engine as E
+    from paper_2511_20714_b200 import kvcache as K
+
+    kw = dict(layers=2, heads=2, head_dim=64, block_len=64, frame_shape=(4, 4), prompt_dim=8)
+    D = 128
+    down, up = _latent_cfg(D, 48, seed=5)
+    down, up = down / np.sqrt(D), up / np.sqrt(48)
+    req = dict(num_blocks=3, seed=6, prompt_schedule=[(0, "a b"), (2, "c")], kv_window=win)
+    mc = E.ModelConfig(**kw)
+    kvc = E.default_kv_config(mc, latent=K.LatentConfig(48, down, up))
+    eng = E.Engine(E.build_model(mc), kvc)
+    got = np.stack([b.latent for b in eng.generate(E.GenerationRequest(
+        schedule=E.DenoiseSchedule([1.0, 0.5]), **req))])
+    omc = OE.ModelConfig(**kw)
+    want, ocache = OE.generate_sequence(OE.ToyModel(omc), OE.GenerationRequest(
+        schedule=OE.DenoiseSchedule([1.0, 0.5]), **req),
+        kv_config=OE.default_kv_config(omc, latent=OK.LatentConfig(48, down, up)))
+    want = np.stack(want)
+    assert np.abs(got - want).max() <= ATOL_LATENT and _cos(got, want) > 0.999
+    assert eng.cache.state() == ocache.state()
