@@ -236,6 +236,14 @@ typedef struct ifx_attn_params {
    * (attention.py:157-180 semantics). NULL = never split. Not combined with row_max. */
   void* workspace;
   int64_t workspace_bytes;
+  /* optional O scatter over peer memory (the Ulysses head->sequence re-shard fused into
+   * the epilogue, replaces parallel.py:164-169's output all-to-all): when o_peer_rows > 0,
+   * output row r is sequence row g = o_row0 + r, stored at row g % o_peer_rows of
+   * o_peer[g / o_peer_rows] (a peer's buffer mapped into this process, ifx_ipc_open; row
+   * stride o_ld, head h at column h*head_dim from that pointer); `o` is then unused */
+  void* o_peer[8];
+  int64_t o_peer_rows;
+  int64_t o_row0;
 } ifx_attn_params;
 
 int ifx_attn_fwd(const ifx_attn_params* p, void* stream);
@@ -287,6 +295,22 @@ int ifx_ulysses_unpack(const void* src, int64_t n, int64_t groups, int64_t world
 int ifx_copy_blocks(const void* src, void* dst, const int64_t* desc, int64_t n_blocks,
                     int64_t max_rows, void* stream);
 
+/* Peer memory over NVLink / NVSwitch (the Ulysses exchange without NCCL on the data
+ * path). ifx_ipc_handle: the 64-byte CUDA IPC handle of a buffer from ifx_dev_alloc (the
+ * ranks exchange them through torch.distributed: plumbing only); ifx_ipc_open maps a
+ * peer's handle into this process (peer access enabled lazily), ifx_ipc_close unmaps. */
+int ifx_ipc_handle(const void* dev_ptr, void* handle_out);
+int ifx_ipc_open(const void* handle, void** dev_ptr_out);
+int ifx_ipc_close(void* dev_ptr);
+/* Barrier across the ranks of a peer mesh, enqueued on `stream` (graph-capturable): every
+ * store this GPU issued before it (earlier kernels on the stream, e.g. a scatter epilogue
+ * into peers' buffers) is visible to every peer after it, and vice versa. pads = host
+ * array of `world` device pointers, pads[p] = peer p's signal pad (uint32[8], zeroed
+ * before first use); counter = this rank's own device uint32 epoch (starts at 0). A peer
+ * that does not arrive within ~timeout_ms traps (a CUDA error instead of a hang). */
+int ifx_peer_barrier(void* const* pads, int world, int rank, uint32_t* counter, int timeout_ms,
+                     void* stream);
+
 /* Dense projection on cuBLASLt (a plain library GEMM; per-shape algorithm choice timed on
  * the first call outside a CUDA-graph capture): D[M,N] = relu?(A[M,K] . B[K,N] + beta * D),
  * row-major bf16 A (row stride lda) and B (ldb), fp32 accumulate, D fp32 or bf16 (ldd). */
@@ -324,6 +348,14 @@ typedef struct ifx_gemm_params {
   int64_t rope_row0, rope_q0, rope_k0, rope_pairs, rope_hs, rope_heads;
   const ifx_kv_pool* page_pool; const int32_t* page_slots;
   int64_t page_first_token, page_token0, page_k_col0, page_v_col0;
+  /* optional peer scatter of the bf16 output (the Ulysses sequence->head re-shard fused
+   * into the epilogue, replaces parallel.py:150-160's all-to-all): column block
+   * b = col / scatter_w (scatter_blocks of them) goes to up to two destinations, DEVICE
+   * int64 scatter[(b*2 + e)*4 + {0,1,2,3}] = {address, row stride in bytes, row_lo,
+   * row_hi}: row r in [row_lo, row_hi) is stored at address + r*stride + (col % scatter_w)*2
+   * (rows outside are skipped; row_hi = 0 marks an unused entry). Addresses are this
+   * process's mappings of peers' buffers (ifx_ipc_open). c may then be NULL. */
+  const int64_t* scatter; int64_t scatter_w; int64_t scatter_blocks;
 } ifx_gemm_params;
 int ifx_gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream);
 /* sum-of-squares parts per row G1 emits for an [M, N] = [M, K] . [K, N] output (the

@@ -46,6 +46,7 @@ EXPORTS = (
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_group_softmax", "ifx_group_softmax_rs", "ifx_ulysses_pack", "ifx_ulysses_unpack",
     "ifx_copy_blocks", "ifx_gemm_bf16", "ifx_gemm_fused", "ifx_gemm_tiles_n",
     "ifx_noise_normal_f32",
+    "ifx_ipc_handle", "ifx_ipc_open", "ifx_ipc_close", "ifx_peer_barrier",
 )
 
 
@@ -77,6 +78,7 @@ class AttnParams(ctypes.Structure):
         ("k_stage", ctypes.c_void_p), ("v_stage", ctypes.c_void_p), ("stage_rows", ctypes.c_int64),
         ("ctx_tile_runs", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_int64),
+        ("o_peer", ctypes.c_void_p * 8), ("o_peer_rows", ctypes.c_int64), ("o_row0", ctypes.c_int64),
     ]
 
 
@@ -100,6 +102,7 @@ class GemmParams(ctypes.Structure):
         ("page_pool", ctypes.c_void_p), ("page_slots", ctypes.c_void_p),
         ("page_first_token", ctypes.c_int64), ("page_token0", ctypes.c_int64),
         ("page_k_col0", ctypes.c_int64), ("page_v_col0", ctypes.c_int64),
+        ("scatter", ctypes.c_void_p), ("scatter_w", ctypes.c_int64), ("scatter_blocks", ctypes.c_int64),
     ]
 
 
@@ -169,6 +172,11 @@ def lib() -> ctypes.CDLL:
             L.ifx_rope_qk.argtypes = [P, I64, I64, I64, I64, I64, I64, I64, P, P, I64, P]
             L.ifx_ulysses_pack.argtypes = [P, I64, I64, I64, I64, I64, ctypes.c_int, P, P]
             L.ifx_ulysses_unpack.argtypes = [P, I64, I64, I64, I64, ctypes.c_int, P, I64, P]
+            L.ifx_ipc_handle.argtypes = [P, P]
+            L.ifx_ipc_open.argtypes = [P, ctypes.POINTER(P)]
+            L.ifx_ipc_close.argtypes = [P]
+            L.ifx_peer_barrier.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P,
+                                           ctypes.c_int, P]
             L.ifx_noise_normal_f32.argtypes = [ctypes.POINTER(ctypes.c_uint64), I64, P, ctypes.c_int]
             _lib = L
     return _lib

@@ -17,7 +17,7 @@ OUT = os.path.join(PKG, "libinferix_b200.so")
 OBJ = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["attn_fwd_sm100.cu", "gemm_sm100.cu", "attn_few_keys.cu", "kv_ops.cu", "kv_latent.cu", "gemm_lt.cpp", "abi.cpp", "pagetable.cpp", "noise_host.cpp"]
+SOURCES = ["attn_fwd_sm100.cu", "gemm_sm100.cu", "attn_few_keys.cu", "kv_ops.cu", "kv_latent.cu", "peer.cu", "gemm_lt.cpp", "abi.cpp", "pagetable.cpp", "noise_host.cpp"]
 
 
 def _npyrandom() -> str:

@@ -80,7 +80,8 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
              row_max: torch.Tensor | None = None, row_sum: torch.Tensor | None = None,
              split_kv: bool = True, stream=None, ctx_slots: torch.Tensor | None = None,
              page_len: int = 0, first_token: int = 0, stage_k: torch.Tensor | None = None,
-             stage_v: torch.Tensor | None = None, tile_runs: torch.Tensor | None = None) -> torch.Tensor:
+             stage_v: torch.Tensor | None = None, tile_runs: torch.Tensor | None = None,
+             o_peers=None, o_rows: int = 0, o_row0: int = 0) -> torch.Tensor:
     """Enqueue K1 (attn_fwd_sm100.cu): out = softmax(q [ctx∥cur]^T * scale) [ctx∥cur].
 
     q/out: [n_q, heads*head_dim] bf16 (row-strided views allowed). cur_*: [n_cur,
@@ -88,6 +89,10 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
     Paged (ctx_slots given): ctx_k/v are the KV pool, the context is tokens [ctx_row0,
     ctx_row0+n_ctx) whose pages from first_token on sit in slot codes ctx_slots (int32
     device tensor; codes < 0 address stage_k/v); tile_runs = tile_run_codes(codes, page_len).
+    o_peers: O scatter over peer memory (the Ulysses head->sequence re-shard in K1's
+    epilogue): output row r is sequence row g = o_row0 + r, written to row g % o_rows of
+    the buffer at address o_peers[g // o_rows] (row stride = out's); `out` only supplies
+    the row stride then.
     """
     p = _abi.AttnParams()
     p.q, p.q_ld, p.n_q = q.data_ptr(), row_ld(q), q.shape[0]
@@ -105,6 +110,10 @@ def attn_fwd(q: torch.Tensor, heads: int, head_dim: int, out: torch.Tensor,
         p.k_cur, p.v_cur = cur_k.data_ptr(), cur_v.data_ptr()
         p.cur_ld, p.n_cur = row_ld(cur_k), cur_k.shape[0]
     p.o, p.o_ld = out.data_ptr(), row_ld(out)
+    if o_peers is not None:
+        for i, a in enumerate(o_peers):
+            p.o_peer[i] = a
+        p.o_peer_rows, p.o_row0 = o_rows, o_row0
     p.heads, p.head_dim = heads, head_dim
     p.scale = (1.0 / math.sqrt(head_dim)) if scale is None else scale
     if mask is not None:
@@ -158,9 +167,9 @@ def gemm_tiles_n(m: int, n: int, k: int) -> int:
     return out.value
 
 
-def gemm_fused(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, beta: float = 0.0,
+def gemm_fused(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None, beta: float = 0.0,
                relu: bool = False, norm_in: RowNorm | None = None, norm_out: RowNorm | None = None,
-               rope=None, page=None, stream=None) -> int:
+               rope=None, page=None, scatter=None, stream=None) -> int:
     """G1 (gemm_sm100.cu): out = f(a @ b) on tcgen05, bf16 a [M, K] / b [K, N], fp32
     accumulate; out bf16, or fp32 with out = beta * out + f(.).
 
@@ -170,15 +179,23 @@ def gemm_fused(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, beta: float 
               per-tile sums of squares to norm_out.ss (norm_out.parts is set).
     rope:     (cos, sin, row0, pairs, head_stride, heads, q_col0, k_col0) 3D RoPE tables.
     page:     (pool abi, slots tensor, first_token, token0, k_col0, v_col0) page write.
+    scatter:  (table, block_width): bf16 output column blocks stored into peers' buffers
+              (device int64 table [blocks, 2, 4], ifx_gemm_params.scatter); out may be None.
     Returns the column tile count (norm_out.parts)."""
     M, K = a.shape
     N = b.shape[1]
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or b.shape[0] != K or \
-            tuple(out.shape) != (M, N):
+            (out is not None and tuple(out.shape) != (M, N)) or (out is None and scatter is None):
         raise DimensionError("gemm expects bf16 a [M, K], b [K, N] and out [M, N]")
     p = _abi.GemmParams()
     p.a, p.lda, p.b, p.ldb = a.data_ptr(), row_ld(a), b.data_ptr(), row_ld(b)
-    p.c, p.ldc, p.c_type = out.data_ptr(), row_ld(out), dtype_code(out.dtype)
+    if out is not None:
+        p.c, p.ldc, p.c_type = out.data_ptr(), row_ld(out), dtype_code(out.dtype)
+    else:
+        p.c, p.ldc, p.c_type = None, N, dtype_code(torch.bfloat16)
+    if scatter is not None:
+        table, width = scatter
+        p.scatter, p.scatter_w, p.scatter_blocks = table.data_ptr(), width, table.shape[0]
     p.m, p.n, p.k, p.beta, p.relu = M, N, K, float(beta), int(relu)
     if norm_in is not None:
         p.rs_part, p.rs_ld, p.rs_parts = norm_in.ss.data_ptr(), norm_in.ss.stride(0), norm_in.parts

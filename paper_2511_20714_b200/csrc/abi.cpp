@@ -102,7 +102,17 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
     return fail(IFX_EDIM, "attention extents must fit int32");
   // a handful of keys (cross-attention to the prompt): K1s, SIMT, no tensor-core tile
   static const bool few_keys_off = std::getenv("IFX_NO_FEW_KEYS") != nullptr;  // A/B probes
-  if (!few_keys_off && !paged && p->mask == nullptr && p->row_max == nullptr &&
+  const bool scatter = p->o_peer_rows > 0;
+  if (scatter) {
+    const int64_t n_peers = (p->o_row0 + p->n_q + p->o_peer_rows - 1) / p->o_peer_rows;
+    if (p->o_row0 < 0 || n_peers > 8 || p->o_row0 + p->n_q > INT32_MAX)
+      return fail(IFX_EDIM, "O scatter rows outside the 8 peers");
+    for (int64_t i = p->o_row0 / p->o_peer_rows; i < n_peers; ++i)
+      if (p->o_peer[i] == nullptr || (reinterpret_cast<uintptr_t>(p->o_peer[i]) & 15))
+        return fail(IFX_EDIM, "O scatter needs a 16-byte aligned buffer for every peer it reaches");
+    if ((p->o_ld * 2) % 16) return fail(IFX_EDIM, "O scatter row stride must be 16-byte aligned");
+  }
+  if (!few_keys_off && !scatter && !paged && p->mask == nullptr && p->row_max == nullptr &&
       p->n_ctx + p->n_cur <= attn_few_keys_max() && p->n_q * p->heads >= 1024 &&
       ((p->q_ld | p->ctx_ld | p->cur_ld | p->o_ld | width) % 8) == 0 &&
       ((reinterpret_cast<uintptr_t>(p->k_ctx) | reinterpret_cast<uintptr_t>(p->v_ctx) |
@@ -168,6 +178,11 @@ int attn_fwd(const ifx_attn_params* p, void* stream) {
   a.scale_log2 = p->scale * 1.4426950408889634f;
   a.o = static_cast<__nv_bfloat16*>(p->o);
   a.o_ld = p->o_ld;
+  if (scatter) {
+    for (int i = 0; i < 8; ++i) a.o_peer[i] = static_cast<__nv_bfloat16*>(p->o_peer[i]);
+    a.o_peer_rows = (int)p->o_peer_rows;
+    a.o_row0 = (int)p->o_row0;
+  }
   a.mask = p->mask;
   a.mask_ld = p->mask_ld;
   a.row_max = p->row_max;
@@ -226,8 +241,14 @@ int choose_splits(const ifx_attn_params* p) {
 // G1 (gemm_sm100.cu): validation + tensor maps; the epilogue options are documented at
 // ifx_gemm_params in include/ifx_abi.h.
 int gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
-  if (p->m < 0 || p->n < 1 || p->k < 1 || p->lda < p->k || p->ldb < p->n || p->ldc < p->n)
+  const bool scat = p->scatter != nullptr;
+  if (p->m < 0 || p->n < 1 || p->k < 1 || p->lda < p->k || p->ldb < p->n ||
+      (p->c != nullptr && p->ldc < p->n) || (p->c == nullptr && !scat))
     return fail(IFX_EDIM, "bad GEMM sizes");
+  if (scat && (p->c_type != IFX_BF16 || p->scatter_w < 8 || p->scatter_w % 8 ||
+               p->scatter_w * p->scatter_blocks < p->n || p->scatter_w > INT32_MAX ||
+               p->scatter_blocks > INT32_MAX))
+    return fail(IFX_EDIM, "peer scatter needs a bf16 output in 8-column-aligned blocks covering N");
   if (p->n % 8) return fail(IFX_EDIM, "GEMM N must be a multiple of 8");
   if (p->m > INT32_MAX || p->n > INT32_MAX || p->k > INT32_MAX)
     return fail(IFX_EDIM, "GEMM extents must fit int32");
@@ -261,6 +282,11 @@ int gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
   a.c = p->c;
   a.ldc = p->ldc;
   a.c_f32 = f32;
+  if (scat) {
+    a.scat = p->scatter;
+    a.scat_w = (int)p->scatter_w;
+    a.scat_blocks = (int)p->scatter_blocks;
+  }
   a.beta = p->beta;
   a.relu = p->relu;
   if (p->rs_part != nullptr) {

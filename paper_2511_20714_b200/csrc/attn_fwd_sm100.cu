@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const bool partial = a.n_splits > 1;
     __nv_bfloat16* orow =
         partial ? a.part_o + ((int64_t)split * a.n_q + grow) * a.part_ld + head * HD + half * (HD / 2)
-                : a.o + (int64_t)grow * a.o_ld + head * HD + half * (HD / 2);
+                : attn_out_row(a, grow < a.n_q ? grow : 0) + head * HD + half * (HD / 2);
     // read and merge all of this warp's O columns first, so the next item's first PV
     // (waiting on o_free) is not held up by the global stores
     uint32_t packed[HD / 64][16];
@@ -642,6 +642,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     named_sync(pair_bar, 64);  // the partner has read `red` before the next item rewrites it
     }
+    if (a.o_peer_rows > 0) __threadfence_system();  // peer stores out before the barrier
   }
 
   tc_fence_before();
@@ -680,7 +681,7 @@ __global__ void attn_combine_kernel(const AttnKernelArgs a) {
       for (int i = 0; i < PER; ++i) acc[i] += wgt * __bfloat162float(src[i]);
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
-    __nv_bfloat16* dst = a.o + (int64_t)row * a.o_ld + head * HD + lane * PER;
+    __nv_bfloat16* dst = attn_out_row(a, row) + head * HD + lane * PER;
 #pragma unroll
     for (int i = 0; i < PER; ++i) dst[i] = __float2bfloat16(acc[i] * inv);
     if (a.row_max != nullptr && lane == 0) {
@@ -688,6 +689,7 @@ __global__ void attn_combine_kernel(const AttnKernelArgs a) {
       a.row_sum[(int64_t)head * a.n_q + row] = den;
     }
   }
+  if (a.o_peer_rows > 0) __threadfence_system();
 }
 
 template <int HD>

@@ -43,7 +43,22 @@ struct AttnKernelArgs {
   int64_t part_ld;
   float* part_m;          // [n_splits, heads, n_q] max (log2 units)
   float* part_l;          // [n_splits, heads, n_q] denominator w.r.t. part_m
+  // O scatter over peer memory (o_peer_rows > 0; the Ulysses head->sequence re-shard fused
+  // into the epilogue): output row r is sequence row g = o_row0 + r, stored at row
+  // g % o_peer_rows of o_peer[g / o_peer_rows] (row stride o_ld)
+  __nv_bfloat16* o_peer[8];
+  int o_peer_rows, o_row0;
 };
+
+// Destination of output row `r` (before the head's column offset).
+__device__ __forceinline__ __nv_bfloat16* attn_out_row(const AttnKernelArgs& a, int r) {
+  if (a.o_peer_rows > 0) {
+    const int g = a.o_row0 + r;
+    const int p = g / a.o_peer_rows;
+    return a.o_peer[p] + (int64_t)(g - p * a.o_peer_rows) * a.o_ld;
+  }
+  return a.o + (int64_t)r * a.o_ld;
+}
 
 // K1s (attn_few_keys.cu): attention over <= attn_few_keys_max() keys, SIMT
 struct FewKeysArgs {

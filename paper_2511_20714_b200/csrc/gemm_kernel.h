@@ -52,6 +52,11 @@ struct GemmArgs {
   uint8_t* pv_host;
   int64_t prow_b, rel0, pk_col0, pv_col0, pwidth;
   int page_len, pad1_;
+  // ---- peer scatter (bf16 output; the Ulysses sequence->head re-shard fused): column block
+  // b = col / scat_w goes to <= 2 destinations scat[(b*2 + e)*4 + {addr, row stride bytes,
+  // row_lo, row_hi}]; rows outside [row_lo, row_hi) skipped. c may be null then.
+  const int64_t* scat;
+  int scat_w, scat_blocks;
 };
 
 // Persistent launch (<= one CTA per SM), BN in {64, 128, 192, 256}; mode 1: one CTA per

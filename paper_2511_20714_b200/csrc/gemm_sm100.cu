@@ -445,7 +445,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
                          : "r"(stg_u + rl * 64 + ((bj ^ ((rl >> 1) & 3)) << 4)));
             const int64_t rr = r0 + rl;
             if (rr < a.M && col < a.N) {
-              *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.c) + rr * a.ldc + col) = o;
+              if (a.c != nullptr)
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.c) + rr * a.ldc + col) = o;
+              if (a.scat != nullptr) {  // straight into the consumer rank's buffer (NVLink)
+                const int blk = col / a.scat_w;
+                const int64_t* d = a.scat + (int64_t)blk * 8;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  if (rr >= __ldg(d + 4 * e + 2) && rr < __ldg(d + 4 * e + 3))
+                    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(__ldg(d + 4 * e)) +
+                                              rr * __ldg(d + 4 * e + 1) +
+                                              (int64_t)(col - blk * a.scat_w) * 2) = o;
+                }
+              }
               if (pstream >= 0) {
                 const int64_t rel = a.rel0 + rr;
                 const int pg = (int)(rel / a.page_len);
@@ -475,6 +487,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
         }
       }
     }
+    if (a.scat != nullptr) __threadfence_system();  // peer stores out before the barrier
   }
 
   tc_fence_before();

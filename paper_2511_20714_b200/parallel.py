@@ -485,11 +485,200 @@ def _copy_blocks(src: torch.Tensor, dst: torch.Tensor, desc) -> None:
         count_launch()
 
 
+class PeerMesh:
+    """Symmetric device arenas over NVLink / NVSwitch peer memory, one per rank.
+
+    Each rank allocates one arena (cudaMalloc via ifx_dev_alloc, outside torch's caching
+    allocator), exports its CUDA IPC handle, and maps every peer's arena (handles exchanged
+    with all_gather_object over the group: host plumbing, no data). Kernels then store
+    straight into a peer's arena (`addr(peer, offset)`) and `barrier()` (ifx_peer_barrier,
+    graph-capturable) orders the phases. Arena = [signal pad 32 B | epoch counter | data]."""
+
+    HEAD = 256  # pad (uint32[8]) at 0, this rank's epoch counter at 64, data from 256
+
+    def __init__(self, comm, nbytes: int, timeout_ms: int | None = None):
+        import ctypes
+        import os
+
+        from .engine import _DevBuf
+        self.comm = comm
+        W, r = comm.world, comm.rank
+        if W > 8:
+            raise ConfigError("peer meshes span at most the 8 GPUs of one box")
+        self.nbytes = int(nbytes)
+        self.buf = _DevBuf(self.HEAD + self.nbytes)
+        raw = torch.as_tensor(self.buf, device=torch.device("cuda", torch.cuda.current_device()))
+        raw[:self.HEAD].zero_()
+        torch.cuda.synchronize()
+        L = _abi.lib()
+        self._opened = []
+        bases = []
+        if W == 1:
+            bases = [self.buf.ptr]
+        else:
+            h = (ctypes.c_char * 64)()
+            _abi.check(L.ifx_ipc_handle(ctypes.c_void_p(self.buf.ptr), h), "ipc_handle")
+            hs = [None] * W
+            comm.dist.all_gather_object(hs, bytes(h), group=comm.group)
+            for i in range(W):
+                if i == r:
+                    bases.append(self.buf.ptr)
+                    continue
+                pp = ctypes.c_void_p()
+                _abi.check(L.ifx_ipc_open(ctypes.c_char_p(hs[i]), ctypes.byref(pp)), "ipc_open")
+                self._opened.append(pp.value)
+                bases.append(pp.value)
+        comm.dist.barrier(group=comm.group)  # every pad zeroed before any barrier kernel
+        self.bases = bases
+        self._pads = (ctypes.c_void_p * W)(*bases)
+        self._counter = ctypes.c_void_p(self.buf.ptr + 64)
+        self.timeout_ms = int(timeout_ms or os.environ.get("IFX_PEER_TIMEOUT_MS", 60000))
+        self.barriers = 0
+
+    def addr(self, peer: int, offset: int = 0) -> int:
+        """Address (in this process) of byte `offset` of `peer`'s data region."""
+        return self.bases[peer] + self.HEAD + int(offset)
+
+    def local(self, offset: int, rows: int, width: int, dtype=torch.bfloat16) -> torch.Tensor:
+        """[rows, width] view of this rank's own data region at byte `offset`."""
+        t = torch.as_tensor(self.buf, device=torch.device("cuda", torch.cuda.current_device()))
+        es = torch.empty((), dtype=dtype).element_size()
+        n = rows * width * es
+        return t[self.HEAD + offset:self.HEAD + offset + n].view(dtype).view(rows, width)
+
+    def barrier(self) -> None:
+        from ._device import count_launch, stream_ptr
+        _abi.check(_abi.lib().ifx_peer_barrier(self._pads, self.comm.world, self.comm.rank,
+                                               self._counter, self.timeout_ms, stream_ptr()),
+                   "peer_barrier")
+        count_launch()
+        self.barriers += 1
+
+    def close(self) -> None:
+        import ctypes
+        for pp in self._opened:
+            _abi.lib().ifx_ipc_close(ctypes.c_void_p(pp))
+        self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
+
+class P2PExchange:
+    """The Ulysses re-shard (parallel.py:150-169) without an all-to-all: G1's QKV epilogue
+    stores each head's Q/K/V column block of this rank's n sequence rows straight into the
+    rank that attends that head (region R of its arena), K1's epilogue stores each output
+    row into the rank that owns that sequence row (region S, [n, Dp]). Two peer barriers
+    per layer-pass (after the QKV GEMM; after attention) order the phases; they also cover
+    the write-after-read hazards (a rank's next QKV GEMM starts only after every rank's
+    attention read R, its next attention only after every rank's wo GEMM read S).
+
+    Works for the whole-head plan (heads % W == 0) and the balanced plan when a head's rows
+    and K/V reach at most two ranks (two scatter entries per block; always when heads >= W,
+    `layout` raises ConfigError otherwise)."""
+
+    def __init__(self, runner, comm):
+        m = runner.model
+        W, r, n, T = comm.world, comm.rank, runner.n, m.config.block_len
+        H, dhp, Dp = m.heads_pad, m.dh_pad, m.attn_width
+        balanced = runner.plan is not None
+        r_bytes = self.region_bytes(H, T, W, dhp, balanced)
+        self.s_off = max(r_bytes) // 256 * 256 + 256
+        self.mesh = PeerMesh(comm, self.s_off + n * Dp * 2)
+        table, self.o_peers = self.layout(H, T, W, r, dhp, balanced, self.mesh.addr, self.s_off)
+        self.table = torch.from_numpy(table.reshape(3 * H, 8)).to(runner.x.device)
+        if balanced:
+            self.r_view = self.mesh.local(0, r_bytes[r] // 2, 1).view(-1)
+        else:
+            self.r_view = self.mesh.local(0, T, 3 * (H // W) * dhp)
+        self.s_view = self.mesh.local(self.s_off, n, Dp)
+        self.n = n
+
+    @classmethod
+    def region_bytes(cls, H, T, W, dhp, balanced):
+        """Bytes of each rank's receive region R (whole-head: [T, 3*wl]; balanced: the Q
+        segments stacked, then K and V [T, hl*dhp])."""
+        if not balanced:
+            return [T * 3 * (H // W) * dhp * 2] * W
+        segs, heads = cls._segments(H, T, W)
+        return [sum(r1 - r0 for _, r0, r1 in segs[k]) * dhp * 2 + 2 * T * len(heads[k]) * dhp * 2
+                for k in range(W)]
+
+    @classmethod
+    def layout(cls, H, T, W, r, dhp, balanced, addr, s_off):
+        """Rank r's G1 scatter table [3H blocks, 2 entries, (address, row stride, row_lo,
+        row_hi)] over the Q|K|V column blocks of its n rows, and K1's per-peer O addresses.
+        addr(peer, byte offset) -> address of that byte of the peer's data region."""
+        n, rb = T // W, dhp * 2
+        table = np.zeros((3 * H, 2, 4), dtype=np.int64)
+        fill = np.zeros(3 * H, dtype=np.int64)
+
+        def put(blk, a, ld, lo, hi):
+            e = fill[blk]
+            if e >= 2:
+                raise ConfigError("a head reaches more than two ranks")
+            table[blk, e] = (a, ld, lo, hi)
+            fill[blk] += 1
+        if not balanced:
+            hl = H // W
+            wl = hl * dhp
+            for g in range(3):
+                for h in range(H):
+                    p, j = divmod(h, hl)
+                    put(g * H + h, addr(p, (r * n) * 3 * wl * 2 + (g * wl + j * dhp) * 2),
+                        3 * wl * 2, 0, n)
+            # K1 over this rank's hl heads, all T rows: row g -> row owner g // n, at the
+            # columns of this rank's heads
+            return table, [addr(p, s_off + r * hl * dhp * 2) for p in range(W)]
+        segs, heads = cls._segments(H, T, W)
+        for k in range(W):
+            kv_w = len(heads[k]) * rb
+            qr_k = sum(r1 - r0 for (_, r0, r1) in segs[k])
+            k_off, v_off = qr_k * rb, qr_k * rb + T * kv_w
+            base = 0
+            for (h, r0, r1) in segs[k]:
+                a, b = max(r0, r * n), min(r1, (r + 1) * n)
+                if b > a:  # local row rr -> Q row base + (r*n + rr - r0) of rank k
+                    put(h, addr(k, (base + r * n - r0) * rb), rb, a - r * n, b - r * n)
+                base += r1 - r0
+            for hi_, h in enumerate(heads[k]):
+                put(H + h, addr(k, k_off + (r * n) * kv_w + hi_ * rb), kv_w, 0, n)
+                put(2 * H + h, addr(k, v_off + (r * n) * kv_w + hi_ * rb), kv_w, 0, n)
+        # K1 per segment (one head): O row i is sequence row r0 + i -> its owner, at the
+        # head's columns (attn(col_off=h*dhp*2, row0=r0))
+        return table, [addr(p, s_off) for p in range(W)]
+
+    @staticmethod
+    def _segments(H, T, W):
+        per = H * T // W
+        segs = []
+        for k in range(W):
+            g, g1, sk = k * per, (k + 1) * per, []
+            while g < g1:
+                h, rr = divmod(g, T)
+                e = min(g1, (h + 1) * T)
+                sk.append((h, rr, rr + e - g))
+                g = e
+            segs.append(sk)
+        return segs, [sorted({h for h, _, _ in sk}) for sk in segs]
+
+    def attn(self, col_off: int = 0, row0: int = 0):
+        """K1 with its O scattered to the row owners' S regions (+ col_off bytes)."""
+        import functools
+
+        from ._device import attn_fwd
+        return functools.partial(attn_fwd, o_peers=[a + col_off for a in self.o_peers],
+                                 o_rows=self.n, o_row0=row0)
+
+
 class UlyssesRunner:
     """BlockRunner (engine.py) for one Ulysses rank: sequence-sharded activations,
     head-sharded attention over the rank-local KV shard (engine.py:185-221 semantics)."""
 
-    def __init__(self, model, comm: UlyssesComm, attn=None):
+    def __init__(self, model, comm: UlyssesComm, attn=None, p2p: bool = False):
         from ._device import attn_fwd
         self.model, self.comm = model, comm
         c = model.config
@@ -531,6 +720,13 @@ class UlyssesRunner:
         self._tv = self._gpool = self._cap = self._graph = None  # CUDA-graph state (_euler_steps)
         self._warm = False
         self._tail = None  # event after the last block's clean pass (_euler_steps: GPU idle?)
+        # the re-shard over peer memory (G1 scatter epilogue + K1 O scatter) instead of
+        # pack -> all-to-all -> unpack
+        self.xch = None
+        if p2p:
+            if attn is not None:
+                raise ConfigError("the peer-scatter exchange runs K1 itself (no attention hook)")
+            self.xch = P2PExchange(self, comm)
 
     def _balanced_attention(self, li, ctx, sc, ev):
         """BalancedPlan: re-shard (one all-to-all), one K1 per segment (a head's query rows,
@@ -564,6 +760,47 @@ class UlyssesRunner:
         _copy_blocks(self.b_orecv, self.attn_s, pl.ounpack)
         return kc, vc
 
+    def _p2p_attention(self, li, ctx, sc, ev, lw, rope, append=None):
+        """QKV projection scattered into the attending ranks (G1 epilogue, RoPE fused), a
+        peer barrier, K1 with O scattered to the row owners, the clean pass's page write of
+        this rank's K / V (`append(kc, vc)`: before the barrier, because once every rank
+        passed it the peers' next QKV epilogue overwrites region R), a peer barrier."""
+        from ._device import gemm_fused
+        from .engine import timing_event
+        m, x = self.model, self.xch
+        c, dhp, wl = m.config, m.dh_pad, self.wl
+        rspec = None if rope is None else (rope[0], rope[1], self.comm.rank * self.n,
+                                           c.head_dim // 2, dhp, m.heads_pad, 0, m.attn_width)
+        gemm_fused(self.h, lw.wqkv, None, rope=rspec, scatter=(x.table, dhp))
+        x.mesh.barrier()
+        if ev is not None:
+            e0 = timing_event()
+            e0.record()
+        if self.plan is None:
+            R = x.r_view
+            q, kc, vc = R[:, :wl], R[:, wl:2 * wl], R[:, 2 * wl:]
+            ctx.attend(li, q, self.hl, dhp, x.s_view, kc, vc, sc, attn=x.attn())
+        else:
+            pl, T = self.plan, self.plan.T
+            kv = x.r_view[pl.k_off // 2:][:2 * T * wl].view(2, T, wl)
+            kc, vc = kv[0], kv[1]
+            qreg = x.r_view[:pl.qr * dhp].view(pl.qr, dhp)
+            last = len(pl.segs) - 1
+            for si, (h, r0, r1) in enumerate(pl.segs):
+                hi_ = pl.heads_of.index(h)
+                b, mm = pl.seg_base[si], r1 - r0
+                c0, c1 = hi_ * dhp, (hi_ + 1) * dhp
+                ctx.attend(li, qreg[b:b + mm], 1, dhp, x.s_view, kc[:, c0:c1], vc[:, c0:c1], sc,
+                           attn=x.attn(col_off=h * dhp * 2, row0=r0), cols=(c0, c1),
+                           first=si == 0, last=si == last)
+        if ev is not None:
+            e1 = timing_event()
+            e1.record()
+            ev.append((e0, e1))
+        if append is not None:
+            append(kc, vc)
+        x.mesh.barrier()
+
     def _rms(self, x, out, tvec=None, t=0.0, x_out=None):
         from ._device import rms_bf16
         return rms_bf16(x, out, tvec, t, x_out)
@@ -571,11 +808,10 @@ class UlyssesRunner:
     def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None,
                 rope=None):
         from ._device import gemm
-        from .engine import _cross_attend, _ffn_up, _residual, timing_event
+        from .engine import _cross_attend, _ffn_up, _residual
         from .kvcache import SELF_ATTN
         m = self.model
         c = m.config
-        dhp, wl = m.dh_pad, self.wl
         sc = 1.0 / math.sqrt(c.head_dim)
         for li, lw in enumerate(m.layers):
             if li == 0:
@@ -585,45 +821,62 @@ class UlyssesRunner:
                     self._rms(latent, self.h, m.time_vec, t, self.x)
             else:
                 self._rms(self.x, self.h)
-            gemm(self.h, lw.wqkv, self.qkv)
-            if rope is not None:  # this rank's rows of the block: table rows rank*n ..
-                from ._device import rope_qk
-                rope_qk(self.qkv, m.heads_pad, dhp, c.head_dim // 2, 0, m.attn_width, rope[0],
-                        rope[1], tab_row0=self.comm.rank * self.n)
             ev = self.attn_events
-            if self.plan is None:
-                qkv_h = self.comm.seq_to_head(self.qkv, 3)          # [T, 3*wl] local heads
-                q, kc, vc = qkv_h[:, :wl], qkv_h[:, wl:2 * wl], qkv_h[:, 2 * wl:]
-                if ev is not None:
-                    e0 = timing_event()
-                    e0.record()
-                ctx.attend(li, q, self.hl, dhp, self.attn_h, kc, vc, sc, attn=self._attn)
-                if ev is not None:
-                    e1 = timing_event()
-                    e1.record()
-                    ev.append((e0, e1))
-                self.comm.head_to_seq(self.attn_h, self.attn_s)      # [n, Dp]
+            if self.xch is not None:
+                app = None
+                if collect_kv:  # rank-local page write of this rank's heads
+                    def app(kc, vc, li=li):
+                        cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
+                self._p2p_attention(li, ctx, sc, ev, lw, rope, app)
+                attn_s = self.xch.s_view
             else:
-                kc, vc = self._balanced_attention(li, ctx, sc, ev)
-            _residual(self.x, self.attn_s, lw.wo)
+                kc, vc = self._a2a_attention(li, ctx, sc, ev, lw, rope)
+                attn_s = self.attn_s
+            _residual(self.x, attn_s, lw.wo)
             if cross is not None:  # sequence-sharded vs replicated prompt K/V: no comm
                 self._rms(self.x, self.h)
                 _cross_attend(self, cross[li], self.x, self.h, sc)
             self._rms(self.x, self.h)
             _ffn_up(self.h, lw.w1, self.ffn)
             _residual(self.x, self.ffn, lw.w2)
-            if collect_kv:  # rank-local page write of this rank's heads
+            if collect_kv and self.xch is None:  # rank-local page write of this rank's heads
                 cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
         if eps_out is not None:
             self._rms(self.x, self.h)
             gemm(self.h, m.w_out, eps_out)
+
+    def _a2a_attention(self, li, ctx, sc, ev, lw, rope):
+        """QKV projection, pack -> all-to-all -> K1 -> all-to-all -> unpack (NCCL)."""
+        from ._device import gemm
+        from .engine import timing_event
+        m, c, dhp, wl = self.model, self.model.config, self.model.dh_pad, self.wl
+        gemm(self.h, lw.wqkv, self.qkv)
+        if rope is not None:  # this rank's rows of the block: table rows rank*n ..
+            from ._device import rope_qk
+            rope_qk(self.qkv, m.heads_pad, dhp, c.head_dim // 2, 0, m.attn_width, rope[0],
+                    rope[1], tab_row0=self.comm.rank * self.n)
+        if self.plan is None:
+            qkv_h = self.comm.seq_to_head(self.qkv, 3)          # [T, 3*wl] local heads
+            q, kc, vc = qkv_h[:, :wl], qkv_h[:, wl:2 * wl], qkv_h[:, 2 * wl:]
+            if ev is not None:
+                e0 = timing_event()
+                e0.record()
+            ctx.attend(li, q, self.hl, dhp, self.attn_h, kc, vc, sc, attn=self._attn)
+            if ev is not None:
+                e1 = timing_event()
+                e1.record()
+                ev.append((e0, e1))
+            self.comm.head_to_seq(self.attn_h, self.attn_s)      # [n, Dp]
+        else:
+            kc, vc = self._balanced_attention(li, ctx, sc, ev)
+        return kc, vc
 
     def denoise(self, latent, schedule, ctx, cross, cache, chunk_index):
         from .engine import _euler_steps, rope_tables
         rope = rope_tables(self.model.config, chunk_index, latent.device)
         # graph capture needs the all-to-alls on the GPU stream: NCCL only (a gloo group
         # stages them through the host)
-        nccl = self.comm.dist.get_backend(self.comm.group) == "nccl"
+        nccl = self.comm.dist.get_backend(self.comm.group) == "nccl" or self.xch is not None
         _euler_steps(self, latent, schedule, ctx, cross, cache, self.eps, rope, graphs_ok=nccl,
                      first_block=chunk_index == 0)
         self.forward(latent, 0.0, ctx, cross, cache, collect_kv=cache is not None,
@@ -641,13 +894,22 @@ class UlyssesEngine:
     """Engine.generate (engine.py:368-411) across the ranks of `comm`. Every rank runs the
     same page-table calls in the same order, so bookkeeping stays identical everywhere."""
 
-    def __init__(self, model, comm: UlyssesComm, kv_config=None, attn=None):
+    def __init__(self, model, comm: UlyssesComm, kv_config=None, attn=None, p2p: bool | None = None):
+        """p2p: re-shard through peer memory (P2PExchange) instead of NCCL all-to-alls.
+        Default (None): IFX_ULYSSES=p2p|nccl, else p2p when no attention hook is given and
+        the plan allows it (heads >= ranks)."""
+        import os
+
         from .engine import default_kv_config
         self.model, self.comm = model, comm
         self.kv_config = kv_config or default_kv_config(model.config)
         if self.kv_config.latent is not None:  # the up-projection mixes every head's columns
             raise ConfigError("latent KV mode is not supported with head-sharded (Ulysses) caches")
-        self.runner = UlyssesRunner(model, comm, attn)
+        if p2p is None:
+            mode = os.environ.get("IFX_ULYSSES", "auto")
+            p2p = mode == "p2p" or (mode == "auto" and attn is None and
+                                     model.heads_pad >= comm.world)
+        self.runner = UlyssesRunner(model, comm, attn, p2p=p2p)
         self.cache = None
 
     def generate(self, request, noise_provider=None, gather: bool = True):

@@ -64,7 +64,7 @@ CFG = dict(layers=2, heads=4, head_dim=64, block_len=256, frame_shape=(8, 8), pr
 REQ = dict(num_blocks=3, seed=0, prompt_schedule=[(0, "a quiet scene"), (2, "rain")])
 
 
-def _rank(rank, world, port, q, cfg=None, kvc=None, pad=True):
+def _rank(rank, world, port, q, cfg=None, kvc=None, pad=True, p2p=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -74,9 +74,12 @@ def _rank(rank, world, port, q, cfg=None, kvc=None, pad=True):
         from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
 
         model = E.ToyModel(E.ModelConfig(**(cfg or CFG)), head_multiple=world if pad else 1)
-        eng = UlyssesEngine(model, UlyssesComm(), E.KvConfig(**kvc) if kvc else None)
+        eng = UlyssesEngine(model, UlyssesComm(), E.KvConfig(**kvc) if kvc else None, p2p=p2p)
         lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
-        q.put((rank, [l.cpu().numpy() for l in lats], eng.cache.state(), eng.comm.bytes))
+        moved = eng.runner.xch.mesh.barriers if p2p else eng.comm.bytes
+        eng.runner.release_graphs()
+        torch.cuda.synchronize()
+        q.put((rank, [l.cpu().numpy() for l in lats], eng.cache.state(), moved))
     finally:
         dist.destroy_process_group()
 
@@ -90,12 +93,16 @@ KV_SPILL = dict(num_layers=2, head_dim=256, page_len=16, capacity_pages_device=4
                 capacity_pages_host=10**4)
 
 
+@pytest.mark.parametrize("p2p", [False, True], ids=["a2a", "p2p"])
 @pytest.mark.parametrize("world,cfg,kvc,pad", [(2, CFG, None, True), (2, CFG_ROPE, None, True),
                                               (2, CFG, KV_SPILL, True),
                                               (2, CFG_ROPE, None, False),  # balanced: 1.5 heads/rank
                                               (2, dict(CFG, heads=3), dict(KV_SPILL, head_dim=192), False),
                                               (3, dict(CFG, block_len=192), None, False)])  # 4 heads / 3 ranks
-def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad):
+def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad, p2p):
+    """2-3 ranks sharing cuda:0 (gloo group). a2a: pack -> all-to-all (host-staged) ->
+    unpack. p2p: no all-to-all — G1's QKV epilogue and K1's epilogue store into the other
+    processes' arenas (CUDA IPC mappings), ordered by ifx_peer_barrier."""
     from paper_2511_20714_b200 import engine as E
 
     ref_model = E.build_model(E.ModelConfig(**cfg))
@@ -104,7 +111,8 @@ def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, q, cfg, kvc, pad)) for r in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, cfg, kvc, pad, p2p))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
@@ -116,7 +124,7 @@ def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad):
             assert np.abs(a - b.latent).max() <= 2e-2, rank
         # replicated page table == single-GPU page table == reference semantics
         assert state == ref_eng.cache.state()
-        assert nbytes > 0
+        assert nbytes > 0  # bytes through the all-to-alls, or peer barriers
     if kvc:
         assert ref_eng.cache.memory_stats().host_pages_used > 0
 
@@ -124,7 +132,7 @@ def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad):
 GRAPH_STEPS = [1.0, 0.75, 0.5]
 
 
-def _rank_nccl(port, q):
+def _rank_nccl(port, q, p2p=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -133,7 +141,7 @@ def _rank_nccl(port, q):
         from paper_2511_20714_b200 import engine as E
         from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
 
-        eng = UlyssesEngine(E.ToyModel(E.ModelConfig(**CFG)), UlyssesComm())
+        eng = UlyssesEngine(E.ToyModel(E.ModelConfig(**CFG)), UlyssesComm(), p2p=p2p)
         # 3 steps: a block's first pass may run eagerly (idle GPU), the rest are captured
         lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule(GRAPH_STEPS), **REQ))
         q.put(([l.cpu().numpy() for l in lats], eng.cache.state(), eng.runner._graph is not None))
@@ -143,17 +151,19 @@ def _rank_nccl(port, q):
         dist.destroy_process_group()
 
 
-def test_ulysses_nccl_graph_capture_world1():
+@pytest.mark.parametrize("p2p", [False, True], ids=["a2a", "p2p"])
+def test_ulysses_nccl_graph_capture_world1(p2p):
     """The NCCL path of the Ulysses runner on one GPU: its denoise passes are captured as
     CUDA graphs with the all-to-alls inside (world size 1 exercises ProcessGroupNCCL under
-    stream capture), and match the single-GPU engine."""
+    stream capture) — or, p2p, with the scatter epilogues and peer barriers inside — and
+    match the single-GPU engine."""
     from paper_2511_20714_b200 import engine as E
 
     ref_eng = E.Engine(E.build_model(E.ModelConfig(**CFG)))
     ref = ref_eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule(GRAPH_STEPS), **REQ))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    p = ctx.Process(target=_rank_nccl, args=(_free_port(), q))
+    p = ctx.Process(target=_rank_nccl, args=(_free_port(), q, p2p))
     p.start()
     lats, state, graphed = q.get(timeout=300)
     p.join(timeout=120)
