@@ -254,14 +254,19 @@ def run_ours(args):
     backend = os.environ.get("IFX_DIST_BACKEND", "nccl")
     local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.ulysses:
+        if world == 1:  # --ulysses at N = 1: the multi-GPU code path on one rank
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
     cfgname = args.config or "c2"
     c = CONFIGS[cfgname]
-    if world > 1:
+    if world > 1 or args.ulysses:
         return run_ulysses_bench(args, c, cfgname, world, rank, local)
     if "prefill" in c:
         return run_host_tier_bench(args, c, cfgname, local)
@@ -503,7 +508,16 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
     req = E.GenerationRequest(nb, E.DenoiseSchedule(STEPS), seed=0)
     # the reference's seeded noise (engine.py:280-282), resident in HBM for `value`
     noise = [torch.from_numpy(E._init_noise(mc, 0, ch)).cuda() for ch in range(nb)]
-    eng = UlyssesEngine(model, comm, kvc)
+    exchange = "peer scatter over NVLink (G1 QKV epilogue + K1 O epilogue, peer barriers)"
+    try:
+        eng = UlyssesEngine(model, comm, kvc, p2p=args.exchange == "p2p")
+    except Exception as e:  # e.g. CUDA IPC unavailable in this container: say so, use NCCL
+        if args.exchange != "p2p":
+            raise
+        exchange = f"NCCL all-to-all (peer mesh setup failed: {type(e).__name__}: {e})"
+        eng = UlyssesEngine(model, comm, kvc, p2p=False)
+    if eng.runner.xch is None and args.exchange == "nccl":
+        exchange = "NCCL all-to-all (K5 pack / unpack)"
     roll = lambda: eng.generate(req, noise_provider=lambda ch: noise[ch], gather=False)  # noqa: E731
     for _ in range(args.warmup):
         roll()
@@ -560,7 +574,8 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
                 "config": {"workload": c["desc"], "parallelism": f"ulysses{world}",
                            "head_split": "whole heads" if eng.runner.plan is None else
                            f"balanced: {eng.runner.plan.hl} heads / {len(eng.runner.plan.segs)} "
-                           f"segments on rank 0", "l2": "inputs larger than L2"},
+                           f"segments on rank 0", "exchange": exchange,
+                           "l2": "inputs larger than L2"},
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak if achieved else None, "traffic": traffic,
                              "traffic_launch": traffic_note, "peak_source": peak_src,
@@ -568,7 +583,8 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
                 "e2e": {"value": nb * FRAMES_PER_BLOCK / float(e2e.item()), "unit": UNIT,
                         "h2d_bytes_per_step": nb * T * D * 4 // world,
                         "d2h_bytes_per_step": nb * T * D * 4},
-                "comm": {"a2a_messages": comm.messages, "a2a_bytes": comm.bytes},
+                "comm": {"a2a_messages": comm.messages, "a2a_bytes": comm.bytes,
+                         "peer_barriers": eng.runner.xch.mesh.barriers if eng.runner.xch else 0},
                 "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
                 "cuda_graphs": "denoise passes captured once per block, replayed (IFX_CUDA_GRAPHS=0: eager)"}
         print(json.dumps(line), flush=True)
@@ -587,6 +603,11 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ulysses", action="store_true",
+                    help="run the Ulysses (multi-GPU) engine even at N = 1 (exchange overhead probe)")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N > 1: Ulysses re-shard through NVLink peer memory (scatter epilogues "
+                         "+ peer barriers) or NCCL all-to-alls")
     ap.add_argument("--rope", action="store_true",
                     help="3D RoPE on Q/K (3 x 30 x 52 grid), fused into the QKV GEMM epilogue")
     args = ap.parse_args()

@@ -520,14 +520,23 @@ class PeerMesh:
             _abi.check(L.ifx_ipc_handle(ctypes.c_void_p(self.buf.ptr), h), "ipc_handle")
             hs = [None] * W
             comm.dist.all_gather_object(hs, bytes(h), group=comm.group)
+            err = None
             for i in range(W):
                 if i == r:
                     bases.append(self.buf.ptr)
                     continue
                 pp = ctypes.c_void_p()
-                _abi.check(L.ifx_ipc_open(ctypes.c_char_p(hs[i]), ctypes.byref(pp)), "ipc_open")
+                rc = L.ifx_ipc_open(ctypes.c_char_p(hs[i]), ctypes.byref(pp))
+                if rc != _abi.OK:
+                    err = f"rank {r} cannot map rank {i}: {L.ifx_last_error().decode()}"
+                    break
                 self._opened.append(pp.value)
                 bases.append(pp.value)
+            errs = [None] * W  # every rank learns whether the mesh is complete
+            comm.dist.all_gather_object(errs, err, group=comm.group)
+            if any(errs):
+                self.close()
+                raise ConfigError("peer mesh: " + "; ".join(e for e in errs if e))
         comm.dist.barrier(group=comm.group)  # every pad zeroed before any barrier kernel
         self.bases = bases
         self._pads = (ctypes.c_void_p * W)(*bases)
