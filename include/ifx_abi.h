@@ -250,6 +250,18 @@ int ifx_attn_fwd(const ifx_attn_params* p, void* stream);
 /* bytes of `workspace` that allow ifx_attn_fwd to split the key range up to 8 ways */
 int ifx_attn_workspace_bytes(const ifx_attn_params* p, int64_t* bytes);
 
+/* K4 alone — merge n_splits attention partials over disjoint key shards (attention.py:
+ * 157-180; the ring strategies, parallel.py:172-298): part_o [n_splits, n_q, part_ld] bf16
+ * normalised outputs (heads*head_dim columns), part_m / part_l [n_splits, heads, n_q] fp32
+ * row max (log2 units, -inf = no visible key) and denominator w.r.t. it — exactly what
+ * ifx_attn_fwd writes with row_max / row_sum set. o = sum_s w_s O_s / sum_s w_s, w_s =
+ * l_s 2^(m_s - max m); if row_max != NULL the merged max / denominator are written too
+ * (denominator 0 = the row saw no key in any shard). */
+int ifx_attn_combine(const void* part_o, int64_t part_ld, const float* part_m,
+                     const float* part_l, int64_t n_splits, int64_t n_q, int64_t heads,
+                     int64_t head_dim, void* o, int64_t o_ld, float* row_max, float* row_sum,
+                     void* stream);
+
 /* Fused RMS-norm (engine.py:171-173) + optional time conditioning, fp32 in, bf16 out:
  * y = bf16( (x + t*tvec) / sqrt(mean((x + t*tvec)^2) + eps) ). If x_out != NULL the
  * conditioned fp32 row is also written there. tvec may be NULL. */
@@ -302,6 +314,10 @@ int ifx_copy_blocks(const void* src, void* dst, const int64_t* desc, int64_t n_b
 int ifx_ipc_handle(const void* dev_ptr, void* handle_out);
 int ifx_ipc_open(const void* handle, void** dev_ptr_out);
 int ifx_ipc_close(void* dev_ptr);
+/* Strided copy by the DMA copy engines (any direction; peers' mapped buffers included):
+ * `rows` rows of width_bytes from src (pitch spitch bytes) to dst (pitch dpitch). */
+int ifx_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,
+                 int64_t rows, void* stream);
 /* Barrier across the ranks of a peer mesh, enqueued on `stream` (graph-capturable): every
  * store this GPU issued before it (earlier kernels on the stream, e.g. a scatter epilogue
  * into peers' buffers) is visible to every peer after it, and vice versa. pads = host

@@ -42,11 +42,11 @@ EXPORTS = (
     "ifx_pt_batch_begin", "ifx_pt_batch_end", "ifx_pt_pending",
     "ifx_kv_append", "ifx_kv_gather", "ifx_kv_append_latent", "ifx_kv_gather_latent", "ifx_kv_move_pages", "ifx_kv_copy_runs", "ifx_host_alloc", "ifx_host_free",
     "ifx_dev_alloc", "ifx_dev_free",
-    "ifx_attn_fwd", "ifx_attn_workspace_bytes",
+    "ifx_attn_fwd", "ifx_attn_workspace_bytes", "ifx_attn_combine",
     "ifx_rms_bf16", "ifx_rope_qk", "ifx_group_softmax", "ifx_group_softmax_rs", "ifx_ulysses_pack", "ifx_ulysses_unpack",
     "ifx_copy_blocks", "ifx_gemm_bf16", "ifx_gemm_fused", "ifx_gemm_tiles_n",
     "ifx_noise_normal_f32",
-    "ifx_ipc_handle", "ifx_ipc_open", "ifx_ipc_close", "ifx_peer_barrier",
+    "ifx_ipc_handle", "ifx_ipc_open", "ifx_ipc_close", "ifx_memcpy2d", "ifx_peer_barrier",
 )
 
 
@@ -175,6 +175,8 @@ def lib() -> ctypes.CDLL:
             L.ifx_ipc_handle.argtypes = [P, P]
             L.ifx_ipc_open.argtypes = [P, ctypes.POINTER(P)]
             L.ifx_ipc_close.argtypes = [P]
+            L.ifx_memcpy2d.argtypes = [P, I64, P, I64, I64, I64, P]
+            L.ifx_attn_combine.argtypes = [P, I64, P, P, I64, I64, I64, I64, P, I64, P, P, P]
             L.ifx_peer_barrier.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P,
                                            ctypes.c_int, P]
             L.ifx_noise_normal_f32.argtypes = [ctypes.POINTER(ctypes.c_uint64), I64, P, ctypes.c_int]

@@ -350,6 +350,35 @@ int ifx_version(void) { return 1; }
 
 int ifx_attn_fwd(const ifx_attn_params* p, void* stream) { return ifx::attn_fwd(p, stream); }
 
+int ifx_attn_combine(const void* part_o, int64_t part_ld, const float* part_m,
+                     const float* part_l, int64_t n_splits, int64_t n_q, int64_t heads,
+                     int64_t head_dim, void* o, int64_t o_ld, float* row_max, float* row_sum,
+                     void* stream) {
+  if (head_dim != 64 && head_dim != 128) return ifx::fail(IFX_EUNSUPPORTED, "head_dim must be 64 or 128");
+  if (n_splits < 1 || n_q < 0 || heads < 1 || part_ld < heads * head_dim || o_ld < heads * head_dim ||
+      n_q > INT32_MAX || n_splits > INT32_MAX)
+    return ifx::fail(IFX_EDIM, "bad combine sizes");
+  if (part_o == nullptr || part_m == nullptr || part_l == nullptr || o == nullptr ||
+      (row_max == nullptr) != (row_sum == nullptr))
+    return ifx::fail(IFX_EDIM, "combine: null operand");
+  if (n_q == 0) return IFX_OK;
+  ifx::AttnKernelArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n_q = (int)n_q;
+  a.heads = (int)heads;
+  a.n_splits = (int)n_splits;
+  a.part_o = static_cast<__nv_bfloat16*>(const_cast<void*>(part_o));
+  a.part_ld = part_ld;
+  a.part_m = const_cast<float*>(part_m);
+  a.part_l = const_cast<float*>(part_l);
+  a.o = static_cast<__nv_bfloat16*>(o);
+  a.o_ld = o_ld;
+  a.row_max = row_max;
+  a.row_sum = row_sum;
+  return ifx::cuda_fail(ifx::attn_combine_launch(a, (int)head_dim, static_cast<cudaStream_t>(stream)),
+                        "attn_combine launch");
+}
+
 int ifx_attn_workspace_bytes(const ifx_attn_params* p, int64_t* bytes) {
   *bytes = ifx::split_workspace_bytes(p, 8);
   return IFX_OK;

@@ -642,7 +642,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     named_sync(pair_bar, 64);  // the partner has read `red` before the next item rewrites it
     }
-    if (a.o_peer_rows > 0) __threadfence_system();  // peer stores out before the barrier
+    // peer stores (O scatter, or partials written into a peer's arena) out before the
+    // barrier that publishes them
+    if (a.o_peer_rows > 0 || a.row_max != nullptr) __threadfence_system();
   }
 
   tc_fence_before();
@@ -689,7 +691,7 @@ __global__ void attn_combine_kernel(const AttnKernelArgs a) {
       a.row_sum[(int64_t)head * a.n_q + row] = den;
     }
   }
-  if (a.o_peer_rows > 0) __threadfence_system();
+  if (a.o_peer_rows > 0 || a.row_max != nullptr) __threadfence_system();
 }
 
 template <int HD>
@@ -724,6 +726,19 @@ int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
 }
 
 }  // namespace
+
+// K4 alone: merge n_splits partials a.part_o / part_m / part_l into a.o (the ring
+// strategies' partials, computed by separate K1 launches over key shards).
+int attn_combine_launch(const AttnKernelArgs& a, int head_dim, cudaStream_t st) {
+  const int64_t warps = (int64_t)a.n_q * a.heads;
+  const int n_sm = device_sms(current_device());
+  const int blocks = (int)((warps + 7) / 8 < n_sm * 16 ? (warps + 7) / 8 : n_sm * 16);
+  if (blocks == 0) return 0;
+  if (head_dim == 128) attn_combine_kernel<128><<<blocks, 256, 0, st>>>(a);
+  else if (head_dim == 64) attn_combine_kernel<64><<<blocks, 256, 0, st>>>(a);
+  else return -1;
+  return (int)cudaGetLastError();
+}
 
 int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int n_q, int heads, cudaStream_t st) {
   if (head_dim == 128) return launch<128>(a, n_q, heads, st);

@@ -79,5 +79,7 @@ int attn_few_keys_launch(const FewKeysArgs& a, int head_dim, cudaStream_t st);
 // Grid (ceil(n_q/128), heads, n_splits) x 320 threads (+ K4 combine when n_splits > 1).
 // Returns cudaError_t.
 int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int n_q, int heads, cudaStream_t st);
+// K4 alone over a.n_splits partials (part_o / part_m / part_l) into a.o.
+int attn_combine_launch(const AttnKernelArgs& a, int head_dim, cudaStream_t st);
 
 }  // namespace ifx

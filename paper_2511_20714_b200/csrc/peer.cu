@@ -99,6 +99,17 @@ int ifx_ipc_close(void* dev_ptr) {
   return ifx::cuda_status(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
 }
 
+int ifx_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,
+                 int64_t rows, void* stream) {
+  if (rows < 0 || width_bytes < 0 || dpitch < width_bytes || spitch < width_bytes)
+    return ifx::fail(IFX_EDIM, "bad 2-D copy");
+  if (rows == 0 || width_bytes == 0) return IFX_OK;
+  return ifx::cuda_status(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch,
+                                            (size_t)width_bytes, (size_t)rows, cudaMemcpyDefault,
+                                            static_cast<cudaStream_t>(stream)),
+                          "cudaMemcpy2DAsync");
+}
+
 int ifx_peer_barrier(void* const* pads, int world, int rank, uint32_t* counter, int timeout_ms,
                      void* stream) {
   if (world < 1 || world > ifx::kMaxPeers || rank < 0 || rank >= world || pads == nullptr ||

@@ -961,3 +961,337 @@ class UlyssesEngine:
                 lat = torch.cat(parts)
             out.append(lat)
         return out
+
+
+# ============================================ sequence-parallel attention across real ranks
+# The reference's three strategies (parallel.py:140-298) run on an in-process WorkerGroup;
+# these are their multi-GPU counterparts: each rank passes ITS shards and gets ITS output
+# rows. Transport is peer memory (a PeerMesh per comm, grown on demand): shards are staged
+# into each rank's arena, peers PULL what they need with the DMA copy engines over NVLink
+# (ifx_memcpy2d, overlapped with the previous step's K1 on a copy stream) or K1 / the copy
+# engines PUSH results into the owner's arena, and ifx_peer_barrier orders the phases. The
+# per-shard partials are K1's (normalised output, row max, denominator) and are merged by
+# K4 (`ifx_attn_combine`) — the reference's merge_partials / finalize_partial
+# (attention.py:157-180) on device.
+class SpTrace:
+    """Inter-rank traffic of the calls on this rank (sender != receiver): messages and
+    logical bytes (unpadded bf16 elements), like WorkerGroup.total_bytes."""
+
+    def __init__(self):
+        self.messages = 0
+        self.bytes = 0
+
+    def add(self, nbytes: int, messages: int = 1) -> None:
+        self.messages += messages
+        self.bytes += int(nbytes)
+
+
+def _sp_mesh(comm, nbytes: int) -> PeerMesh:
+    """The comm's sequence-parallel mesh, re-created (collectively: every rank asks for the
+    same size, which depends only on the global shard lengths) when too small."""
+    mesh = getattr(comm, "_sp_mesh", None)
+    if mesh is None or mesh.nbytes < nbytes:
+        if mesh is not None:
+            torch.cuda.synchronize()
+            mesh.close()
+        mesh = PeerMesh(comm, max(int(nbytes), 1 << 20))
+        comm._sp_mesh = mesh
+    return mesh
+
+
+class _SpCall:
+    """Arena layout of one sequence-parallel call (byte offsets identical on every rank)."""
+
+    def __init__(self, comm, q, k, v, heads, mask):
+        from .errors import MaskError
+        W, r = comm.world, comm.rank
+        q, k, v = (_dev(x) for x in (q, k, v))
+        if q.dim() != 2 or k.dim() != 2 or v.shape != k.shape or q.shape[1] != k.shape[1]:
+            raise DimensionError("q [n, d], k / v [m, d] shards expected")
+        d = q.shape[1]
+        if heads < 1 or d % heads:
+            raise DimensionError(f"model dim {d} not divisible by heads {heads}")
+        dh = d // heads
+        if dh > 128:
+            raise DimensionError("head_dim above 128 is not supported")
+        lens = [None] * W
+        comm.dist.all_gather_object(lens, (q.shape[0], k.shape[0]), group=comm.group)
+        self.q_lens, self.kv_lens = [a for a, _ in lens], [b for _, b in lens]
+        self.q_off = [0] + list(np.cumsum(self.q_lens))
+        self.kv_off = [0] + list(np.cumsum(self.kv_lens))
+        N, M = int(self.q_off[-1]), int(self.kv_off[-1])
+        if mask is None:
+            mask = np.ones((N, M), dtype=bool)
+        mk = torch.as_tensor(np.asarray(mask) if not isinstance(mask, torch.Tensor) else mask)
+        if tuple(mk.shape) != (N, M):
+            raise DimensionError(f"mask {tuple(mk.shape)} does not match [{N}, {M}]")
+        if not bool(mk.bool().any(dim=1).all()):  # scaled_dot_attention / finalize raise
+            raise MaskError("query row with no allowed key")
+        self.mask = mk.to(q.device, torch.uint8).contiguous()
+        self.W, self.r, self.heads, self.dh, self.d = W, r, heads, dh, d
+        self.dhp = 64 if dh <= 64 else 128
+        self.wp = heads * self.dhp  # padded row width (elements)
+        self.n_max, self.m_max = max(max(self.q_lens), 1), max(max(self.kv_lens), 1)
+        self.N, self.M = N, M
+        off = 0
+
+        def region(nbytes):
+            nonlocal off
+            o = off
+            off += (int(nbytes) + 255) // 256 * 256
+            return o
+        rb = self.wp * 2
+        self.o_qp, self.o_kp, self.o_vp = (region(self.n_max * rb), region(self.m_max * rb),
+                                           region(self.m_max * rb))
+        self.o_po = region(W * self.n_max * rb)
+        self.o_pm = region(W * heads * self.n_max * 4)
+        self.o_pl = region(W * heads * self.n_max * 4)
+        self.o_out = region(self.n_max * rb)
+        self.o_buf = region(2 * max(self.n_max, self.m_max) * rb * 2)  # pull double buffers
+        self.total = off
+        self.mesh = _sp_mesh(comm, self.total)
+        self.q, self.k, self.v = q, k, v
+        self.trace = getattr(comm, "sp_trace", None)
+        if self.trace is None:
+            self.trace = comm.sp_trace = SpTrace()
+
+    def local(self, off, rows, width, dtype=torch.bfloat16):
+        return self.mesh.local(off, rows, width, dtype)
+
+    def stage(self):
+        """Own shards -> the arena, each head zero-padded to dhp columns; partial slots
+        reset (max -inf, denominator 0: a shard without keys contributes nothing)."""
+        hp, dh = self.dhp, self.dh
+        for x, o in ((self.q, self.o_qp), (self.k, self.o_kp), (self.v, self.o_vp)):
+            n = x.shape[0]
+            dst = self.local(o, max(n, 1), self.wp)
+            dst.zero_()
+            if n:
+                src = x.to(torch.bfloat16).contiguous().view(n, self.heads, dh)
+                dst[:n].view(n, self.heads, hp)[:, :, :dh].copy_(src)
+        # partial slot s of this rank's rows: O [n, wp] at o_po + s*n*rb, max / denominator
+        # [heads, n] at o_pm / o_pl + s*heads*n*4 (K1's statistics layout, K4's input)
+        self.local(self.o_po, self.W * self.n_max, self.wp).zero_()  # 0-weight slots stay finite
+        self.local(self.o_pm, self.W * self.heads, self.n_max, torch.float32).fill_(float("-inf"))
+        self.local(self.o_pl, self.W * self.heads, self.n_max, torch.float32).zero_()
+
+    def slot(self, owner: int, s: int):
+        """Addresses (in owner's arena) of partial slot s of owner's rows."""
+        n, rb = self.q_lens[owner], self.wp * 2
+        a = self.mesh.addr
+        return (a(owner, self.o_po + s * n * rb), a(owner, self.o_pm + s * self.heads * n * 4),
+                a(owner, self.o_pl + s * self.heads * n * 4))
+
+    def pull(self, dst, src, width_b, rows, dpitch, spitch, stream):
+        from ._device import stream_ptr
+        if rows:
+            _abi.check(_abi.lib().ifx_memcpy2d(dst, dpitch, src, spitch, width_b, rows,
+                                               stream_ptr(stream)), "memcpy2d")
+
+    def partial(self, q_t, k_t, v_t, n_k, mask_view, po, pm, pl):
+        """K1 over one key shard with partial statistics, written to (po, pm, pl) (raw
+        addresses, possibly in a peer's arena)."""
+        from ._device import attn_fwd
+        if q_t.shape[0] == 0 or n_k == 0:
+            return
+        p_out = _RawRows(po, q_t.shape[0], self.wp)
+        attn_fwd(q_t, self.heads, self.dhp, p_out, k_t, v_t, 0, n_k, scale=1.0 / math.sqrt(self.dh),
+                 mask=mask_view, row_max=_RawRows(pm, 1, 1, torch.float32),
+                 row_sum=_RawRows(pl, 1, 1, torch.float32), split_kv=False)
+
+    def combine(self):
+        from ._device import count_launch, stream_ptr
+        n = self.q_lens[self.r]
+        out = self.local(self.o_out, self.n_max, self.wp)
+        if n:
+            mesh = self.mesh
+            _abi.check(_abi.lib().ifx_attn_combine(
+                mesh.addr(self.r, self.o_po), self.wp, mesh.addr(self.r, self.o_pm),
+                mesh.addr(self.r, self.o_pl), self.W, n, self.heads, self.dhp,
+                out.data_ptr(), self.wp, None, None, stream_ptr()), "attn_combine")
+            count_launch()
+        return out
+
+    def result(self, out):
+        n = self.q_lens[self.r]
+        y = out[:n].view(n, self.heads, self.dhp)[:, :, :self.dh].reshape(n, self.d)
+        return y.float()
+
+
+class _RawRows:
+    """A [rows, width] stand-in for attn_fwd's output / statistics arguments at a raw device
+    address (e.g. inside a peer's arena): attn_fwd only reads data_ptr() and the row stride."""
+
+    def __init__(self, addr: int, rows: int, width: int, dtype=torch.bfloat16):
+        self._addr, self.shape, self.dtype = int(addr), (rows, width), dtype
+
+    def data_ptr(self) -> int:
+        return self._addr
+
+    def stride(self, dim=None):
+        s = (self.shape[1], 1)
+        return s if dim is None else s[dim]
+
+    def dim(self) -> int:
+        return 2
+
+
+def ulysses_attention_dist(comm, q, k, v, heads: int, mask=None):
+    """parallel.py:140-169 across real ranks. Each rank pulls its heads' columns of every
+    rank's Q/K/V shard (copy engines, NVLink), attends them over the whole sequence with
+    one K1, and pushes each owner's output rows into its arena; two peer barriers."""
+    W, r = comm.world, comm.rank
+    if heads % W:
+        raise DimensionError(f"heads {heads} not divisible by world_size {W}")
+    c = _SpCall(comm, q, k, v, heads, mask)
+    mesh, hl = c.mesh, heads // W
+    hw, rb = hl * c.dhp * 2, c.wp * 2
+    c.stage()
+    # pull region (reused): Q [N, hl*dhp] | K [M, hl*dhp] | V [M, hl*dhp] | O [N, hl*dhp]
+    need = (2 * c.N + 2 * c.M) * hw
+    buf = torch.empty(need // 2, device=c.q.device, dtype=torch.bfloat16)
+    uq = buf[:c.N * hw // 2].view(c.N, hl * c.dhp)
+    uk = buf[c.N * hw // 2:(c.N + c.M) * hw // 2].view(c.M, hl * c.dhp)
+    uv = buf[(c.N + c.M) * hw // 2:(c.N + 2 * c.M) * hw // 2].view(c.M, hl * c.dhp)
+    uo = buf[(c.N + 2 * c.M) * hw // 2:].view(c.N, hl * c.dhp)
+    mesh.barrier()
+    st = torch.cuda.current_stream()
+    for i in range(W):
+        col = r * hw
+        c.pull(uq[c.q_off[i]:].data_ptr(), mesh.addr(i, c.o_qp) + col, hw, c.q_lens[i], hw, rb, st)
+        c.pull(uk[c.kv_off[i]:].data_ptr(), mesh.addr(i, c.o_kp) + col, hw, c.kv_lens[i], hw, rb, st)
+        c.pull(uv[c.kv_off[i]:].data_ptr(), mesh.addr(i, c.o_vp) + col, hw, c.kv_lens[i], hw, rb, st)
+        if i != r:
+            c.trace.add(hl * c.dh * 2 * (c.q_lens[i] + 2 * c.kv_lens[i]))
+    from ._device import attn_fwd
+    attn_fwd(uq, hl, c.dhp, uo, uk, uv, 0, c.M, scale=1.0 / math.sqrt(c.dh), mask=c.mask)
+    for i in range(W):  # each owner's rows of this rank's heads -> the owner's arena
+        c.pull(mesh.addr(i, c.o_out) + r * hw, uo[c.q_off[i]:].data_ptr(), hw, c.q_lens[i], rb, hw, st)
+        if i != r:
+            c.trace.add(hl * c.dh * 2 * c.q_lens[i])
+    mesh.barrier()
+    out = c.result(c.local(c.o_out, c.n_max, c.wp))
+    mesh.barrier()  # nobody re-stages this arena while a peer still reads it
+    return out
+
+
+def ring_attention_pass_kv_dist(comm, q, k, v, mask=None, heads: int = 1):
+    """parallel.py:172-244 across real ranks: the K/V shards visit every rank in ring order
+    (owner r-s at step s); the next shard is pulled from its owner's arena on a copy stream
+    while K1 attends the current one; one partial per step, merged by K4."""
+    W, r = comm.world, comm.rank
+    c = _SpCall(comm, q, k, v, heads, mask)
+    mesh, rb = c.mesh, c.wp * 2
+    c.stage()
+    mesh.barrier()
+    main = torch.cuda.current_stream()
+    cp = torch.cuda.Stream()
+    n = c.q_lens[r]
+    qv = c.local(c.o_qp, c.n_max, c.wp)[:n]
+    bufs = [(c.o_buf + j * 2 * c.m_max * rb, c.o_buf + (j * 2 + 1) * c.m_max * rb) for j in range(2)]
+    ready = [torch.cuda.Event() for _ in range(W)]
+    free = [torch.cuda.Event() for _ in range(2)]
+
+    def fetch(s):
+        o = (r - s) % W
+        kb, vb = bufs[s % 2]
+        if s >= 2:
+            cp.wait_event(free[s % 2])
+        c.pull(mesh.addr(r, kb), mesh.addr(o, c.o_kp), rb, c.kv_lens[o], rb, rb, cp)
+        c.pull(mesh.addr(r, vb), mesh.addr(o, c.o_vp), rb, c.kv_lens[o], rb, rb, cp)
+        ready[s].record(cp)
+        c.trace.add(2 * c.kv_lens[o] * c.d * 2)
+    cp.wait_stream(main)
+    if W > 1:
+        fetch(1)
+    for s in range(W):
+        o = (r - s) % W
+        if s == 0:
+            kt, vt = c.local(c.o_kp, c.m_max, c.wp), c.local(c.o_vp, c.m_max, c.wp)
+        else:
+            main.wait_event(ready[s])
+            kb, vb = bufs[s % 2]
+            kt, vt = c.local(kb, c.m_max, c.wp), c.local(vb, c.m_max, c.wp)
+        if s + 1 < W and s + 1 >= 2:  # buffer (s+1)%2 was read by step s-1's K1
+            free[(s + 1) % 2].record(main)
+            fetch(s + 1)
+        po, pm, pl = c.slot(r, s)
+        mv = c.mask[c.q_off[r]:c.q_off[r] + n, c.kv_off[o]:c.kv_off[o] + c.kv_lens[o]]
+        c.partial(qv, kt, vt, c.kv_lens[o], mv, po, pm, pl)
+    out = c.result(c.combine())
+    mesh.barrier()  # every peer finished pulling this rank's shards
+    return out
+
+
+def ring_attention_pass_q_dist(comm, q, k, v, mask=None, heads: int = 1):
+    """parallel.py:247-298 across real ranks: K/V stay; every rank's Q visits this rank
+    (pulled from its owner's arena on a copy stream, overlapping the previous step), K1
+    writes the partial of that Q against the local K/V straight into the OWNER's partial
+    slot (its arena, over NVLink), and after one peer barrier each owner merges its W
+    partials with K4 (the reference's traveling partial + final gather, reassociated)."""
+    W, r = comm.world, comm.rank
+    c = _SpCall(comm, q, k, v, heads, mask)
+    mesh, rb = c.mesh, c.wp * 2
+    c.stage()
+    mesh.barrier()
+    main = torch.cuda.current_stream()
+    cp = torch.cuda.Stream()
+    m = c.kv_lens[r]
+    kt, vt = c.local(c.o_kp, c.m_max, c.wp), c.local(c.o_vp, c.m_max, c.wp)
+    bufs = [c.o_buf + j * c.n_max * rb for j in range(2)]
+    ready = [torch.cuda.Event() for _ in range(W)]
+    free = [torch.cuda.Event() for _ in range(2)]
+
+    def fetch(s):
+        o = (r - s) % W
+        if s >= 2:
+            cp.wait_event(free[s % 2])
+        c.pull(mesh.addr(r, bufs[s % 2]), mesh.addr(o, c.o_qp), rb, c.q_lens[o], rb, rb, cp)
+        ready[s].record(cp)
+        c.trace.add(c.q_lens[o] * c.d * 2)
+    cp.wait_stream(main)
+    if W > 1:
+        fetch(1)
+    for s in range(W):
+        o = (r - s) % W
+        if s == 0:
+            qt = c.local(c.o_qp, c.n_max, c.wp)[:c.q_lens[o]]
+        else:
+            main.wait_event(ready[s])
+            qt = c.local(bufs[s % 2], c.n_max, c.wp)[:c.q_lens[o]]
+        if s + 1 < W and s + 1 >= 2:
+            free[(s + 1) % 2].record(main)
+            fetch(s + 1)
+        # the partial lands in owner o's slot r: partials (normalised O, max, denominator)
+        po, pm, pl = c.slot(o, r)
+        mv = c.mask[c.q_off[o]:c.q_off[o] + c.q_lens[o], c.kv_off[r]:c.kv_off[r] + m]
+        c.partial(qt, kt, vt, m, mv, po, pm, pl)
+        if o != r and m and c.q_lens[o]:
+            c.trace.add(c.q_lens[o] * (c.d + 2 * c.heads) * 2)
+    mesh.barrier()
+    out = c.result(c.combine())
+    mesh.barrier()
+    return out
+
+
+STRATEGY_FNS = {"ulysses": ulysses_attention_dist, "ring_pass_kv": ring_attention_pass_kv_dist,
+                "ring_pass_q": ring_attention_pass_q_dist}
+
+
+def sequence_parallel_attention(comm, q, k, v, heads: int, mask=None, strategy: str | None = None,
+                                link: LinkCostModel | None = None):
+    """The strategy menu of parallel.py:300-364 dispatched on real ranks: `strategy` None
+    picks choose_strategy(seq_len, heads, world, link, head_dim) on the global length (the
+    default link model is NVLink-like: 5 us per message, 1/700 GB/s per byte). Returns
+    (this rank's output rows [n, d] fp32, the strategy used)."""
+    if strategy is None:
+        lens = [None] * comm.world
+        comm.dist.all_gather_object(lens, int(_dev(q).shape[0]), group=comm.group)
+        d = _dev(q).shape[1]
+        link = link or LinkCostModel(cost_per_message=5e-6, cost_per_byte=1.0 / 700e9)
+        strategy = choose_strategy(sum(lens), heads, comm.world, link, head_dim=d // heads)["strategy"]
+    if strategy not in STRATEGY_FNS:
+        raise DimensionError(f"unknown strategy {strategy!r}")
+    fn = STRATEGY_FNS[strategy]
+    out = fn(comm, q, k, v, heads, mask) if strategy == "ulysses" else fn(comm, q, k, v, mask, heads)
+    return out, strategy
