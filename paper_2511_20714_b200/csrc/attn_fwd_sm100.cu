@@ -55,14 +55,6 @@ constexpr int NB = 2;            // S buffers in TMEM (P aliases S)
 constexpr int NTHREADS = 320;    // 10 warps
 constexpr int NSOFT = 256;       // softmax threads
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if max grows > 2^8
-// S_j = Q K_j^T as two N = 64 MMAs, one per key half, each with its own completion barrier
-// (and per-half S / PV hand-off barriers): half 0's softmax starts while half 1's QK^T still
-// runs, so the two softmax warps of a sub-partition are offset instead of hitting MUFU and
-// TMEM together.
-#ifndef IFX_K1_HALF_QK
-#define IFX_K1_HALF_QK 0  // measured slower: profiles/r05_k1_half_qk.md
-#endif
-constexpr bool kHalfQK = IFX_K1_HALF_QK != 0;
 #ifndef IFX_POLY_PAIRS_OF_8
 #define IFX_POLY_PAIRS_OF_8 2  // r03 power-capped bench: 1-2 beat 3 (profiles/r03_attn_poly.md)
 #endif
@@ -110,9 +102,8 @@ struct Layout {
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
   static constexpr int OFF_RED = OFF_V + NS * KV_BYTES;  // float [2 halves][3][BM] merge swap
   static constexpr int OFF_BAR = OFF_RED + 2 * 3 * BM * 4;
-  // q_full[2] q_empty[2] k_full k_empty v_full v_empty s_full[2] s_empty[2] p_full[2]
-  // pv_done[2] o_free (the [2]s per S buffer: one per key half)
-  static constexpr int NBAR = 4 + 4 * NS + 8 * NB + 1;
+  // q_full[2] q_empty[2] k_full k_empty v_full v_empty s_full s_empty p_full[2] pv_done o_free
+  static constexpr int NBAR = 4 + 4 * NS + 5 * NB + 1;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
   // TMEM columns: S0 [0,128) S1 [128,256) O_lo [256, 256+HD) O_hi [384, 384+HD).
   // Key half h of S_b (columns 64h..64h+63) is overwritten in place by its packed bf16 P
@@ -181,11 +172,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* k_empty = k_full + NS;
   uint64_t* v_full = k_empty + NS;
   uint64_t* v_empty = v_full + NS;
-  uint64_t* s_full = v_empty + NS;    // [NB][2 key halves] (half 1 unused without kHalfQK)
-  uint64_t* s_empty = s_full + 2 * NB;
-  uint64_t* p_full = s_empty + 2 * NB;
+  uint64_t* s_full = v_empty + NS;
+  uint64_t* s_empty = s_full + NB;
+  uint64_t* p_full = s_empty + NB;   // [NB][2 key halves]
   uint64_t* pv_done = p_full + 2 * NB;
-  uint64_t* o_free = pv_done + 2 * NB;  // the softmax warps have read O of their current item
+  uint64_t* o_free = pv_done + NB;  // the softmax warps have read O of their current item
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NBAR);
 
   const int warp = warp_id();
@@ -207,12 +198,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(v_empty + s, 1);
     }
     for (int b = 0; b < NB; ++b) {
-      for (int h = 0; h < 2; ++h) {
-        mbar_init(s_full + 2 * b + h, 1);
-        mbar_init(s_empty + 2 * b + h, kHalfQK ? NSOFT / 2 : NSOFT);
-        mbar_init(p_full + 2 * b + h, NSOFT / 2);
-        mbar_init(pv_done + 2 * b + h, 1);
-      }
+      mbar_init(s_full + b, 1);
+      mbar_init(s_empty + b, NSOFT);
+      mbar_init(p_full + 2 * b, NSOFT / 2);
+      mbar_init(p_full + 2 * b + 1, NSOFT / 2);
+      mbar_init(pv_done + b, 1);
     }
     fence_barrier_init();
   }
@@ -370,7 +360,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ===================== MMA issuer =====================
     if (elect_one()) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);  // Q, K both K-major
-      constexpr uint32_t idesc_qk_h = idesc_bf16_f32(BM, HALF, 0, 0);  // one key half
       constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, HD, 0, 1);  // P (TMEM), V MN-major
       int g0 = 0;  // key tiles of earlier items (ring / S-buffer position)
       for (int it = blockIdx.x, k = 0; it < n_items; it += gridDim.x, ++k) {
@@ -386,44 +375,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int b = gj % NB;
             const uint32_t bph = (gj / NB) & 1;
             mbar_wait(k_full + s, (gj / NS) & 1);
-            const uint32_t k_base = smem_u32(sK + s * L::KV_BYTES);
+            mbar_wait(s_empty + b, bph ^ 1);                    // S_b of tile gj-NB read
             // P_b aliases S_b: explicit wait for PV(gj-NB) before QK(gj) overwrites it. The
             // PTX guarantees in-order execution only between MMAs on the same accumulator,
             // and PV and QK^T use different ones; dropping the wait measured +0.3 % in the
             // bench (profiles/r03_k1_persistent.md), not worth a possible WAR race.
-            if (kHalfQK) {
+            if (gj >= NB) mbar_wait(pv_done + b, bph ^ 1);
+            tc_fence_after();
+            const uint32_t k_base = smem_u32(sK + s * L::KV_BYTES);
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {  // S_b[:, 64h..] = Q K_j[64h .. 64h+63]^T
-                mbar_wait(s_empty + 2 * b + h, bph ^ 1);
-                if (gj >= NB) mbar_wait(pv_done + 2 * b + h, bph ^ 1);
-                tc_fence_after();
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                  const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-                  const uint32_t offk = (kk >> 2) * (BN * 128) + h * HALF * 128 + (kk & 3) * 32;
-                  mma_bf16_ss(tmem + b * 128 + h * HALF, smem_desc_sw128(q_base + off, 16, 1024),
-                              smem_desc_sw128(k_base + offk, 16, 1024), idesc_qk_h, kk > 0);
-                }
-                mma_commit(s_full + 2 * b + h);
-              }
-              mma_commit(k_empty + s);
-            } else {
-              mbar_wait(s_empty + 2 * b, bph ^ 1);              // S_b of tile gj-NB read
-              if (gj >= NB) {
-                mbar_wait(pv_done + 2 * b, bph ^ 1);
-                mbar_wait(pv_done + 2 * b + 1, bph ^ 1);
-              }
-              tc_fence_after();
-#pragma unroll
-              for (int kk = 0; kk < HD / 16; ++kk) {
-                const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-                const uint32_t offk = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-                mma_bf16_ss(tmem + b * 128, smem_desc_sw128(q_base + off, 16, 1024),
-                            smem_desc_sw128(k_base + offk, 16, 1024), idesc_qk, kk > 0);
-              }
-              mma_commit(k_empty + s);
-              mma_commit(s_full + 2 * b);
+            for (int kk = 0; kk < HD / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+              const uint32_t offk = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
+              mma_bf16_ss(tmem + b * 128, smem_desc_sw128(q_base + off, 16, 1024),
+                          smem_desc_sw128(k_base + offk, 16, 1024), idesc_qk, kk > 0);
             }
+            mma_commit(k_empty + s);
+            mma_commit(s_full + b);
           }
           if (k >= 1 && j == (n_tiles > 0 ? 1 : 0)) {
             // O is overwritten by this item's first PV: the previous item's epilogue must
@@ -451,9 +419,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mma_bf16_ts(tmem + L::TM_O(h), tmem + b * 128 + L::TM_P(h) + kk * 8, bdesc,
                             idesc_pv, (j > 1 || kk > 0) ? 1u : 0u);
               }
-              mma_commit(pv_done + 2 * b + h);
             }
             mma_commit(v_empty + s);
+            mma_commit(pv_done + b);
           }
         }
         mma_commit(q_empty + ib);  // this item's QK^T MMAs have read its Q buffer
@@ -489,7 +457,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int b = gj % NB;
       const int jt = t0 + j;
       const int c0 = half * HALF;  // first key column of this warp
-      mbar_wait(s_full + 2 * b + (kHalfQK ? half : 0), (gj / NB) & 1);
+      mbar_wait(s_full + b, (gj / NB) & 1);
       tc_fence_after();
       float sv[HALF];
 #pragma unroll
@@ -501,7 +469,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(s_empty + 2 * b + (kHalfQK ? half : 0));
+      mbar_arrive(s_empty + b);
 
       const bool full = mrow == nullptr && jt != part0 && jt != part1 && jt != part2;
       if (!full) {
@@ -574,7 +542,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (__any_sync(0xffffffffu, rescale_o)) {  // O_half *= alpha once PV_{j-1} landed
         const float f = rescale_o ? alpha : 1.f;
         const int jp = gj - 1;
-        mbar_wait(pv_done + 2 * (jp % NB) + half, (jp / NB) & 1);
+        mbar_wait(pv_done + (jp % NB), (jp / NB) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
@@ -601,9 +569,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     // ---------------- epilogue: O / l -> bf16 -> global (this warp's half of O) --------
     if (n_tiles > 0) {
-      const int jl = g0 + n_tiles - 1;  // both halves' accumulators are read below
-      mbar_wait(pv_done + 2 * (jl % NB), (jl / NB) & 1);
-      mbar_wait(pv_done + 2 * (jl % NB) + 1, (jl / NB) & 1);
+      const int jl = g0 + n_tiles - 1;
+      mbar_wait(pv_done + (jl % NB), (jl / NB) & 1);
       tc_fence_after();
     }
     g0 += n_tiles;
