@@ -119,9 +119,20 @@ def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad, p2p):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    # directly against the numpy oracle (the reference restated, pinned by the golden
+    # fixtures), not only against the single-GPU engine
+    from oracle import engine as OE
+    ocfg = dict(cfg)
+    oreq = OE.GenerationRequest(schedule=OE.DenoiseSchedule([1.0, 0.5]), **REQ)
+    okv = None
+    if kvc:
+        from oracle.kvcache import KvConfig as OKv
+        okv = OKv(**kvc)
+    want, _ = OE.generate_sequence(OE.ToyModel(OE.ModelConfig(**ocfg)), oreq, kv_config=okv)
     for rank, lats, state, nbytes in res:
-        for a, b in zip(lats, ref):
+        for a, b, w in zip(lats, ref, want):
             assert np.abs(a - b.latent).max() <= 2e-2, rank
+            assert np.abs(a - w).max() <= 2e-2, rank
         # replicated page table == single-GPU page table == reference semantics
         assert state == ref_eng.cache.state()
         assert nbytes > 0  # bytes through the all-to-alls, or peer barriers
@@ -130,6 +141,49 @@ def test_ulysses_engine_matches_single_gpu(world, cfg, kvc, pad, p2p):
 
 
 GRAPH_STEPS = [1.0, 0.75, 0.5]
+
+
+def _a2a_var_capture(port, q):
+    """NCCL's variable-size all-to-all (the balanced plan's re-shard) inside a CUDA graph
+    capture on a world-1 group: recorded once, replayed with new data."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2511_20714_b200.parallel import UlyssesComm
+        comm = UlyssesComm()
+        send = torch.zeros(1000, device="cuda", dtype=torch.bfloat16)
+        recv = torch.zeros(1000, device="cuda", dtype=torch.bfloat16)
+        comm.a2a_var(send, [1000], recv, [1000])  # warm-up outside the capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            comm.a2a_var(send, [1000], recv, [1000])
+            g.capture_end()
+        ok = []
+        for i in range(3):
+            send.copy_(torch.arange(1000, device="cuda").to(torch.bfloat16) * (i + 1))
+            g.replay()
+            torch.cuda.synchronize()
+            ok.append(bool(torch.equal(recv, send)))
+        del g
+        torch.cuda.synchronize()
+        q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ulysses_a2a_var_nccl_graph_capture_world1():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_a2a_var_capture, args=(_free_port(), q))
+    p.start()
+    ok = q.get(timeout=300)
+    p.join(timeout=120)
+    assert p.exitcode == 0 and ok == [True, True, True]
 
 
 def _rank_nccl(port, q, p2p=False):
