@@ -369,7 +369,8 @@ typedef struct ifx_gemm_params {
    * b = col / scatter_w (scatter_blocks of them) goes to up to two destinations, DEVICE
    * int64 scatter[(b*2 + e)*4 + {0,1,2,3}] = {address, row stride in bytes, row_lo,
    * row_hi}: row r in [row_lo, row_hi) is stored at address + r*stride + (col % scatter_w)*2
-   * (rows outside are skipped; row_hi = 0 marks an unused entry). Addresses are this
+   * (rows outside are skipped; row_hi = 0 marks an unused entry); scatter_w is a multiple
+   * of 32. Addresses are this
    * process's mappings of peers' buffers (ifx_ipc_open). c may then be NULL. */
   const int64_t* scatter; int64_t scatter_w; int64_t scatter_blocks;
 } ifx_gemm_params;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -226,9 +227,13 @@ int choose_splits(const ifx_attn_params* p) {
     const double w = (double)(ctas * s) / sms;
     return w / std::ceil(w);
   };
+  static const int min_tiles = [] {  // key tiles per split at least (A/B: IFX_K1_MIN_SPLIT_TILES)
+    const char* e = std::getenv("IFX_K1_MIN_SPLIT_TILES");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
   int best = 1;
   double best_eff = eff(1);
-  for (int s = 2; s <= 8 && tiles / s >= 16; ++s) {
+  for (int s = 2; s <= 8 && tiles / s >= min_tiles; ++s) {
     if (p->workspace_bytes < split_workspace_bytes(p, s)) break;
     if (eff(s) > best_eff + 0.05) {
       best = s;
@@ -245,10 +250,10 @@ int gemm_fused(const ifx_gemm_params* p, int64_t* out_tiles_n, void* stream) {
   if (p->m < 0 || p->n < 1 || p->k < 1 || p->lda < p->k || p->ldb < p->n ||
       (p->c != nullptr && p->ldc < p->n) || (p->c == nullptr && !scat))
     return fail(IFX_EDIM, "bad GEMM sizes");
-  if (scat && (p->c_type != IFX_BF16 || p->scatter_w < 8 || p->scatter_w % 8 ||
+  if (scat && (p->c_type != IFX_BF16 || p->scatter_w < 32 || p->scatter_w % 32 ||
                p->scatter_w * p->scatter_blocks < p->n || p->scatter_w > INT32_MAX ||
                p->scatter_blocks > INT32_MAX))
-    return fail(IFX_EDIM, "peer scatter needs a bf16 output in 8-column-aligned blocks covering N");
+    return fail(IFX_EDIM, "peer scatter needs a bf16 output in 32-column-aligned blocks covering N");
   if (p->n % 8) return fail(IFX_EDIM, "GEMM N must be a multiple of 8");
   if (p->m > INT32_MAX || p->n > INT32_MAX || p->k > INT32_MAX)
     return fail(IFX_EDIM, "GEMM extents must fit int32");

@@ -425,6 +425,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
                          : "memory");
           __syncwarp();
           const int col = col0 + 8 * bj;
+          // peer scatter: a 32-column chunk lies in one column block (scat_w % 32 == 0), so
+          // its (<= 2) destinations are read once per chunk, not per store
+          uint8_t* sc_base[2] = {nullptr, nullptr};
+          int64_t sc_ld[2] = {0, 0}, sc_lo[2] = {0, 0}, sc_hi[2] = {0, 0};
+          if (a.scat != nullptr && col0 < a.N) {
+            const int blk = col0 / a.scat_w;
+            const int64_t* d = a.scat + (int64_t)blk * 8;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              sc_ld[e] = __ldg(d + 4 * e + 1);
+              sc_lo[e] = __ldg(d + 4 * e + 2);
+              sc_hi[e] = __ldg(d + 4 * e + 3);
+              sc_base[e] = reinterpret_cast<uint8_t*>(__ldg(d + 4 * e)) +
+                           (int64_t)(col - blk * a.scat_w) * 2;
+            }
+          }
           int pstream = -1;  // page write: 0 = K stream, 1 = V stream of this chunk
           int64_t poff = 0;
           if (a.slots != nullptr) {
@@ -448,15 +464,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
               if (a.c != nullptr)
                 *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.c) + rr * a.ldc + col) = o;
               if (a.scat != nullptr) {  // straight into the consumer rank's buffer (NVLink)
-                const int blk = col / a.scat_w;
-                const int64_t* d = a.scat + (int64_t)blk * 8;
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  if (rr >= __ldg(d + 4 * e + 2) && rr < __ldg(d + 4 * e + 3))
-                    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(__ldg(d + 4 * e)) +
-                                              rr * __ldg(d + 4 * e + 1) +
-                                              (int64_t)(col - blk * a.scat_w) * 2) = o;
-                }
+                for (int e = 0; e < 2; ++e)
+                  if (rr >= sc_lo[e] && rr < sc_hi[e])
+                    *reinterpret_cast<uint4*>(sc_base[e] + rr * sc_ld[e]) = o;
               }
               if (pstream >= 0) {
                 const int64_t rel = a.rel0 + rr;

@@ -497,6 +497,8 @@ class PeerMesh:
     HEAD = 256  # pad (uint32[8]) at 0, this rank's epoch counter at 64, data from 256
 
     def __init__(self, comm, nbytes: int, timeout_ms: int | None = None):
+        if getattr(comm, "loopback", False):
+            return self._init_loopback(comm, nbytes, timeout_ms)
         import ctypes
         import os
 
@@ -544,6 +546,30 @@ class PeerMesh:
         self.timeout_ms = int(timeout_ms or os.environ.get("IFX_PEER_TIMEOUT_MS", 60000))
         self.barriers = 0
 
+    def _init_loopback(self, comm, nbytes, timeout_ms):
+        """One process standing in for rank comm.rank of comm.world (tools/rank_probe.py):
+        every 'peer' arena is a slice of one local allocation, barriers pass at once. The
+        kernels run exactly one rank's launches (the scatter stores land in local HBM
+        instead of crossing NVLink; peers' rows stay stale): a compute-only timing probe."""
+        import ctypes
+        import os
+
+        from .engine import _DevBuf
+        self.comm, W = comm, comm.world
+        self.nbytes = int(nbytes)
+        self.stride = (self.HEAD + self.nbytes + 255) // 256 * 256
+        self.buf = _DevBuf(self.stride * W)
+        raw = torch.as_tensor(self.buf, device=torch.device("cuda", torch.cuda.current_device()))
+        raw.zero_()
+        self._opened = []
+        self.bases = [self.buf.ptr + p * self.stride for p in range(W)]
+        self._own = self.bases[comm.rank]
+        self._pads = (ctypes.c_void_p * 1)(self._own)
+        self._counter = ctypes.c_void_p(self._own + 64)
+        self.timeout_ms = int(timeout_ms or os.environ.get("IFX_PEER_TIMEOUT_MS", 60000))
+        self.barriers = 0
+        self.loopback = True
+
     def addr(self, peer: int, offset: int = 0) -> int:
         """Address (in this process) of byte `offset` of `peer`'s data region."""
         return self.bases[peer] + self.HEAD + int(offset)
@@ -553,11 +579,14 @@ class PeerMesh:
         t = torch.as_tensor(self.buf, device=torch.device("cuda", torch.cuda.current_device()))
         es = torch.empty((), dtype=dtype).element_size()
         n = rows * width * es
-        return t[self.HEAD + offset:self.HEAD + offset + n].view(dtype).view(rows, width)
+        o = self.HEAD + offset + (self._own - self.buf.ptr if getattr(self, "loopback", False) else 0)
+        return t[o:o + n].view(dtype).view(rows, width)
 
     def barrier(self) -> None:
         from ._device import count_launch, stream_ptr
-        _abi.check(_abi.lib().ifx_peer_barrier(self._pads, self.comm.world, self.comm.rank,
+        lb = getattr(self, "loopback", False)
+        _abi.check(_abi.lib().ifx_peer_barrier(self._pads, 1 if lb else self.comm.world,
+                                               0 if lb else self.comm.rank,
                                                self._counter, self.timeout_ms, stream_ptr()),
                    "peer_barrier")
         count_launch()
@@ -574,6 +603,20 @@ class PeerMesh:
             self.close()
         except Exception:  # interpreter shutdown
             pass
+
+
+class LoopbackComm:
+    """Stand-in for UlyssesComm in a single process that runs ONE rank's share of a W-rank
+    Ulysses job (tools/rank_probe.py): the world-1 process group does the plumbing, the peer
+    mesh loops back (PeerMesh._init_loopback). Timing only — other ranks' data never arrive."""
+
+    loopback = True
+
+    def __init__(self, world: int, rank: int = 0):
+        import torch.distributed as dist
+        self.dist, self.group = dist, None
+        self.world, self.rank = world, rank
+        self.messages = self.bytes = 0
 
 
 class P2PExchange:

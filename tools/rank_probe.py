@@ -1,0 +1,136 @@
+"""Compute-only timing of ONE rank's share of a W-rank Ulysses rollout, on one GPU.
+
+    python tools/rank_probe.py [--configs c2 c4] [--worlds 1 2 4 8] [--ranks 0]
+
+The Ulysses engine runs with a LoopbackComm (parallel.py): rank r of W with exactly the
+kernels it launches in the real job (GEMMs on n = T/W rows, the QKV scatter epilogue, K1
+over its heads / balanced segments for all T queries, the O scatter, peer barriers), but
+every peer arena is local memory and barriers pass at once — no NVLink time, no waiting
+for slower ranks. ms_rank is therefore a lower bound of the W-GPU step; W * value_1 /
+value_W compares it to perfect strong scaling. Prints one JSON line per (config, W, rank).
+"""
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+
+def _profile(roll, name, W, r):
+    import collections
+
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        roll()
+        torch.cuda.synchronize()
+    path = f"/tmp/rank_trace_{os.getpid()}.json"
+    prof.export_chrome_trace(path)
+    ev = json.load(open(path))["traceEvents"]
+    os.unlink(path)
+    k = [e for e in ev if e.get("cat") == "kernel" and "dur" in e]
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for e in k:
+        n = e["name"]
+        if "gemm_kernel" in n:
+            key = "G1 " + n[n.index("gemm_kernel"):n.index(">", n.index("gemm_kernel")) + 1]
+        elif "nvjet" in n or "cutlass" in n or "cublas" in n.lower() or "gemm" in n.lower():
+            key = "cuBLASLt"
+        else:
+            import re
+            m = re.search(r"::(\w+)(<[^()]*>)?\(", n.replace("(anonymous namespace)", "anon"))
+            key = (m.group(1) + (m.group(2) or "")) if m else n[:60]
+        agg[key][0] += 1
+        agg[key][1] += e["dur"]
+    busy = sum(v[1] for v in agg.values())
+    span = max(e["ts"] + e["dur"] for e in k) - min(e["ts"] for e in k)
+    print(json.dumps({"profile": name, "world": W, "rank": r, "span_ms": round(span / 1e3, 2),
+                      "kernel_ms": round(busy / 1e3, 2), "launches": len(k),
+                      "kernels": {n: [c, round(us / 1e3, 2)] for n, (c, us) in
+                                  sorted(agg.items(), key=lambda x: -x[1][1])[:14]}}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", nargs="+", default=["c2", "c4"])
+    ap.add_argument("--worlds", nargs="+", type=int, default=[1, 2, 4, 8])
+    ap.add_argument("--ranks", nargs="+", type=int, default=[0])
+    ap.add_argument("--rollouts", type=int, default=2)
+    ap.add_argument("--profile", action="store_true",
+                    help="also print per-kernel GPU time of one rollout (torch.profiler / CUPTI)")
+    args = ap.parse_args()
+    import torch.distributed as dist
+
+    import bench
+    from paper_2511_20714_b200 import engine as E
+    from paper_2511_20714_b200.parallel import LoopbackComm, UlyssesEngine
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29541")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    for name in args.configs:
+        c = bench.CONFIGS[name]
+        mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
+                           block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
+                           weight_seed=0)
+        model = E.ToyModel(mc, weights=c["weights"])
+        nb = c["blocks"]
+        kvc = E.default_kv_config(mc, capacity_pages_device=10**8, capacity_pages_host=4096)
+        req = E.GenerationRequest(nb, E.DenoiseSchedule(bench.STEPS), seed=0)
+        noise = [torch.from_numpy(E._init_noise(mc, 0, ch)).cuda() for ch in range(nb)]
+        flops = bench.attn_flops_per_rollout(c)
+        base = None
+        for W in args.worlds:
+            if mc.block_len % W:
+                continue
+            for r in args.ranks:
+                if r >= W:
+                    continue
+                eng = UlyssesEngine(model, LoopbackComm(W, r), kvc, p2p=True)
+                roll = lambda: eng.generate(req, noise_provider=lambda ch: noise[ch], gather=False)  # noqa: E731
+                for _ in range(2):
+                    roll()
+                torch.cuda.synchronize()
+                eng.runner.attn_events = []
+                roll()
+                torch.cuda.synchronize()
+                attn_ms = sum(a.elapsed_time(b) for a, b in eng.runner.attn_events)
+                eng.runner.attn_events = None
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(args.rollouts):
+                    roll()
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / args.rollouts
+                value = nb * bench.FRAMES_PER_BLOCK / (ms / 1e3)
+                if W == 1 and r == 0:
+                    base = value
+                plan = eng.runner.plan
+                print(json.dumps({
+                    "config": name, "world": W, "rank": r, "ms_rank": round(ms, 2),
+                    "value_if_all_ranks_equal": round(value, 3),
+                    "strong_scaling_bound": round(value / (W * base), 3) if base else None,
+                    "k1_ms": round(attn_ms, 2), "k1_share": round(attn_ms / ms, 3),
+                    "k1_tflops_rank": round(flops / W / (attn_ms / 1e3) / 1e12, 1),
+                    "head_split": "whole heads" if plan is None else
+                    f"balanced: {plan.hl} heads / {len(plan.segs)} segments"}), flush=True)
+                if args.profile:
+                    _profile(roll, name, W, r)
+                eng.runner.release_graphs()
+                del eng
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()
+        del model
+        torch.cuda.empty_cache()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
