@@ -13,6 +13,7 @@
 #include <cstdint>
 
 #include "attn_kernel.h"
+#include "launch.cuh"
 
 namespace ifx {
 namespace {
@@ -36,6 +37,7 @@ __device__ __forceinline__ void bf16x8(const uint4& u, float (&f)[8]) {
 // through L1) are 8-way broadcasts.
 template <int HD, int kMaxKeys>
 __global__ void __launch_bounds__(256) attn_few_keys_kernel(FewKeysArgs a) {
+  pdl_wait();
   constexpr int DPT = HD / 4;      // dims per thread
   constexpr int VPT = DPT / 8;     // 16-byte vectors per thread
   const int nk = a.n_ctx + a.n_cur;
@@ -117,7 +119,7 @@ int attn_few_keys_max() { return kMaxKeysAll; }
 
 template <int HD, int MAXK>
 static int launch_fk(const FewKeysArgs& a, size_t, int blocks, cudaStream_t st) {
-  attn_few_keys_kernel<HD, MAXK><<<blocks, 256, 0, st>>>(a);
+  launch_pdl(attn_few_keys_kernel<HD, MAXK>, dim3(blocks), dim3(256), 0, st, 1, a);
   return (int)cudaGetLastError();
 }
 

@@ -40,6 +40,7 @@
 
 #include "attn_kernel.h"
 #include "device_state.h"
+#include "launch.cuh"
 #include "sm100_ptx.cuh"
 
 namespace ifx {
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // setup above overlapped the previous kernel (launch.cuh)
 
   if (warp == 0 && !PAGED) {
     // ===================== TMA producer (contiguous context) =====================
@@ -647,6 +649,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (a.o_peer_rows > 0 || a.row_max != nullptr) __threadfence_system();
   }
 
+  pdl_trigger();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -659,6 +662,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // out = sum_s w_s O_s / sum_s w_s with w_s = l_s * 2^(m_s - max_s m_s).
 template <int HD>
 __global__ void attn_combine_kernel(const AttnKernelArgs a) {
+  pdl_wait();
   constexpr int PER = HD / 32;
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -716,13 +720,11 @@ int launch(const AttnKernelArgs& a, int n_q, int heads, cudaStream_t st) {
   }();
   const int64_t items = (int64_t)((n_q + BM - 1) / BM) * heads * a.n_splits;
   const int grid = (int)(per_item || items < n_sm ? items : n_sm);
-  fn<<<grid, NTHREADS, L::SMEM, st>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(fn, dim3(grid), dim3(NTHREADS), L::SMEM, st, 1, a);
   if (e != cudaSuccess || a.n_splits == 1) return (int)e;
   const int64_t warps = (int64_t)n_q * heads;
   const int blocks = (int)((warps + 7) / 8 < n_sm * 16 ? (warps + 7) / 8 : n_sm * 16);
-  attn_combine_kernel<HD><<<blocks, 256, 0, st>>>(a);
-  return (int)cudaGetLastError();
+  return (int)launch_pdl(attn_combine_kernel<HD>, dim3(blocks), dim3(256), 0, st, 1, a);
 }
 
 }  // namespace
@@ -734,10 +736,9 @@ int attn_combine_launch(const AttnKernelArgs& a, int head_dim, cudaStream_t st) 
   const int n_sm = device_sms(current_device());
   const int blocks = (int)((warps + 7) / 8 < n_sm * 16 ? (warps + 7) / 8 : n_sm * 16);
   if (blocks == 0) return 0;
-  if (head_dim == 128) attn_combine_kernel<128><<<blocks, 256, 0, st>>>(a);
-  else if (head_dim == 64) attn_combine_kernel<64><<<blocks, 256, 0, st>>>(a);
-  else return -1;
-  return (int)cudaGetLastError();
+  if (head_dim == 128) return (int)launch_pdl(attn_combine_kernel<128>, dim3(blocks), dim3(256), 0, st, 1, a);
+  if (head_dim == 64) return (int)launch_pdl(attn_combine_kernel<64>, dim3(blocks), dim3(256), 0, st, 1, a);
+  return -1;
 }
 
 int attn_fwd_launch(const AttnKernelArgs& a, int head_dim, int n_q, int heads, cudaStream_t st) {

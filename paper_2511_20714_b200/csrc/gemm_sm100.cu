@@ -36,6 +36,7 @@
 #include <cstdlib>
 
 #include "device_state.h"
+#include "launch.cuh"
 #include "gemm_kernel.h"
 #include "sm100_ptx.cuh"
 
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
   if (CL > 1) cluster_sync_all();  // the peer's barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // setup above overlapped the previous kernel (launch.cuh)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
@@ -501,6 +503,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
     if (a.scat != nullptr) __threadfence_system();  // peer stores out before the barrier
   }
 
+  pdl_trigger();
   tc_fence_before();
   __syncthreads();
   if (CL > 1) cluster_sync_all();  // no multicast or remote arrive still targets this CTA
@@ -526,22 +529,9 @@ int launch(const GemmArgs& a, cudaStream_t st) {
   const int per = n_sm / CL;
   const int grid = (units < per ? units : per) * CL;
   if (CL == 1) {
-    gemm_kernel<BN, 1, false><<<grid, NTHREADS, L::SMEM, st>>>(a);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(gemm_kernel<BN, 1, false>, dim3(grid), dim3(NTHREADS), L::SMEM, st, 1, a);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NTHREADS);
-  cfg.dynamicSmemBytes = L::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CL, PAIR>, a);
+  return (int)launch_pdl(gemm_kernel<BN, CL, PAIR>, dim3(grid), dim3(NTHREADS), L::SMEM, st, CL, a);
 }
 
 }  // namespace

@@ -9,6 +9,7 @@
 
 #include "device_state.h"
 #include "kv_kernels.h"
+#include "launch.cuh"
 
 namespace ifx {
 namespace {
@@ -73,6 +74,7 @@ __device__ __forceinline__ uint8_t* pool_row(const PoolPtrs& p, bool is_v, int32
 __global__ void append_same(const uint8_t* __restrict__ ks, const uint8_t* __restrict__ vs,
                             int64_t src_ld_b, PoolPtrs pool, const int32_t* __restrict__ slots,
                             int64_t rel0, int64_t t, int64_t row_vecs) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * t;
@@ -89,6 +91,7 @@ __global__ void append_same(const uint8_t* __restrict__ ks, const uint8_t* __res
 __global__ void append_f32_bf16(const float* __restrict__ ks, const float* __restrict__ vs,
                                 int64_t src_ld, PoolPtrs pool, const int32_t* __restrict__ slots,
                                 int64_t rel0, int64_t t, int64_t row_vecs) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * t;
@@ -128,6 +131,7 @@ __global__ void __launch_bounds__(256) append_bulk(const uint8_t* __restrict__ k
                                                    int64_t src_ld_b, PoolPtrs pool,
                                                    const int32_t* __restrict__ slots, int64_t rel0,
                                                    int64_t t, int row_b) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t bulk_smem[];
   __shared__ __align__(8) uint64_t bars[8][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,6 +196,7 @@ __global__ void __launch_bounds__(256) append_bulk(const uint8_t* __restrict__ k
 __global__ void gather_rows(PoolPtrs pool, const int32_t* __restrict__ slots,
                             const int64_t* __restrict__ tokens, int64_t rel0, int64_t n,
                             int64_t row_vecs, uint8_t* __restrict__ ko, uint8_t* __restrict__ vo) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < 2 * n;
@@ -211,6 +216,7 @@ __global__ void gather_rows(PoolPtrs pool, const int32_t* __restrict__ slots,
 // (move, K|V, 4 KB piece) so a batch of large pages spreads over every SM.
 __global__ void move_pages(PoolPtrs pool, const int64_t* __restrict__ moves, int64_t n, int dir,
                            int64_t page_vecs, int64_t piece_vecs) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t pieces = (page_vecs + piece_vecs - 1) / piece_vecs;
   const int64_t units = n * 2 * pieces;
@@ -238,6 +244,7 @@ __global__ void move_pages(PoolPtrs pool, const int64_t* __restrict__ moves, int
 __global__ void rms_bf16_kernel(const float* __restrict__ x, int64_t rows, int64_t width,
                                 const float* __restrict__ tvec, float t, float* __restrict__ x_out,
                                 __nv_bfloat16* __restrict__ y) {
+  pdl_wait();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
@@ -278,6 +285,7 @@ template <int kRmsThreads, int VPT>
 __global__ void __launch_bounds__(kRmsThreads) rms_row_kernel(
     const float* __restrict__ x, int64_t rows, int width, const float* __restrict__ tvec, float t,
     float* __restrict__ x_out, __nv_bfloat16* __restrict__ y) {
+  pdl_wait();
   __shared__ float part[kRmsThreads / 32];
   const int tid = threadIdx.x;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -325,6 +333,7 @@ __global__ void __launch_bounds__(kRmsThreads) rms_row_kernel(
 __global__ void ulysses_transpose(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                   int64_t n, int64_t groups, int64_t world, int64_t chunk_vecs,
                                   int64_t ld_b, bool pack) {
+  pdl_wait();
   const int64_t total = n * groups * world * chunk_vecs;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -349,6 +358,7 @@ __global__ void rope_qk_kernel(__nv_bfloat16* __restrict__ qkv, int64_t rows, in
                                int heads, int64_t head_stride, int pairs, int64_t q_col0,
                                int64_t k_col0, const float* __restrict__ cos_t,
                                const float* __restrict__ sin_t, int64_t tab_row0) {
+  pdl_wait();
   const int64_t total = rows * heads * pairs;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -374,6 +384,7 @@ __global__ void rope_qk_kernel(__nv_bfloat16* __restrict__ qkv, int64_t rows, in
 // rows, row bytes) in bytes, row bytes a multiple of 16. grid.x = block, grid.y = row chunk.
 __global__ void copy_blocks_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                    const int64_t* __restrict__ desc, int rows_per_cta) {
+  pdl_wait();
   const int64_t* d = desc + 6 * blockIdx.x;
   const int64_t rows = d[4];
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta;
@@ -395,6 +406,7 @@ __global__ void group_softmax_kernel(const float* __restrict__ s, int64_t rows, 
                                      __nv_bfloat16* __restrict__ p, int64_t p_ld,
                                      const float* __restrict__ rs_part, int rs_parts,
                                      int64_t rs_ld, float rs_inv_d, float rs_eps) {
+  pdl_wait();
   const int64_t total = rows * groups;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -439,7 +451,7 @@ int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf1
   const int threads = 256;
   const PoolPtrs pool = pool_ptrs(dk, dv, hk, hv, width, pool_bf16 ? 2 : 4, page_len);
   if (!src_bf16 && pool_bf16) {
-    append_f32_bf16<<<grid_for(2 * t * 32, threads), threads, 0, st>>>(
+    launch_pdl(append_f32_bf16, dim3(grid_for(2 * t * 32, threads)), dim3(threads), 0, st, 1,
         static_cast<const float*>(ks), static_cast<const float*>(vs), src_ld, pool, slots, rel0, t,
         width / 8);
   } else if ((width * (pool_bf16 ? 2 : 4)) <= kBulkMaxRowBytes && !std::getenv("IFX_K2_SIMT")) {
@@ -455,13 +467,13 @@ int kv_append_launch(const void* ks, const void* vs, int64_t src_ld, int src_bf1
     int blocks = (int)((2 * t + 7) / 8);
     const int cap = kSMs_now() * (row_b <= 4096 ? 4 : 1);
     if (blocks > cap) blocks = cap;
-    append_bulk<<<blocks, threads, smem, st>>>(static_cast<const uint8_t*>(ks),
+    launch_pdl(append_bulk, dim3(blocks), dim3(threads), smem, st, 1, static_cast<const uint8_t*>(ks),
                                                static_cast<const uint8_t*>(vs),
                                                src_ld * (pool_bf16 ? 2 : 4), pool, slots, rel0, t,
                                                row_b);
   } else {
     const int esz = pool_bf16 ? 2 : 4;
-    append_same<<<grid_for(2 * t * 32, threads), threads, 0, st>>>(
+    launch_pdl(append_same, dim3(grid_for(2 * t * 32, threads)), dim3(threads), 0, st, 1,
         static_cast<const uint8_t*>(ks), static_cast<const uint8_t*>(vs), src_ld * esz, pool, slots,
         rel0, t, width * esz / 16);
   }
@@ -495,7 +507,7 @@ int copy_blocks_launch(const void* src, void* dst, const int64_t* desc, int64_t 
                        int64_t max_rows, cudaStream_t st) {
   const int rows_per_cta = 64;
   dim3 grid((unsigned)n_blocks, (unsigned)((max_rows + rows_per_cta - 1) / rows_per_cta));
-  copy_blocks_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(src),
+  launch_pdl(copy_blocks_kernel, dim3(grid), dim3(256), 0, st, 1, static_cast<const uint8_t*>(src),
                                            static_cast<uint8_t*>(dst), desc, rows_per_cta);
   return (int)cudaGetLastError();
 }
@@ -505,7 +517,7 @@ int group_softmax_launch(const float* s, int64_t rows, int groups, int gs, int64
                          int rs_parts, int64_t rs_ld, float rs_inv_d, float rs_eps,
                          cudaStream_t st) {
   const int threads = 256;
-  group_softmax_kernel<<<grid_for(rows * groups, threads), threads, 0, st>>>(
+  launch_pdl(group_softmax_kernel, dim3(grid_for(rows * groups, threads)), dim3(threads), 0, st, 1,
       s, rows, groups, gs, ld, scale_log2, static_cast<__nv_bfloat16*>(p), p_ld, rs_part,
       rs_parts, rs_ld, rs_inv_d, rs_eps);
   return (int)cudaGetLastError();
@@ -518,19 +530,19 @@ int rms_launch(const float* x, int64_t rows, int64_t width, const float* tvec, f
   const int gr = (int)(rows < (int64_t)kSMs_now() * 64 ? rows : (int64_t)kSMs_now() * 64);
   if (v128 <= 24 && gr > 0) {  // wider rows: the warp-per-row kernel (two passes)
     if (v128 <= 3)
-      rms_row_kernel<128, 3><<<gr, 128, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
+      launch_pdl(rms_row_kernel<128, 3>, dim3(gr), dim3(128), 0, st, 1, x, rows, (int)width, tvec, t, x_out, yb);
     else if (v128 <= 6)
-      rms_row_kernel<128, 6><<<gr, 128, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
+      launch_pdl(rms_row_kernel<128, 6>, dim3(gr), dim3(128), 0, st, 1, x, rows, (int)width, tvec, t, x_out, yb);
     else if (v128 <= 12)  // e.g. 5,120 (Wan-14B): 256 threads x 5 vectors
-      rms_row_kernel<256, 6><<<gr, 256, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
+      launch_pdl(rms_row_kernel<256, 6>, dim3(gr), dim3(256), 0, st, 1, x, rows, (int)width, tvec, t, x_out, yb);
     else
-      rms_row_kernel<512, 6><<<gr, 512, 0, st>>>(x, rows, (int)width, tvec, t, x_out, yb);
+      launch_pdl(rms_row_kernel<512, 6>, dim3(gr), dim3(512), 0, st, 1, x, rows, (int)width, tvec, t, x_out, yb);
     return (int)cudaGetLastError();
   }
   const int threads = 256;
   const int64_t blocks = (rows + 7) / 8;
   const int g = (int)(blocks < (int64_t)kSMs_now() * 16 ? blocks : (int64_t)kSMs_now() * 16);
-  rms_bf16_kernel<<<g, threads, 0, st>>>(x, rows, width, tvec, t, x_out, yb);
+  launch_pdl(rms_bf16_kernel, dim3(g), dim3(threads), 0, st, 1, x, rows, width, tvec, t, x_out, yb);
   return (int)cudaGetLastError();
 }
 
@@ -538,7 +550,7 @@ int rope_launch(void* qkv, int64_t rows, int64_t ld, int heads, int64_t head_str
                 int64_t q_col0, int64_t k_col0, const float* cos_t, const float* sin_t,
                 int64_t tab_row0, cudaStream_t st) {
   const int threads = 256;
-  rope_qk_kernel<<<grid_for(rows * heads * pairs, threads), threads, 0, st>>>(
+  launch_pdl(rope_qk_kernel, dim3(grid_for(rows * heads * pairs, threads)), dim3(threads), 0, st, 1,
       static_cast<__nv_bfloat16*>(qkv), rows, ld, heads, head_stride, pairs, q_col0, k_col0, cos_t,
       sin_t, tab_row0);
   return (int)cudaGetLastError();
@@ -548,7 +560,7 @@ int ulysses_launch(const void* src, void* dst, int64_t n, int64_t groups, int64_
                    int64_t chunk_bytes, int64_t ld_bytes, bool pack, cudaStream_t st) {
   const int threads = 256;
   const int64_t cv = chunk_bytes / 16;
-  ulysses_transpose<<<grid_for(n * groups * world * cv, threads), threads, 0, st>>>(
+  launch_pdl(ulysses_transpose, dim3(grid_for(n * groups * world * cv, threads)), dim3(threads), 0, st, 1,
       static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), n, groups, world, cv, ld_bytes,
       pack);
   return (int)cudaGetLastError();

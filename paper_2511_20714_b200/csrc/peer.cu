@@ -20,6 +20,7 @@
 
 #include "../../include/ifx_abi.h"
 #include "common_host.h"
+#include "launch.cuh"
 
 namespace ifx {
 namespace {
@@ -44,6 +45,7 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 
 __global__ void peer_barrier_kernel(const BarrierArgs a) {
+  pdl_wait();
   __shared__ uint32_t epoch;
   if (threadIdx.x == 0) {
     epoch = *a.counter + 1u;
@@ -126,7 +128,7 @@ int ifx_peer_barrier(void* const* pads, int world, int rank, uint32_t* counter, 
   a.world = world;
   a.rank = rank;
   a.timeout_cycles = (long long)timeout_ms * 2000000LL;  // ~2 GHz SM clock, upper bound
-  ifx::peer_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  ifx::launch_pdl(ifx::peer_barrier_kernel, dim3(1), dim3(32), 0, static_cast<cudaStream_t>(stream), 1, a);
   return ifx::cuda_status(cudaGetLastError(), "peer_barrier launch");
 }
 

@@ -48,8 +48,13 @@ def _profile(roll, name, W, r):
         agg[key][1] += e["dur"]
     busy = sum(v[1] for v in agg.values())
     span = max(e["ts"] + e["dur"] for e in k) - min(e["ts"] for e in k)
+    ks = sorted(k, key=lambda e: e["ts"])
+    gaps = [b["ts"] - (a["ts"] + a["dur"]) for a, b in zip(ks, ks[1:])]
+    hist = {lab: round(sum(g for g in gaps if lo <= g < hi) / 1e3, 2) for lab, lo, hi in
+            (("<2us", -1e9, 2), ("2-5us", 2, 5), ("5-20us", 5, 20), ("20-200us", 20, 200),
+             (">200us", 200, 1e12))}
     print(json.dumps({"profile": name, "world": W, "rank": r, "span_ms": round(span / 1e3, 2),
-                      "kernel_ms": round(busy / 1e3, 2), "launches": len(k),
+                      "kernel_ms": round(busy / 1e3, 2), "launches": len(k), "gap_ms_by_size": hist,
                       "kernels": {n: [c, round(us / 1e3, 2)] for n, (c, us) in
                                   sorted(agg.items(), key=lambda x: -x[1][1])[:14]}}), flush=True)
 
