@@ -53,6 +53,11 @@ def _profile(roll, name, W, r):
     hist = {lab: round(sum(g for g in gaps if lo <= g < hi) / 1e3, 2) for lab, lo, hi in
             (("<2us", -1e9, 2), ("2-5us", 2, 5), ("5-20us", 5, 20), ("20-200us", 20, 200),
              (">200us", 200, 1e12))}
+    big = sorted(range(len(gaps)), key=lambda i: -gaps[i])[:12]
+    t0 = ks[0]["ts"]
+    top = [(round(gaps[i], 1), round((ks[i]["ts"] - t0) / 1e3, 2), ks[i]["name"][:40], ks[i + 1]["name"][:40])
+           for i in sorted(big)]
+    print(json.dumps({"top_gaps_us_at_ms_after_before": top}), flush=True)
     print(json.dumps({"profile": name, "world": W, "rank": r, "span_ms": round(span / 1e3, 2),
                       "kernel_ms": round(busy / 1e3, 2), "launches": len(k), "gap_ms_by_size": hist,
                       "kernels": {n: [c, round(us / 1e3, 2)] for n, (c, us) in
