@@ -486,6 +486,16 @@ def run_host_tier_bench(args, c, cfgname, local):
     return 0
 
 
+def head_split(runner) -> str:
+    """How a Ulysses rank's attention is split (parallel.py plans)."""
+    if runner.grouped is not None:
+        g = runner.grouped
+        return f"grouped: {g.G} head groups x {g.R} row slices ({g.hl} heads, {g.rows} query rows per rank)"
+    if runner.plan is not None:
+        return f"balanced: {runner.plan.hl} heads / {len(runner.plan.segs)} segments on rank 0"
+    return "whole heads"
+
+
 def run_ulysses_bench(args, c, cfgname, world, rank, local):
     """bench.py for N > 1: one rollout strong-scaled over N GPUs with Ulysses."""
     import torch
@@ -572,9 +582,7 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
                          if c["weights"] == "reference" else "synthetic (reference-seeded noise, "
                          "torch-seeded random-init weights)"),
                 "config": {"workload": c["desc"], "parallelism": f"ulysses{world}",
-                           "head_split": "whole heads" if eng.runner.plan is None else
-                           f"balanced: {eng.runner.plan.hl} heads / {len(eng.runner.plan.segs)} "
-                           f"segments on rank 0", "exchange": exchange,
+                           "head_split": head_split(eng.runner), "exchange": exchange,
                            "l2": "inputs larger than L2"},
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak if achieved else None, "traffic": traffic,

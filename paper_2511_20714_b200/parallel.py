@@ -498,7 +498,8 @@ class PeerMesh:
 
     def __init__(self, comm, nbytes: int, timeout_ms: int | None = None):
         if getattr(comm, "loopback", False):
-            return self._init_loopback(comm, nbytes, timeout_ms)
+            self._init_loopback(comm, nbytes, timeout_ms)
+            return
         import ctypes
         import os
 
@@ -619,6 +620,32 @@ class LoopbackComm:
         self.messages = self.bytes = 0
 
 
+def grouped_split(heads: int, world: int):
+    """(G, R) for heads that do not divide the ranks: G head groups x R row slices with
+    G * R = W, heads % G == 0, R <= 2 (largest G); None if there is none (balanced plan)."""
+    if heads % world == 0:
+        return None
+    for g in range(world, 0, -1):
+        if world % g == 0 and heads % g == 0 and world // g <= 2 and g < world:
+            return g, world // g
+    return None
+
+
+class GroupedPlan:
+    """Ulysses x sequence split for heads that do not divide the ranks (peer exchange only):
+    rank k = g*R + r attends head group g (H/G whole heads) for query rows [r*T/R,
+    (r+1)*T/R) against the full sequence's K/V of its heads (the whole block's K/V reaches
+    the R ranks of its group). Same query-row work as the balanced plan, but ONE K1 launch
+    over whole heads per layer-pass (e.g. 12 heads on 8 ranks: 3 heads x half the rows)."""
+
+    def __init__(self, heads: int, T: int, world: int, rank: int, G: int, R: int):
+        self.G, self.R, self.T = G, R, T
+        self.g, self.r = divmod(rank, R)
+        self.hl = heads // G
+        self.rows = T // R
+        self.row0 = self.r * self.rows
+
+
 class P2PExchange:
     """The Ulysses re-shard (parallel.py:150-169) without an all-to-all: G1's QKV epilogue
     stores each head's Q/K/V column block of this rank's n sequence rows straight into the
@@ -637,22 +664,33 @@ class P2PExchange:
         W, r, n, T = comm.world, comm.rank, runner.n, m.config.block_len
         H, dhp, Dp = m.heads_pad, m.dh_pad, m.attn_width
         balanced = runner.plan is not None
-        r_bytes = self.region_bytes(H, T, W, dhp, balanced)
+        grouped = (runner.grouped.G, runner.grouped.R) if runner.grouped is not None else None
+        r_bytes = self.region_bytes(H, T, W, dhp, balanced, grouped)
         self.s_off = max(r_bytes) // 256 * 256 + 256
         self.mesh = PeerMesh(comm, self.s_off + n * Dp * 2)
-        table, self.o_peers = self.layout(H, T, W, r, dhp, balanced, self.mesh.addr, self.s_off)
+        table, self.o_peers = self.layout(H, T, W, r, dhp, balanced, self.mesh.addr, self.s_off,
+                                          grouped)
         self.table = torch.from_numpy(table.reshape(3 * H, 8)).to(runner.x.device)
         if balanced:
             self.r_view = self.mesh.local(0, r_bytes[r] // 2, 1).view(-1)
+        elif grouped is not None:
+            gp = runner.grouped
+            wl = gp.hl * dhp
+            self.q_view = self.mesh.local(0, gp.rows, wl)
+            self.k_view = self.mesh.local(gp.rows * wl * 2, T, wl)
+            self.v_view = self.mesh.local((gp.rows + T) * wl * 2, T, wl)
         else:
             self.r_view = self.mesh.local(0, T, 3 * (H // W) * dhp)
         self.s_view = self.mesh.local(self.s_off, n, Dp)
         self.n = n
 
     @classmethod
-    def region_bytes(cls, H, T, W, dhp, balanced):
+    def region_bytes(cls, H, T, W, dhp, balanced, grouped=None):
         """Bytes of each rank's receive region R (whole-head: [T, 3*wl]; balanced: the Q
-        segments stacked, then K and V [T, hl*dhp])."""
+        segments stacked, then K and V [T, hl*dhp]; grouped: Q [T/R, wl], K, V [T, wl])."""
+        if grouped is not None:
+            G, R = grouped
+            return [(T // R + 2 * T) * (H // G) * dhp * 2] * W
         if not balanced:
             return [T * 3 * (H // W) * dhp * 2] * W
         segs, heads = cls._segments(H, T, W)
@@ -660,7 +698,7 @@ class P2PExchange:
                 for k in range(W)]
 
     @classmethod
-    def layout(cls, H, T, W, r, dhp, balanced, addr, s_off):
+    def layout(cls, H, T, W, r, dhp, balanced, addr, s_off, grouped=None):
         """Rank r's G1 scatter table [3H blocks, 2 entries, (address, row stride, row_lo,
         row_hi)] over the Q|K|V column blocks of its n rows, and K1's per-peer O addresses.
         addr(peer, byte offset) -> address of that byte of the peer's data region."""
@@ -674,6 +712,21 @@ class P2PExchange:
                 raise ConfigError("a head reaches more than two ranks")
             table[blk, e] = (a, ld, lo, hi)
             fill[blk] += 1
+        if grouped is not None:
+            G, R = grouped
+            hl, rows = H // G, T // R
+            wl = hl * dhp
+            rs = (r * n) // rows  # the row slice this rank's sequence rows fall in
+            for h in range(H):
+                g, j = divmod(h, hl)
+                # Q rows -> the group's rank for this row slice, at row r*n - rs*rows + rr
+                put(h, addr(g * R + rs, ((r * n - rs * rows) * wl + j * dhp) * 2), wl * 2, 0, n)
+                for r2 in range(R):  # K / V rows -> every row slice of the group
+                    put(H + h, addr(g * R + r2, ((rows + r * n) * wl + j * dhp) * 2), wl * 2, 0, n)
+                    put(2 * H + h, addr(g * R + r2, ((rows + T + r * n) * wl + j * dhp) * 2),
+                        wl * 2, 0, n)
+            g = r // R
+            return table, [addr(p, s_off + g * hl * dhp * 2) for p in range(W)]
         if not balanced:
             hl = H // W
             wl = hl * dhp
@@ -742,7 +795,12 @@ class UlyssesRunner:
         # heads divisible by the ranks: classic Ulysses (whole heads per rank, K5 pack);
         # otherwise the balanced plan (query rows of a head split across ranks)
         self.plan = None
-        if model.heads_pad % W:
+        self.grouped = None
+        gs = grouped_split(model.heads_pad, W) if (model.heads_pad % W and p2p) else None
+        if gs is not None:  # peer exchange: whole head groups x row slices, one K1 launch
+            self.grouped = GroupedPlan(model.heads_pad, c.block_len, W, comm.rank, *gs)
+            self.hl = self.grouped.hl
+        elif model.heads_pad % W:
             self.plan = BalancedPlan(model.heads_pad, c.block_len, W, comm.rank, model.dh_pad, dev)
             self.hl = self.plan.hl
         else:
@@ -828,7 +886,11 @@ class UlyssesRunner:
         if ev is not None:
             e0 = timing_event()
             e0.record()
-        if self.plan is None:
+        if self.grouped is not None:  # whole heads, this rank's row slice of the queries
+            kc, vc = x.k_view, x.v_view
+            ctx.attend(li, x.q_view, self.hl, dhp, x.s_view, kc, vc, sc,
+                       attn=x.attn(row0=self.grouped.row0))
+        elif self.plan is None:
             R = x.r_view
             q, kc, vc = R[:, :wl], R[:, wl:2 * wl], R[:, 2 * wl:]
             ctx.attend(li, q, self.hl, dhp, x.s_view, kc, vc, sc, attn=x.attn())

@@ -92,6 +92,43 @@ def test_p2p_layout_equals_all_to_all(heads, world, T, dhp, balanced):
         assert np.array_equal(S, qkv[r * n:(r + 1) * n, :Dp])
 
 
+@pytest.mark.parametrize("heads,world,T,dhp", [(12, 8, 64, 8), (6, 4, 32, 16), (3, 2, 16, 8),
+                                                (10, 4, 16, 8)])
+def test_p2p_grouped_layout(heads, world, T, dhp):
+    """Grouped plan (G head groups x R row slices): rank g*R + r receives Q rows of slice r
+    for its H/G heads and the whole sequence's K/V of those heads; one K1 over the slice's
+    rows writes each output row to its sequence owner."""
+    from paper_2511_20714_b200.parallel import GroupedPlan, grouped_split
+    gs = grouped_split(heads, world)
+    assert gs is not None
+    G, R = gs
+    rng = np.random.default_rng(heads + world)
+    Dp, n = heads * dhp, T // world
+    qkv = rng.integers(0, 2**15, size=(T, 3 * Dp), dtype=np.uint16)
+    rb = P2PExchange.region_bytes(heads, T, world, dhp, False, gs)
+    s_off = max(rb) // 256 * 256 + 256
+    arenas = [np.zeros(s_off + n * Dp * 2, np.uint8) for _ in range(world)]
+    layouts = [P2PExchange.layout(heads, T, world, r, dhp, False, _addr, s_off, gs)
+               for r in range(world)]
+    for r in range(world):
+        _scatter_rows(arenas, layouts[r][0], np.ascontiguousarray(qkv[r * n:(r + 1) * n]), dhp)
+    for k in range(world):
+        gp = GroupedPlan(heads, T, world, k, G, R)
+        wl = gp.hl * dhp
+        reg = arenas[k][:rb[k]].view(np.uint16)
+        q = reg[:gp.rows * wl].reshape(gp.rows, wl)
+        kk = reg[gp.rows * wl:(gp.rows + T) * wl].reshape(T, wl)
+        vv = reg[(gp.rows + T) * wl:(gp.rows + 2 * T) * wl].reshape(T, wl)
+        cols = slice(gp.g * wl, (gp.g + 1) * wl)
+        assert np.array_equal(q, qkv[gp.row0:gp.row0 + gp.rows, cols])
+        assert np.array_equal(kk, qkv[:, Dp:2 * Dp][:, cols])
+        assert np.array_equal(vv, qkv[:, 2 * Dp:][:, cols])
+        _o_scatter(arenas, layouts[k][1], gp.rows, np.ascontiguousarray(q), n, Dp, row0=gp.row0)
+    for r in range(world):
+        S = arenas[r][s_off:].view(np.uint16).reshape(n, Dp)
+        assert np.array_equal(S, qkv[r * n:(r + 1) * n, :Dp])
+
+
 def test_p2p_layout_rejects_three_way_heads():
     # 1 head on 4 ranks: its K/V would reach all 4 (two scatter entries per block)
     from paper_2511_20714_b200.errors import ConfigError

@@ -122,15 +122,13 @@ def main():
                 value = nb * bench.FRAMES_PER_BLOCK / (ms / 1e3)
                 if W == 1 and r == 0:
                     base = value
-                plan = eng.runner.plan
                 print(json.dumps({
                     "config": name, "world": W, "rank": r, "ms_rank": round(ms, 2),
                     "value_if_all_ranks_equal": round(value, 3),
                     "strong_scaling_bound": round(value / (W * base), 3) if base else None,
                     "k1_ms": round(attn_ms, 2), "k1_share": round(attn_ms / ms, 3),
                     "k1_tflops_rank": round(flops / W / (attn_ms / 1e3) / 1e12, 1),
-                    "head_split": "whole heads" if plan is None else
-                    f"balanced: {plan.hl} heads / {len(plan.segs)} segments"}), flush=True)
+                    "head_split": bench.head_split(eng.runner)}), flush=True)
                 if args.profile:
                     _profile(roll, name, W, r)
                 eng.runner.release_graphs()
