@@ -25,6 +25,7 @@ import hashlib
 import math
 import os
 import threading
+import time
 import weakref
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -672,6 +673,31 @@ def timing_event() -> torch.cuda.Event:
                             external=torch.cuda.is_current_stream_capturing())
 
 
+HOST_BOUND_CAPTURE = os.environ.get("IFX_HOST_BOUND_CAPTURE", "1") != "0"  # A/B switch
+
+
+def _timed_eager_pass(runner, latent, tv, ctx, cross, cache, eps, rope) -> None:
+    """runner.forward, eagerly, noting the host enqueue time and a GPU event pair of the pass
+    (read later by _host_bound, once the events completed)."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
+    e1.record()
+    runner._pass_probe = (e0, e1, (time.perf_counter() - t0) * 1e3)
+
+
+def _host_bound(runner) -> bool:
+    """True when the runner's last timed eager pass was enqueue-bound: its GPU span (event
+    to event) barely exceeded the host's enqueue time, i.e. the GPU waited for launches (a
+    GPU-bound pass runs far longer than it takes to enqueue)."""
+    probe = getattr(runner, "_pass_probe", None)
+    if probe is None or not HOST_BOUND_CAPTURE or not probe[1].query():
+        return False
+    e0, e1, host_ms = probe
+    return e0.elapsed_time(e1) < 1.25 * host_ms
+
+
 def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, eps, rope,
                  graphs_ok: bool = True, first_block: bool = False) -> None:
     """The S denoise passes of a block (engine.py:299-301). Within a block every pass
@@ -696,23 +722,29 @@ def _euler_steps(runner, latent, schedule: DenoiseSchedule, ctx, cross, cache, e
     if len(steps) > 1 and not runner._warm:
         # the runner's first pass runs eagerly: library state (cuBLASLt handle, workspace,
         # per-shape algorithm choice in ifx_gemm_bf16) is set up outside any capture
-        torch.mul(m.time_vec, steps[0], out=tv)
+        torch.mul(m.time_vec, steps[0], out=tv)  # (not timed: library setup skews it)
         runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
         latent.add_(eps, alpha=-float(schedule.step_scale))
         runner._warm = True
         steps = steps[1:]
-    # the first block of a run on a drained GPU runs eagerly: a capture would leave the GPU
-    # idle for its whole duration (in steady state it overlaps the previous block's clean
-    # pass; a host-bound Ulysses rank keeps capturing every later block)
-    eager_block = first_block and (runner._tail is None or runner._tail.query())
+    # the first block of a run on a drained GPU runs eagerly when the GPU is the bottleneck:
+    # a capture would leave it idle for the capture's duration (in steady state a capture
+    # overlaps the previous block's clean pass). A host-bound runner (a pass enqueues slower
+    # than the GPU runs it, e.g. a Ulysses rank at 8 GPUs) captures this block too: eager
+    # passes would idle the GPU for longer than one capture.
+    eager_block = (first_block and (runner._tail is None or runner._tail.query())
+                   and not _host_bound(runner))
     use = (GRAPHS and graphs_ok and len(steps) > 1 and not eager_block and _mha_hook() is None
            and (ctx is None or (ctx.paged and not ctx.jobs)))
     if use and isinstance(cross, _LazyFold):
         cross.materialize()  # fold ops (and their allocations) must not enter the graph
     if not use:
-        for t in steps:
+        for i, t in enumerate(steps):
             torch.mul(m.time_vec, t, out=tv)
-            runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
+            if i == 0 and runner.attn_events is None:
+                _timed_eager_pass(runner, latent, tv, ctx, cross, cache, eps, rope)
+            else:
+                runner.forward(latent, tv, ctx, cross, cache, eps_out=eps, rope=rope)
             latent.add_(eps, alpha=-float(schedule.step_scale))
         return
     ev = runner.attn_events
