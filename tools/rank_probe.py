@@ -64,6 +64,69 @@ def _profile(roll, name, W, r):
                                   sorted(agg.items(), key=lambda x: -x[1][1])[:14]}}), flush=True)
 
 
+def _c5_rank(name, c, W, r, steps):
+    """c5 (minute-long 14B rollout) as one rank of W: the rank's head shard of a cache with
+    `prefill` cached blocks (synthetic K/V through the cache API, the reference's per-block
+    fetch bookkeeping), all of it HBM-resident, then `steps` generated blocks timed."""
+    import bench
+    from paper_2511_20714_b200 import engine as E
+    from paper_2511_20714_b200.kvcache import CROSS_ATTN, SELF_ATTN, KvCache
+    from paper_2511_20714_b200.parallel import LoopbackComm, UlyssesEngine
+    mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
+                       block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
+                       weight_seed=0)
+    model = E.ToyModel(mc, weights=c["weights"])
+    T, L = mc.block_len, mc.layers
+    nb_pre = c["prefill"]
+    kvc = E.default_kv_config(mc, capacity_pages_device=10**8, capacity_pages_host=4096)
+    eng = UlyssesEngine(model, LoopbackComm(W, r), kvc, p2p=True)
+    rn = eng.runner
+    cache = KvCache(kvc, dtype=torch.bfloat16, reserve_tokens=T * (nb_pre + steps + 2),
+                    row_width=rn.wl, cross_row_width=model.attn_width)
+    emb = E.embed_prompt(model, "a quiet scene")
+    for li, (kc, vc) in enumerate(E._cross_kv(model, emb)):
+        cache.append_block(li, kc, vc, kind=CROSS_ATTN, chunk_index=0)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    kv = [torch.randn(T, rn.wl, device="cuda", generator=g).bfloat16() for _ in range(2)]
+    for b in range(nb_pre):
+        with cache.batch():
+            E._KvContext(model, cache, rn.stager, 1)
+            E._touch_cross(model, cache)
+        for li in range(L):
+            cache.append_block(li, kv[0], kv[1], kind=SELF_ATTN, chunk_index=b)
+    torch.cuda.synchronize()
+    sched = E.DenoiseSchedule(bench.STEPS)
+    noise = torch.randn(rn.n, mc.model_dim, device="cuda", generator=g)
+
+    def block(ch):
+        ctx, cross = E._block_context(model, cache, None, rn.stager, len(bench.STEPS) + 1)
+        rn.denoise(noise.clone(), sched, ctx, cross, cache, ch)
+
+    block(nb_pre)  # warm
+    torch.cuda.synchronize()
+    rn.attn_events = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        block(nb_pre + 1 + i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    attn_ms = sum(a.elapsed_time(b) for a, b in rn.attn_events) / steps
+    rn.attn_events = None
+    P = len(bench.STEPS) + 1
+    flops = sum(4.0 * T * (b * T + T) * mc.model_dim * L * P
+                for b in range(nb_pre + 1, nb_pre + 1 + steps)) / steps / W
+    st = cache.memory_stats()
+    print(json.dumps({"config": name, "world": W, "rank": r, "cached_blocks": nb_pre + 1,
+                      "ms_per_block_rank": round(ms, 1),
+                      "latent_frames_per_s_if_all_ranks_equal": round(3 / (ms / 1e3), 3),
+                      "k1_ms": round(attn_ms, 1), "k1_tflops_rank": round(flops / (attn_ms / 1e3) / 1e12, 1),
+                      "kv_shard_device_GB": round(st.device_pages_used * 16 * rn.wl * 2 * 2 / 1e9, 2),
+                      "host_pages": st.host_pages_used, "head_split": bench.head_split(rn)}), flush=True)
+    rn.release_graphs()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", nargs="+", default=["c2", "c4"])
@@ -86,6 +149,12 @@ def main():
     torch.backends.cuda.matmul.allow_tf32 = False
     for name in args.configs:
         c = bench.CONFIGS[name]
+        if "prefill" in c:
+            for W in args.worlds:
+                for r in args.ranks:
+                    if W >= 4 and r < W:  # a rank's shard of the 60-block cache fits HBM
+                        _c5_rank(name, c, W, r, args.rollouts)
+            continue
         mc = E.ModelConfig(layers=c["layers"], heads=c["heads"], head_dim=c["head_dim"],
                            block_len=c["block_len"], frame_shape=c["frame_shape"], prompt_dim=16,
                            weight_seed=0)
