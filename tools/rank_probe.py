@@ -179,7 +179,13 @@ def main():
                 eng.runner.attn_events = []
                 roll()
                 torch.cuda.synchronize()
-                attn_ms = sum(a.elapsed_time(b) for a, b in eng.runner.attn_events)
+                evs = eng.runner.attn_events
+                attn_ms = sum(a.elapsed_time(b) for a, b in evs)
+                per = len(evs) // nb if len(evs) % nb == 0 else 0
+                T_ = mc.block_len
+                blk_tf = [round(4.0 * T_ * (b + 1) * T_ * mc.model_dim * c["layers"] * (len(bench.STEPS) + 1) / W
+                                / (sum(x.elapsed_time(y) for x, y in evs[b * per:(b + 1) * per]) / 1e3) / 1e12, 1)
+                          for b in range(nb)] if per else None
                 eng.runner.attn_events = None
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
@@ -197,6 +203,7 @@ def main():
                     "strong_scaling_bound": round(value / (W * base), 3) if base else None,
                     "k1_ms": round(attn_ms, 2), "k1_share": round(attn_ms / ms, 3),
                     "k1_tflops_rank": round(flops / W / (attn_ms / 1e3) / 1e12, 1),
+                    "k1_tflops_by_block": blk_tf,
                     "head_split": bench.head_split(eng.runner)}), flush=True)
                 if args.profile:
                     _profile(roll, name, W, r)
