@@ -837,6 +837,12 @@ class UlyssesRunner:
             if attn is not None:
                 raise ConfigError("the peer-scatter exchange runs K1 itself (no attention hook)")
             self.xch = P2PExchange(self, comm)
+        # G1 with the norms fused into the projections' epilogues (engine _forward_g1) when
+        # it beats cuBLASLt + the RMS kernel on this rank's shapes (small row counts: wave
+        # and launch bound), chosen by timing both once (IFX_G1=all / off forces it)
+        from ._device import RowNorm
+        self.norm = RowNorm(self.h, torch.empty(n, 2 * -(-D // 64), device=dev), 0, D)
+        self.g1_all = self.xch is not None and self._choose_g1_all()
 
     def _balanced_attention(self, li, ctx, sc, ev):
         """BalancedPlan: re-shard (one all-to-all), one K1 per segment (a head's query rows,
@@ -870,7 +876,7 @@ class UlyssesRunner:
         _copy_blocks(self.b_orecv, self.attn_s, pl.ounpack)
         return kc, vc
 
-    def _p2p_attention(self, li, ctx, sc, ev, lw, rope, append=None):
+    def _p2p_attention(self, li, ctx, sc, ev, lw, rope, append=None, norm_in=None):
         """QKV projection scattered into the attending ranks (G1 epilogue, RoPE fused), a
         peer barrier, K1 with O scattered to the row owners, the clean pass's page write of
         this rank's K / V (`append(kc, vc)`: before the barrier, because once every rank
@@ -881,7 +887,7 @@ class UlyssesRunner:
         c, dhp, wl = m.config, m.dh_pad, self.wl
         rspec = None if rope is None else (rope[0], rope[1], self.comm.rank * self.n,
                                            c.head_dim // 2, dhp, m.heads_pad, 0, m.attn_width)
-        gemm_fused(self.h, lw.wqkv, None, rope=rspec, scatter=(x.table, dhp))
+        gemm_fused(self.h, lw.wqkv, None, norm_in=norm_in, rope=rspec, scatter=(x.table, dhp))
         x.mesh.barrier()
         if ev is not None:
             e0 = timing_event()
@@ -919,6 +925,46 @@ class UlyssesRunner:
         from ._device import rms_bf16
         return rms_bf16(x, out, tvec, t, x_out)
 
+    def _choose_g1_all(self) -> bool:
+        """Time this rank's wo / w1 / w2 on G1 (fused residual + norm statistics, norm as a
+        row scale) against cuBLASLt plus the RMS kernels they replace; QKV is on G1 either
+        way (scatter epilogue)."""
+        from . import engine as E
+        from ._device import gemm, gemm_fused
+        if E.G1 in ("all", "off", "qkv"):
+            return E.G1 == "all"
+        lw, norm = self.model.layers[0], self.norm
+        self.x.normal_()
+        self.h.copy_(self.x)
+        self.ffn.normal_()
+
+        def timed(fn, n=6):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(n):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / n
+
+        def lt():
+            gemm(self.attn_s, lw.wo, self.x, beta=1.0)
+            for _ in range(2):
+                self._rms(self.x, self.h)
+            gemm(self.h, lw.w1, self.ffn, relu=True)
+            gemm(self.ffn, lw.w2, self.x, beta=1.0)
+            self._rms(self.x, self.h)
+
+        def g1():
+            gemm_fused(self.attn_s, lw.wo, self.x, beta=1.0, norm_out=norm)
+            gemm_fused(self.h, lw.w1, self.ffn, relu=True, norm_in=norm)
+            gemm_fused(self.ffn, lw.w2, self.x, beta=1.0, norm_out=norm)
+
+        t_lt, t_g1 = min(timed(lt) for _ in range(2)), min(timed(g1) for _ in range(2))
+        self.g1_choice = {"cublaslt_rms_ms": t_lt, "g1_fused_ms": t_g1}
+        return t_g1 < 0.95 * t_lt
+
     def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None,
                 rope=None):
         from ._device import gemm
@@ -927,6 +973,9 @@ class UlyssesRunner:
         m = self.model
         c = m.config
         sc = 1.0 / math.sqrt(c.head_dim)
+        if self.g1_all:
+            return self._forward_g1(latent, t, ctx, cross, cache, collect_kv, chunk_index,
+                                    eps_out, rope, sc)
         for li, lw in enumerate(m.layers):
             if li == 0:
                 if isinstance(t, torch.Tensor):  # t*time_vec on device (graph replays)
@@ -958,6 +1007,36 @@ class UlyssesRunner:
         if eps_out is not None:
             self._rms(self.x, self.h)
             gemm(self.h, m.w_out, eps_out)
+
+    def _forward_g1(self, latent, t, ctx, cross, cache, collect_kv, chunk_index, eps_out, rope, sc):
+        """forward() with every projection on G1 and the RMS norms in the epilogues (engine
+        BlockRunner._forward_g1): the residual GEMMs emit the bf16 rows and their sums of
+        squares, the next projection applies the norm as a row scale."""
+        from ._device import gemm_fused
+        from .engine import _cross_attend_g1
+        from .kvcache import SELF_ATTN
+        m, norm = self.model, self.norm
+        for li, lw in enumerate(m.layers):
+            if li == 0:  # x = latent + t*time_vec fused into the first norm (engine.py:199)
+                if isinstance(t, torch.Tensor):
+                    self._rms(latent, self.h, t, 1.0, self.x)
+                else:
+                    self._rms(latent, self.h, m.time_vec, t, self.x)
+                nin = None
+            else:
+                nin = norm
+            app = None
+            if collect_kv:
+                def app(kc, vc, li=li):
+                    cache.append_block(li, kc, vc, kind=SELF_ATTN, chunk_index=chunk_index)
+            self._p2p_attention(li, ctx, sc, self.attn_events, lw, rope, app, norm_in=nin)
+            gemm_fused(self.xch.s_view, lw.wo, self.x, beta=1.0, norm_out=norm)
+            if cross is not None:
+                _cross_attend_g1(self, cross[li], norm, sc)
+            gemm_fused(self.h, lw.w1, self.ffn, relu=True, norm_in=norm)
+            gemm_fused(self.ffn, lw.w2, self.x, beta=1.0, norm_out=norm)
+        if eps_out is not None:
+            gemm_fused(self.h, m.w_out, eps_out, norm_in=norm)
 
     def _a2a_attention(self, li, ctx, sc, ev, lw, rope):
         """QKV projection, pack -> all-to-all -> K1 -> all-to-all -> unpack (NCCL)."""

@@ -64,9 +64,11 @@ CFG = dict(layers=2, heads=4, head_dim=64, block_len=256, frame_shape=(8, 8), pr
 REQ = dict(num_blocks=3, seed=0, prompt_schedule=[(0, "a quiet scene"), (2, "rain")])
 
 
-def _rank(rank, world, port, q, cfg=None, kvc=None, pad=True, p2p=False):
+def _rank(rank, world, port, q, cfg=None, kvc=None, pad=True, p2p=False, g1=None):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if g1 is not None:
+        os.environ["IFX_G1"] = g1  # read when the engine module is imported (below)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -91,6 +93,35 @@ CFG_ROPE = dict(CFG, rope_grid=(1, 16, 16), heads=3)  # 3 heads on 2 ranks: dumm
 # host pool, restores / demotions move data per rank, host pages are staged for K1
 KV_SPILL = dict(num_layers=2, head_dim=256, page_len=16, capacity_pages_device=40,
                 capacity_pages_host=10**4)
+
+
+@pytest.mark.parametrize("world,cfg", [(2, CFG), (2, CFG_ROPE)])
+def test_ulysses_p2p_fused_norm_path(world, cfg):
+    """The peer-exchange rank with every projection on G1 and the RMS norms fused into the
+    epilogues (IFX_G1=all; chosen automatically at small per-rank row counts) vs the
+    single-GPU engine and the oracle (grouped plan for 3 heads on 2 ranks)."""
+    from oracle import engine as OE
+    from paper_2511_20714_b200 import engine as E
+
+    ref = E.Engine(E.build_model(E.ModelConfig(**cfg))).generate(
+        E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **REQ))
+    want, _ = OE.generate_sequence(OE.ToyModel(OE.ModelConfig(**cfg)),
+                                   OE.GenerationRequest(schedule=OE.DenoiseSchedule([1.0, 0.5]), **REQ))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, cfg, None, False, True, "all"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, lats, state, _ in res:
+        for a, b, w in zip(lats, ref, want):
+            assert np.abs(a - b.latent).max() <= 2e-2, rank
+            assert np.abs(a - w).max() <= 2e-2, rank
 
 
 @pytest.mark.parametrize("p2p", [False, True], ids=["a2a", "p2p"])

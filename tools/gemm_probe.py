@@ -2,7 +2,9 @@
 projection shapes. Each shape: 5 warm-up calls, then 20 timed calls with CUDA events on
 the current stream, both libraries alternating in rounds; prints one JSON line per shape.
 
-    python tools/gemm_probe.py [c2|c4|all]
+    python tools/gemm_probe.py [c2|c4|all] [--ranks W]
+
+--ranks W: the shapes of one Ulysses rank at W ranks (M = T / W rows).
 """
 
 import json
@@ -35,11 +37,13 @@ def timed(fn, n=20):
 
 
 def main():
-    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    which = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "all"
+    W = int(sys.argv[sys.argv.index("--ranks") + 1]) if "--ranks" in sys.argv else 1
     cfgs = ["c2", "c4"] if which == "all" else [which]
     g = torch.Generator(device="cuda").manual_seed(0)
     for cfg in cfgs:
         for name, M, N, K, mode in SHAPES[cfg]:
+            M //= W
             a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
             b = (torch.randn(K, N, device="cuda", generator=g) / K ** 0.5).bfloat16()
             f32 = mode.startswith("f32")
@@ -61,7 +65,7 @@ def main():
                 t_g1.append(timed(g1))
                 t_lt.append(timed(lt))
             fl = 2.0 * M * N * K
-            rec = {"cfg": cfg, "gemm": name, "M": M, "N": N, "K": K, "epilogue": mode,
+            rec = {"cfg": cfg, "ranks": W, "gemm": name, "M": M, "N": N, "K": K, "epilogue": mode,
                    "g1_us": min(t_g1) * 1e3, "cublaslt_us": min(t_lt) * 1e3,
                    "g1_tflops": fl / (min(t_g1) * 1e-3) / 1e12,
                    "cublaslt_tflops": fl / (min(t_lt) * 1e-3) / 1e12,

@@ -204,7 +204,8 @@ def main():
                     "k1_ms": round(attn_ms, 2), "k1_share": round(attn_ms / ms, 3),
                     "k1_tflops_rank": round(flops / W / (attn_ms / 1e3) / 1e12, 1),
                     "k1_tflops_by_block": blk_tf,
-                    "head_split": bench.head_split(eng.runner)}), flush=True)
+                    "head_split": bench.head_split(eng.runner), "g1_fused_norms": eng.runner.g1_all,
+                    "g1_choice_ms": getattr(eng.runner, "g1_choice", None)}), flush=True)
                 if args.profile:
                     _profile(roll, name, W, r)
                 eng.runner.release_graphs()
