@@ -963,7 +963,13 @@ class UlyssesRunner:
 
         t_lt, t_g1 = min(timed(lt) for _ in range(2)), min(timed(g1) for _ in range(2))
         self.g1_choice = {"cublaslt_rms_ms": t_lt, "g1_fused_ms": t_g1}
-        return t_g1 < 0.95 * t_lt
+        use = t_g1 < 0.95 * t_lt
+        comm = self.comm
+        if comm.world > 1 and not getattr(comm, "loopback", False):
+            votes = [None] * comm.world  # one decision for all ranks (rank 0's timing)
+            comm.dist.all_gather_object(votes, use, group=comm.group)
+            use = votes[0]
+        return use
 
     def forward(self, latent, t, ctx, cross, cache, collect_kv=False, chunk_index=0, eps_out=None,
                 rope=None):
