@@ -1126,6 +1126,11 @@ class UlyssesEngine:
         # the reference's seeded host noise (engine.py:280-282), generated bit-exactly by the
         # native parallel PCG64 parser; each rank copies only its sequence slice to the GPU
         make_noise = noise_provider or (lambda ch: _init_noise_pinned(c, request.seed, ch))
+        # the next block's noise is drawn (and pinned) on a host thread while this block's
+        # passes are enqueued: a rank at 8 GPUs is close to enqueue-bound
+        from concurrent.futures import ThreadPoolExecutor
+        pool = ThreadPoolExecutor(1)
+        nxt = pool.submit(make_noise, 0)
         cur = None
         out = []
         for chunk in range(request.num_blocks):
@@ -1136,7 +1141,9 @@ class UlyssesEngine:
                 for li, (kc, vc) in enumerate(_cross_kv(m, embed_prompt(m, prompt))):
                     self.cache.append_block(li, kc, vc, kind=CROSS_ATTN, chunk_index=chunk)
                 cur = prompt
-            noise = make_noise(chunk)
+            noise = nxt.result()
+            if chunk + 1 < request.num_blocks:
+                nxt = pool.submit(make_noise, chunk + 1)
             full = noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)
             lat = full[rank * n:(rank + 1) * n].to(m.time_vec.device, torch.float32,
                                                    non_blocking=True).clone()
@@ -1150,6 +1157,7 @@ class UlyssesEngine:
                 self.comm.dist.all_gather(parts, lat, group=self.comm.group)
                 lat = torch.cat(parts)
             out.append(lat)
+        pool.shutdown(wait=False)
         return out
 
 
