@@ -203,7 +203,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -373,7 +373,7 @@ def run_ours(args):
         "clocks": clocks,
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -482,7 +482,7 @@ def run_host_tier_bench(args, c, cfgname, local):
                       "pcie_GBps_if_serial": (moved[0] + moved[1] + staged) / (ms / 1e3) / 1e9},
         "gpu_launches": None, "clocks": clk.summary(), "cpu_baseline": None,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -595,7 +595,7 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
                          "peer_barriers": eng.runner.xch.mesh.barriers if eng.runner.xch else 0},
                 "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
                 "cuda_graphs": "denoise passes captured once per block, replayed (IFX_CUDA_GRAPHS=0: eager)"}
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.barrier()
     eng.runner.release_graphs()  # captured NCCL work must be freed before the group
     torch.cuda.synchronize()
@@ -603,7 +603,27 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
     return 0
 
 
+_JSON_FD = None  # the real stdout when fd 1 is redirected (N > 1)
+
+
+def emit(line: dict) -> None:
+    """Print the run's ONE JSON line on stdout (the real one, see main)."""
+    text = json.dumps(line) + "\n"
+    if _JSON_FD is None:
+        sys.stdout.write(text)
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, text.encode())
+
+
 def main():
+    global _JSON_FD
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or "--ulysses" in sys.argv:
+        # NCCL writes its banner ("NCCL version ...") to fd 1 on rank 0: keep stdout to the
+        # JSON line by sending everything else written to fd 1 to stderr
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
