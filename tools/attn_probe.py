@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--no-split", action="store_true")
     ap.add_argument("--paged", action="store_true", help="context through a page_len-16 slot table")
     ap.add_argument("--cross", type=int, default=0, help="n prompt keys only (cross-attention)")
+    ap.add_argument("--rows", type=int, default=0, help="query rows (default T; e.g. 2340 = "
+                    "one rank of 8 at the 12-head shape, grouped plan)")
     args = ap.parse_args()
     T, H, dh = 4680, args.heads, 128
     D = H * dh
@@ -46,7 +48,8 @@ def main():
         qkv = torch.randn(T, 3 * D, device="cuda").bfloat16()
         ks = torch.randn(max(C, 1), D, device="cuda").bfloat16()
         vs = torch.randn(max(C, 1), D, device="cuda").bfloat16()
-        out = torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
+        NQ = args.rows or T
+        out = torch.empty(NQ, D, device="cuda", dtype=torch.bfloat16)
         kw = {}
         if args.paged and C:  # engine layout: page k of the stream in slot k (appends are in order)
             P = 16
@@ -59,7 +62,7 @@ def main():
             kw = dict(ctx_slots=torch.arange(n_pages, device="cuda", dtype=torch.int32), page_len=P,
                       first_token=0, tile_runs=torch.from_numpy(
                           tile_run_codes(np.arange(n_pages, dtype=np.int32), P)).cuda())
-        f = lambda: attn_fwd(qkv[:, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:],  # noqa: E731
+        f = lambda: attn_fwd(qkv[:NQ, :D], H, dh, out, ks, vs, 0, C, qkv[:, D:2 * D], qkv[:, 2 * D:],  # noqa: E731
                              split_kv=not args.no_split, **kw)
         for _ in range(3):
             f()
@@ -71,7 +74,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.iters
-        flops = 4.0 * T * (C + T) * D
+        flops = 4.0 * NQ * (C + T) * D
         res.append({"b": b, "ms": round(ms, 4), "tflops": round(flops / ms / 1e9, 1)})
         print(json.dumps(res[-1]), flush=True)
 
