@@ -1,0 +1,4 @@
+export PYTHONPATH=$PWD
+for t in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_probe2.py > gpurun_out/san2_$t.log 2>&1; echo "$t rc=$?"; tail -3 gpurun_out/san2_$t.log
+done
