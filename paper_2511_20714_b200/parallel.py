@@ -653,11 +653,13 @@ class P2PExchange:
     row into the rank that owns that sequence row (region S, [n, Dp]). Two peer barriers
     per layer-pass (after the QKV GEMM; after attention) order the phases; they also cover
     the write-after-read hazards (a rank's next QKV GEMM starts only after every rank's
-    attention read R, its next attention only after every rank's wo GEMM read S).
+    attention read R, its next attention only after every rank's wo GEMM read S — so the
+    clean pass's page write, which reads this rank's K/V from R, runs before the second).
 
-    Works for the whole-head plan (heads % W == 0) and the balanced plan when a head's rows
-    and K/V reach at most two ranks (two scatter entries per block; always when heads >= W,
-    `layout` raises ConfigError otherwise)."""
+    Layouts (`layout`): whole heads (heads % W == 0: R = [T, 3*wl]); grouped (GroupedPlan:
+    Q [T/R, wl] of the rank's row slice, K and V [T, wl]); balanced (BalancedPlan: Q
+    segments stacked, K and V [T, hl*dhp]) when a head's rows and K/V reach at most two
+    ranks (two scatter entries per column block; `layout` raises ConfigError otherwise)."""
 
     def __init__(self, runner, comm):
         m = runner.model
