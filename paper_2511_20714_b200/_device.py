@@ -167,6 +167,9 @@ def gemm_tiles_n(m: int, n: int, k: int) -> int:
     return out.value
 
 
+_G1_ARGS: dict = {}  # gemm_fused argument blocks by call signature (pointers, shapes)
+
+
 def gemm_fused(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None, beta: float = 0.0,
                relu: bool = False, norm_in: RowNorm | None = None, norm_out: RowNorm | None = None,
                rope=None, page=None, scatter=None, stream=None) -> int:
@@ -181,7 +184,28 @@ def gemm_fused(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None, beta:
     page:     (pool abi, slots tensor, first_token, token0, k_col0, v_col0) page write.
     scatter:  (table, block_width): bf16 output column blocks stored into peers' buffers
               (device int64 table [blocks, 2, 4], ifx_gemm_params.scatter); out may be None.
-    Returns the column tile count (norm_out.parts)."""
+    Returns the column tile count (norm_out.parts).
+
+    The argument block of a call without a page write is cached on its pointers and shapes:
+    the engine repeats the same calls on the same buffers every pass, and re-filling the
+    ctypes struct was most of the host cost of a launch."""
+    key = None
+    if page is None:
+        key = (a.data_ptr(), a.shape, a.stride(0), b.data_ptr(), b.shape, b.stride(0),
+               None if out is None else (out.data_ptr(), out.shape, out.stride(0), out.dtype),
+               beta, relu,
+               None if norm_in is None else (norm_in.ss.data_ptr(), norm_in.parts, norm_in.dim),
+               None if norm_out is None else (norm_out.rows_bf16.data_ptr(), norm_out.ss.data_ptr()),
+               None if rope is None else (rope[0].data_ptr(), rope[1].data_ptr(), *rope[2:]),
+               None if scatter is None else (scatter[0].data_ptr(), scatter[1]))
+        hit = _G1_ARGS.get(key)
+        if hit is not None:
+            pref, tn, tref = hit
+            _abi.check(_abi.lib().ifx_gemm_fused(pref, tref, stream_ptr(stream)), "gemm_fused")
+            LAUNCHES[0] += 1
+            if norm_out is not None:
+                norm_out.parts, norm_out.dim = tn.value, b.shape[1]
+            return tn.value
     M, K = a.shape
     N = b.shape[1]
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or b.shape[0] != K or \
@@ -219,6 +243,10 @@ def gemm_fused(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None, beta:
                "gemm_fused")
     del keep
     LAUNCHES[0] += 1
+    if key is not None:
+        if len(_G1_ARGS) > 4096:
+            _G1_ARGS.clear()
+        _G1_ARGS[key] = (ctypes.byref(p), tn, ctypes.byref(tn))  # byref keeps p alive
     if norm_out is not None:
         norm_out.parts, norm_out.dim = tn.value, N
     return tn.value
