@@ -3,16 +3,19 @@
 blocks (C = b*T context keys + T own keys), non-causal. Same FLOP accounting as
 tools/attn_probe.py: 4*T*(C+T)*D / CUDA-event time."""
 import json
+import sys
 
 import torch
 
 from vllm.vllm_flash_attn.cute.interface import flash_attn_func
 
-T, H, dh = 4680, 12, 128
+T, dh = 4680, 128
+H = int(sys.argv[sys.argv.index("--heads") + 1]) if "--heads" in sys.argv else 12
+NQ = int(sys.argv[sys.argv.index("--rows") + 1]) if "--rows" in sys.argv else T
 D = H * dh
 for b in (0, 1, 3, 6, 20):
     C = b * T
-    q = torch.randn(1, T, H, dh, device="cuda", dtype=torch.bfloat16)
+    q = torch.randn(1, NQ, H, dh, device="cuda", dtype=torch.bfloat16)
     k = torch.randn(1, C + T, H, dh, device="cuda", dtype=torch.bfloat16)
     v = torch.randn(1, C + T, H, dh, device="cuda", dtype=torch.bfloat16)
     f = lambda: flash_attn_func(q, k, v, causal=False)  # noqa: E731
@@ -27,4 +30,5 @@ for b in (0, 1, 3, 6, 20):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
     print(json.dumps({"impl": "fa4-cute (vllm, reference ceiling)", "b": b, "ms": round(ms, 4),
-                      "tflops": round(4.0 * T * (C + T) * D / ms / 1e9, 1)}), flush=True)
+                      "heads": H, "rows": NQ,
+                      "tflops": round(4.0 * NQ * (C + T) * D / ms / 1e9, 1)}), flush=True)
