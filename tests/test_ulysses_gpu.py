@@ -256,3 +256,59 @@ def test_ulysses_nccl_graph_capture_world1(p2p):
     for a, b in zip(lats, ref):
         assert np.abs(a - b.latent).max() <= 2e-2
     assert state == ref_eng.cache.state()
+
+
+C2W = dict(layers=2, heads=12, head_dim=128, block_len=4680, frame_shape=(4, 4), prompt_dim=16,
+           weight_seed=0)
+C2REQ = dict(num_blocks=2, seed=0, prompt_schedule=[(0, "a quiet scene")])
+
+
+def _rank_c2(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_20714_b200 import engine as E
+        from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
+
+        eng = UlyssesEngine(E.build_model(E.ModelConfig(**C2W)), UlyssesComm(), p2p=True)
+        lats = eng.generate(E.GenerationRequest(schedule=E.DenoiseSchedule([1.0, 0.5]), **C2REQ))
+        plan = ("grouped" if eng.runner.grouped is not None else
+                "balanced" if eng.runner.plan is not None else "whole")
+        eng.runner.release_graphs()
+        torch.cuda.synchronize()
+        q.put((rank, [x.cpu().numpy() for x in lats], eng.cache.state(), plan))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_ulysses_p2p_c2_shape_vs_oracle(world):
+    """The peer-exchange Ulysses engine at the benchmark's width and block length (12 heads
+    x 128, 4,680 tokens, reference PCG64 weights and seeded noise; 2 layers, 2 blocks) on
+    `world` rank processes sharing cuda:0 — 2 ranks: whole heads (6 per rank); 8 ranks: the
+    grouped plan the 8-GPU bench runs (4 head groups x 2 row slices) — vs the numpy oracle:
+    max-abs <= 2e-2, cosine > 0.999, page table identical on every rank."""
+    from oracle import engine as OE
+
+    want, ocache = OE.generate_sequence(OE.ToyModel(OE.ModelConfig(**C2W)), OE.GenerationRequest(
+        schedule=OE.DenoiseSchedule([1.0, 0.5]), **C2REQ))
+    want = np.stack(want)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_c2, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, lats, state, plan in res:
+        got = np.stack(lats)
+        a, b = got.ravel().astype(np.float64), want.ravel().astype(np.float64)
+        cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+        assert np.abs(got - want).max() <= 2e-2 and cos > 0.999, (rank, float(np.abs(got - want).max()))
+        assert state == ocache.state()
+        assert plan == ("whole" if world == 2 else "grouped")
