@@ -1214,6 +1214,18 @@ def _prompt_for_chunk(schedule, chunk: int) -> str:
     return text
 
 
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev: torch.device, which: int) -> torch.cuda.Stream:
+    """Per-device side streams for a block's input (0: noise H2D) and output (1: latent and
+    frames D2H) transfers, so the DMA copy engines overlap neighbouring blocks' passes."""
+    st = _COPY_STREAMS.get((dev, which))
+    if st is None:
+        st = _COPY_STREAMS[(dev, which)] = torch.cuda.Stream(dev)
+    return st
+
+
 def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSchedule, prompt_ctx,
                    chunk_index: int, seed: int, prompt_text: str = "", noise=None,
                    to_host: bool = True, _ready=None) -> GeneratedBlock:
@@ -1227,8 +1239,18 @@ def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSche
     if noise is None:
         noise = _init_noise_pinned(c, seed, chunk_index)
     src = noise if isinstance(noise, torch.Tensor) else torch.from_numpy(noise)
-    lat = torch.empty(src.shape, device=require_cuda(), dtype=torch.float32)
-    lat.copy_(src, non_blocking=True)  # async H2D when the noise lives in pinned memory
+    dev = require_cuda()
+    main = torch.cuda.current_stream()
+    if src.is_cuda or not src.is_pinned():
+        lat = torch.empty(src.shape, device=dev, dtype=torch.float32)
+        lat.copy_(src, non_blocking=True)
+    else:  # pinned host noise: H2D on its own stream, overlapping the previous block
+        cin = _copy_stream(dev, 0)
+        with torch.cuda.stream(cin):  # allocated on that stream, used by main after the copy
+            lat = torch.empty(src.shape, device=dev, dtype=torch.float32)
+            lat.copy_(src, non_blocking=True)
+        main.wait_stream(cin)
+        lat.record_stream(main)
     runner = _runner(model)
     ctx, cross = _block_context(model, cache, prompt_ctx, runner.stager, len(schedule.steps) + 1)
     runner.denoise(lat, schedule, ctx, cross, cache, chunk_index)
@@ -1239,13 +1261,19 @@ def generate_block(model: ToyModel, cache: KvCache | None, schedule: DenoiseSche
     px = _decode_px(model, lat)
     lat_h = torch.empty(lat.shape, dtype=torch.float32, pin_memory=True)
     px_h = torch.empty(px.shape, dtype=torch.uint8, pin_memory=True)
-    lat_h.copy_(lat, non_blocking=True)
-    px_h.copy_(px, non_blocking=True)
+    # D2H on its own stream: the next block's passes start while the results stream out
+    cs = _copy_stream(lat.device, 1)
+    cs.wait_stream(main)
+    with torch.cuda.stream(cs):
+        lat_h.copy_(lat, non_blocking=True)
+        px_h.copy_(px, non_blocking=True)
+    lat.record_stream(cs)
+    px.record_stream(cs)
+    ev = torch.cuda.Event()
+    ev.record(cs)
     if _ready is None:
-        torch.cuda.current_stream().synchronize()
+        ev.synchronize()
     else:
-        ev = torch.cuda.Event()
-        ev.record()
         _ready.append(ev)
     return GeneratedBlock(chunk_index, lat_h.numpy(), list(px_h.view(-1, h, w).numpy()), prompt_text)
 
