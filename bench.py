@@ -563,8 +563,7 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
     # e2e: host noise (reference seeding) in, gathered latents out
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        lats = eng.generate(req)
-        host = [l.cpu() for l in lats]
+        host = eng.generate(req, to_host=True)  # gathered latents in pinned host memory
     torch.cuda.synchronize()
     e2e = torch.tensor([(time.perf_counter() - t0) / args.steps], device="cuda")
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)

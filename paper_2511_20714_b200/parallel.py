@@ -1113,8 +1113,10 @@ class UlyssesEngine:
         self.runner = UlyssesRunner(model, comm, attn, p2p=p2p)
         self.cache = None
 
-    def generate(self, request, noise_provider=None, gather: bool = True):
-        """Returns per-block full latents (gathered) if `gather`, else local shards."""
+    def generate(self, request, noise_provider=None, gather: bool = True, to_host: bool = False):
+        """Returns per-block full latents (gathered) if `gather`, else local shards; with
+        `to_host` as pinned host tensors, each block's copy running on a side stream while
+        the next block computes."""
         from .engine import (_block_context, _cross_kv, _init_noise_pinned,
                              _prompt_for_chunk, embed_prompt)
         from .kvcache import CROSS_ATTN, KvCache
@@ -1158,8 +1160,21 @@ class UlyssesEngine:
                 parts = [torch.empty_like(lat) for _ in range(self.comm.world)]
                 self.comm.dist.all_gather(parts, lat, group=self.comm.group)
                 lat = torch.cat(parts)
+            if to_host:
+                from .engine import _copy_stream
+                main = torch.cuda.current_stream()
+                cs = _copy_stream(lat.device, 1)
+                cs.wait_stream(main)
+                host = torch.empty(lat.shape, dtype=lat.dtype, pin_memory=True)
+                with torch.cuda.stream(cs):
+                    host.copy_(lat, non_blocking=True)
+                lat.record_stream(cs)
+                lat = host
             out.append(lat)
         pool.shutdown(wait=False)
+        if to_host:
+            from .engine import _copy_stream
+            _copy_stream(torch.device("cuda", torch.cuda.current_device()), 1).synchronize()
         return out
 
 
