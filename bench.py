@@ -22,6 +22,14 @@ cpu_baseline  the numpy oracle port (oracle/engine.py:layer_pass) on the host co
          two layer-passes at the exact shape (b = 0 and 1 cached blocks), extrapolated
          linearly in b to the same rollout.
 
+N > 1 (torchrun, one rank per GPU): the same c2 rollout strong-scaled with Ulysses; the
+head <-> sequence re-shard runs through NVLink peer memory (G1's QKV epilogue and K1's O
+epilogue store into the consuming rank; peer barriers; `--exchange nccl` for all-to-alls);
+12 heads on 8 GPUs use the grouped plan (4 head groups x 2 query-row slices). value = all
+ranks' frames / max-over-ranks device time; e2e through UlyssesEngine.generate with host
+noise and gathered latents copied to host; roofline = rank 0's K1 launches; stdout carries
+only rank 0's JSON line. `--ulysses` runs that engine at N = 1.
+
 --impl reference: the reference's CPU algorithm (the oracle port; the Python reference
 cannot travel to the GPU box) on all host cores, same metric/config; each step is one
 bounded sample (a pair of layer-passes), extrapolated to the rollout.
