@@ -256,7 +256,7 @@ int ifx_attn_workspace_bytes(const ifx_attn_params* p, int64_t* bytes);
  * row max (log2 units, -inf = no visible key) and denominator w.r.t. it — exactly what
  * ifx_attn_fwd writes with row_max / row_sum set. o = sum_s w_s O_s / sum_s w_s, w_s =
  * l_s 2^(m_s - max m); if row_max != NULL the merged max / denominator are written too
- * (denominator 0 = the row saw no key in any shard). */
+ * (denominator 0 = the row saw no key in any shard). n_splits <= 32. */
 int ifx_attn_combine(const void* part_o, int64_t part_ld, const float* part_m,
                      const float* part_l, int64_t n_splits, int64_t n_q, int64_t heads,
                      int64_t head_dim, void* o, int64_t o_ld, float* row_max, float* row_sum,

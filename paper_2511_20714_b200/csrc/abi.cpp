@@ -360,7 +360,8 @@ int ifx_attn_combine(const void* part_o, int64_t part_ld, const float* part_m,
                      int64_t head_dim, void* o, int64_t o_ld, float* row_max, float* row_sum,
                      void* stream) {
   if (head_dim != 64 && head_dim != 128) return ifx::fail(IFX_EUNSUPPORTED, "head_dim must be 64 or 128");
-  if (n_splits < 1 || n_q < 0 || heads < 1 || part_ld < heads * head_dim || o_ld < heads * head_dim ||
+  if (n_splits < 1 || n_splits > 32 || n_q < 0 || heads < 1 || part_ld < heads * head_dim ||
+      o_ld < heads * head_dim ||
       n_q > INT32_MAX || n_splits > INT32_MAX)
     return ifx::fail(IFX_EDIM, "bad combine sizes");
   if (part_o == nullptr || part_m == nullptr || part_l == nullptr || o == nullptr ||

@@ -37,6 +37,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "attn_kernel.h"
 #include "device_state.h"
@@ -644,14 +645,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     named_sync(pair_bar, 64);  // the partner has read `red` before the next item rewrites it
     }
-    // peer stores (O scatter, or partials written into a peer's arena) out before the
-    // barrier that publishes them
-    if (a.o_peer_rows > 0 || a.row_max != nullptr) __threadfence_system();
   }
 
   pdl_trigger();
   tc_fence_before();
   __syncthreads();
+  // peer stores (O scatter, or partials written into a peer's arena) out before the barrier
+  // that publishes them: one system fence per CTA, cumulative over the CTA's stores
+  if (threadIdx.x == 0 && (a.o_peer_rows > 0 || a.row_max != nullptr)) __threadfence_system();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -663,39 +664,57 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 template <int HD>
 __global__ void attn_combine_kernel(const AttnKernelArgs a) {
   pdl_wait();
-  constexpr int PER = HD / 32;
+  constexpr int PER = HD / 32;  // head dims per lane: one 8-byte (HD 128) / 4-byte load
+  using Vec = typename std::conditional<PER == 4, uint2, uint32_t>::type;
   const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
+  const int S = a.n_splits;  // <= 32: lane s holds split s's statistics
   for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
        w < (int64_t)a.n_q * a.heads; w += n_warps) {
     const int row = (int)(w / a.heads), head = (int)(w % a.heads);
-    float M = -INFINITY;
-    for (int s = 0; s < a.n_splits; ++s)
-      M = fmaxf(M, a.part_m[((int64_t)s * a.heads + head) * a.n_q + row]);
+    float ms = -INFINITY, ls = 0.f;
+    if (lane < S) {
+      const int64_t k = ((int64_t)lane * a.heads + head) * a.n_q + row;
+      ms = a.part_m[k];
+      ls = a.part_l[k];
+    }
+    float M = ms;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float wl = (ms == -INFINITY) ? 0.f : ls * exp2f(ms - M);
+    float den = wl;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
     float acc[PER];
 #pragma unroll
     for (int i = 0; i < PER; ++i) acc[i] = 0.f;
-    float den = 0.f;
-    for (int s = 0; s < a.n_splits; ++s) {
-      const int64_t k = ((int64_t)s * a.heads + head) * a.n_q + row;
-      const float ms = a.part_m[k];
-      const float wgt = (ms == -INFINITY) ? 0.f : a.part_l[k] * exp2f(ms - M);
-      den += wgt;
-      const __nv_bfloat16* src =
-          a.part_o + ((int64_t)s * a.n_q + row) * a.part_ld + head * HD + lane * PER;
+    for (int s = 0; s < S; ++s) {
+      const float wgt = __shfl_sync(0xffffffffu, wl, s);
+      const Vec v = *reinterpret_cast<const Vec*>(
+          a.part_o + ((int64_t)s * a.n_q + row) * a.part_ld + head * HD + lane * PER);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
-      for (int i = 0; i < PER; ++i) acc[i] += wgt * __bfloat162float(src[i]);
+      for (int i = 0; i < PER / 2; ++i) {
+        const float2 f = __bfloat1622float2(h2[i]);
+        acc[2 * i] = fmaf(wgt, f.x, acc[2 * i]);
+        acc[2 * i + 1] = fmaf(wgt, f.y, acc[2 * i + 1]);
+      }
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
-    __nv_bfloat16* dst = attn_out_row(a, row) + head * HD + lane * PER;
+    Vec out;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
 #pragma unroll
-    for (int i = 0; i < PER; ++i) dst[i] = __float2bfloat16(acc[i] * inv);
+    for (int i = 0; i < PER / 2; ++i) o2[i] = __floats2bfloat162_rn(acc[2 * i] * inv, acc[2 * i + 1] * inv);
+    *reinterpret_cast<Vec*>(attn_out_row(a, row) + head * HD + lane * PER) = out;
     if (a.row_max != nullptr && lane == 0) {
       a.row_max[(int64_t)head * a.n_q + row] = M;
       a.row_sum[(int64_t)head * a.n_q + row] = den;
     }
   }
-  if (a.o_peer_rows > 0 || a.row_max != nullptr) __threadfence_system();
+  if (a.o_peer_rows > 0 || a.row_max != nullptr) {  // peer stores out before the barrier:
+    __syncthreads();                                  // one system fence per CTA, cumulative
+    if (threadIdx.x == 0) __threadfence_system();     // over the CTA's stores (bar.sync)
+  }
 }
 
 template <int HD>

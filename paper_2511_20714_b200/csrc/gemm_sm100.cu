@@ -500,12 +500,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_kernel(const __grid_constant
         }
       }
     }
-    if (a.scat != nullptr) __threadfence_system();  // peer stores out before the barrier
   }
 
   pdl_trigger();
   tc_fence_before();
   __syncthreads();
+  // peer-scatter stores out before the barrier that publishes them (one system fence per
+  // CTA, cumulative over the CTA's stores through the bar.sync above)
+  if (threadIdx.x == 0 && a.scat != nullptr) __threadfence_system();
   if (CL > 1) cluster_sync_all();  // no multicast or remote arrive still targets this CTA
   if (warp == 1) {
     tc_fence_after();
