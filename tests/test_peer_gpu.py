@@ -119,3 +119,36 @@ def test_peer_barrier_rejects_bad_meshes():
     with pytest.raises(DimensionError):
         _abi.check(_abi.lib().ifx_peer_barrier(pads, 9, 0, ctypes.c_void_p(arena.data_ptr() + 128),
                                                100, None), "barrier")
+
+
+@pytest.mark.parametrize("splits,hd", [(1, 128), (3, 128), (8, 64), (32, 128)])
+def test_attn_combine_matches_torch(splits, hd):
+    """K4 alone (ifx_attn_combine): merge `splits` normalised partials with their (max,
+    denominator) statistics, some splits dead (max -inf), vs the merge in torch fp64
+    (attention.py:157-180)."""
+    from paper_2511_20714_b200 import _abi
+    from paper_2511_20714_b200._device import stream_ptr
+
+    torch.manual_seed(splits)
+    n, H = 300, 3
+    D = H * hd
+    po = torch.randn(splits, n, D, device="cuda").bfloat16()
+    pm = torch.randn(splits, H, n, device="cuda") * 3
+    pl = torch.rand(splits, H, n, device="cuda") * 5 + 0.1
+    if splits > 1:  # a dead split for every row of head 1, a row dead in all but one split
+        pm[0, 1] = float("-inf")
+        pm[1:, 0, 7] = float("-inf")
+    out = torch.empty(n, D, device="cuda", dtype=torch.bfloat16)
+    rmax = torch.empty(H, n, device="cuda")
+    rsum = torch.empty(H, n, device="cuda")
+    _abi.check(_abi.lib().ifx_attn_combine(po.data_ptr(), D, pm.data_ptr(), pl.data_ptr(), splits, n,
+                                           H, hd, out.data_ptr(), D, rmax.data_ptr(), rsum.data_ptr(),
+                                           stream_ptr()), "combine")
+    torch.cuda.synchronize()
+    M = pm.double().amax(0)                                   # [H, n]
+    w = torch.where(pm.isinf(), torch.zeros_like(pl.double()), pl.double() * torch.exp2(pm.double() - M))
+    den = w.sum(0)                                            # [H, n]
+    o = po.double().view(splits, n, H, hd)
+    want = (o * w.permute(0, 2, 1)[..., None]).sum(0) / den.t()[..., None]
+    assert torch.allclose(out.double().view(n, H, hd), want, atol=2e-2, rtol=1e-2)
+    assert torch.allclose(rsum.double(), den, rtol=1e-4) and torch.allclose(rmax.double(), M)
