@@ -15,6 +15,19 @@ Reference: /root/reference/pkg/src/inferix/parallel.py. Two layers:
    head-sharded, the KV cache head-sharded and rank-local (never communicated), the page
    table replicated and identical on every rank, and cross-attention sequence-sharded
    against replicated prompt K/V (no communication).
+
+3. The same exchange over NVLink peer memory instead of NCCL (`P2PExchange`, the default
+   when every rank can map every other rank's arena): `PeerMesh` opens each rank's arena
+   in every other rank through CUDA IPC; G1's scatter epilogue writes each Q/K/V column
+   block straight into the owner's head-group buffer, K1 scatters its output rows back
+   into the sequence owners' buffers, and a graph-capturable barrier kernel
+   (ifx_peer_barrier) orders the two passes — no pack/unpack kernels and no all-to-all
+   launches. Head counts that do not divide the world use the grouped plan
+   (`grouped_split`: G head groups x R <= 2 query-row slices, one K1 launch per rank).
+
+The reference's per-strategy entry points also exist over real ranks
+(`ulysses_attention_dist`, `ring_attention_pass_kv_dist`, `ring_attention_pass_q_dist`,
+`sequence_parallel_attention`), with the same SpTrace byte accounting as layer 1.
 """
 
 from __future__ import annotations
