@@ -1119,11 +1119,19 @@ class UlyssesEngine:
         self.kv_config = kv_config or default_kv_config(model.config)
         if self.kv_config.latent is not None:  # the up-projection mixes every head's columns
             raise ConfigError("latent KV mode is not supported with head-sharded (Ulysses) caches")
+        self.runner = None
         if p2p is None:
             mode = os.environ.get("IFX_ULYSSES", "auto")
-            p2p = mode == "p2p" or (mode == "auto" and attn is None and
-                                     model.heads_pad >= comm.world)
-        self.runner = UlyssesRunner(model, comm, attn, p2p=p2p)
+            p2p = mode == "p2p"
+            if mode == "auto" and attn is None and model.heads_pad >= comm.world:
+                try:  # peer mesh failures are agreed across ranks: all fall back together
+                    self.runner = UlyssesRunner(model, comm, attn, p2p=True)
+                except ConfigError as e:
+                    import warnings
+                    warnings.warn(f"Ulysses: peer-memory exchange unavailable ({e}); "
+                                  "using NCCL all-to-alls", RuntimeWarning)
+        if self.runner is None:
+            self.runner = UlyssesRunner(model, comm, attn, p2p=bool(p2p))
         self.cache = None
 
     def generate(self, request, noise_provider=None, gather: bool = True, to_host: bool = False):

@@ -236,6 +236,52 @@ def _rank_nccl(port, q, p2p=False):
         dist.destroy_process_group()
 
 
+def _auto_fallback(port, q):
+    """UlyssesEngine's default exchange when the peer mesh cannot be built (CUDA IPC refused,
+    simulated): every rank falls back to the NCCL all-to-alls instead of failing."""
+    import warnings
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.pop("IFX_ULYSSES", None)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2511_20714_b200 import engine as E
+        from paper_2511_20714_b200 import parallel as P
+        from paper_2511_20714_b200.errors import ConfigError
+
+        def refuse(self, *a, **k):
+            raise ConfigError("peer mesh: cudaIpcOpenMemHandle refused (test)")
+        P.PeerMesh.__init__ = refuse
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            eng = P.UlyssesEngine(E.build_model(E.ModelConfig(**CFG)), P.UlyssesComm())
+        lats = [b.cpu().numpy() for b in eng.generate(E.GenerationRequest(
+            schedule=E.DenoiseSchedule(GRAPH_STEPS), **REQ))]
+        q.put((eng.runner.xch is None, any("NCCL" in str(x.message) for x in w), lats))
+        eng.runner.release_graphs()
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ulysses_auto_exchange_falls_back_to_nccl():
+    from paper_2511_20714_b200 import engine as E
+
+    ref = E.Engine(E.build_model(E.ModelConfig(**CFG))).generate(
+        E.GenerationRequest(schedule=E.DenoiseSchedule(GRAPH_STEPS), **REQ))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_auto_fallback, args=(_free_port(), q))
+    p.start()
+    nccl, warned, lats = q.get(timeout=300)
+    p.join(timeout=120)
+    assert p.exitcode == 0 and nccl and warned
+    for a, b in zip(lats, ref):
+        assert np.abs(a - b.latent).max() <= 2e-2
+
+
 @pytest.mark.parametrize("p2p", [False, True], ids=["a2a", "p2p"])
 def test_ulysses_nccl_graph_capture_world1(p2p):
     """The NCCL path of the Ulysses runner on one GPU: its denoise passes are captured as
