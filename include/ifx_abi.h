@@ -32,6 +32,7 @@ extern "C" {
 #define IFX_ECONFIG 5   /* ConfigError     (errors.py:24) */
 #define IFX_ECUDA 16    /* CUDA runtime/driver failure (no reference equivalent) */
 #define IFX_EUNSUPPORTED 17
+#define IFX_ENCCL 18    /* NCCL failure, or NCCL not loadable (ifx_comm_*) */
 
 /* stream kinds (kvcache.py:75-76) */
 #define IFX_SELF_ATTN 0
@@ -326,6 +327,27 @@ int ifx_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int
  * that does not arrive within ~timeout_ms traps (a CUDA error instead of a hang). */
 int ifx_peer_barrier(void* const* pads, int world, int rank, uint32_t* counter, int timeout_ms,
                      void* stream);
+
+/* NCCL communicator for hosts that run the Ulysses exchange without torch.distributed
+ * (SURVEY §8(b) `ifx_comm_init`; replaces the reference's WorkerGroup / all_to_all,
+ * parallel.py:63-111, with a real collective over NVLink / NVSwitch). NCCL is loaded on
+ * first use (dlopen libnccl.so.2); IFX_ENCCL when it is absent or a call fails.
+ * ifx_comm_unique_id: 128 opaque bytes, made on rank 0 and sent to every rank out of band.
+ * ifx_comm_init: this rank's communicator on the CURRENT CUDA device (collective over the
+ * `world` ranks). ifx_comm_all_to_all: the variable-size byte all-to-all of the Ulysses
+ * re-shard (what UlyssesComm.a2a_var does over torch.distributed): host arrays of `world`
+ * byte offsets / sizes into the DEVICE buffers send / recv, enqueued on `stream`.
+ * ifx_comm_all_gather: `bytes` from every rank into recv[rank * bytes] (e.g. the 64-byte
+ * CUDA IPC handles a peer mesh needs, copied to device first). */
+typedef struct ifx_comm ifx_comm;
+int ifx_comm_unique_id(void* id_out);
+int ifx_comm_init(const void* id, int world, int rank, ifx_comm** out);
+int ifx_comm_destroy(ifx_comm* comm);
+int ifx_comm_size(const ifx_comm* comm, int* world, int* rank);
+int ifx_comm_all_to_all(ifx_comm* comm, const void* send, const int64_t* send_off,
+                        const int64_t* send_bytes, void* recv, const int64_t* recv_off,
+                        const int64_t* recv_bytes, void* stream);
+int ifx_comm_all_gather(ifx_comm* comm, const void* send, int64_t bytes, void* recv, void* stream);
 
 /* Dense projection on cuBLASLt (a plain library GEMM; per-shape algorithm choice timed on
  * the first call outside a CUDA-graph capture): D[M,N] = relu?(A[M,K] . B[K,N] + beta * D),

@@ -25,13 +25,13 @@ from .errors import (
 LIB_PATH = os.environ.get("IFX_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libinferix_b200.so")  # override: A/B builds
 
-OK, EDIM, EMASK, ECAPACITY, ERANGE, ECONFIG, ECUDA, EUNSUPPORTED = 0, 1, 2, 3, 4, 5, 16, 17
+OK, EDIM, EMASK, ECAPACITY, ERANGE, ECONFIG, ECUDA, EUNSUPPORTED, ENCCL = 0, 1, 2, 3, 4, 5, 16, 17, 18
 SELF_ATTN, CROSS_ATTN = 0, 1
 F32, BF16 = 0, 1
 
 _ERRORS = {EDIM: DimensionError, EMASK: MaskError, ECAPACITY: CapacityError,
            ERANGE: OutOfRangeError, ECONFIG: ConfigError, ECUDA: CudaError,
-           EUNSUPPORTED: DimensionError}
+           EUNSUPPORTED: DimensionError, ENCCL: CudaError}
 
 # every symbol include/ifx_abi.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -47,6 +47,8 @@ EXPORTS = (
     "ifx_copy_blocks", "ifx_gemm_bf16", "ifx_gemm_fused", "ifx_gemm_tiles_n",
     "ifx_noise_normal_f32",
     "ifx_ipc_handle", "ifx_ipc_open", "ifx_ipc_close", "ifx_memcpy2d", "ifx_peer_barrier",
+    "ifx_comm_unique_id", "ifx_comm_init", "ifx_comm_destroy", "ifx_comm_size",
+    "ifx_comm_all_to_all", "ifx_comm_all_gather",
 )
 
 
@@ -179,6 +181,12 @@ def lib() -> ctypes.CDLL:
             L.ifx_attn_combine.argtypes = [P, I64, P, P, I64, I64, I64, I64, P, I64, P, P, P]
             L.ifx_peer_barrier.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, P,
                                            ctypes.c_int, P]
+            L.ifx_comm_unique_id.argtypes = [P]
+            L.ifx_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
+            L.ifx_comm_destroy.argtypes = [P]
+            L.ifx_comm_size.argtypes = [P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+            L.ifx_comm_all_to_all.argtypes = [P, P, PI64, PI64, P, PI64, PI64, P]
+            L.ifx_comm_all_gather.argtypes = [P, P, I64, P, P]
             L.ifx_noise_normal_f32.argtypes = [ctypes.POINTER(ctypes.c_uint64), I64, P, ctypes.c_int]
             _lib = L
     return _lib

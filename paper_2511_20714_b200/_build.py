@@ -17,7 +17,7 @@ OUT = os.path.join(PKG, "libinferix_b200.so")
 OBJ = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["attn_fwd_sm100.cu", "gemm_sm100.cu", "attn_few_keys.cu", "kv_ops.cu", "kv_latent.cu", "peer.cu", "gemm_lt.cpp", "abi.cpp", "pagetable.cpp", "noise_host.cpp"]
+SOURCES = ["attn_fwd_sm100.cu", "gemm_sm100.cu", "attn_few_keys.cu", "kv_ops.cu", "kv_latent.cu", "peer.cu", "comm.cpp", "gemm_lt.cpp", "abi.cpp", "pagetable.cpp", "noise_host.cpp"]
 
 
 def _npyrandom() -> str:
@@ -74,7 +74,7 @@ def build(verbose: bool = False) -> str:
     cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, _npyrandom(), "-lcudart_static",
            f"-L{lt}", "-l:libcublasLt.so.12", "-Xlinker", f"-rpath={lt}",
            "-Xlinker", "--disable-new-dtags",  # DT_RPATH: wins over LD_LIBRARY_PATH
-           "-Xlinker", "--exclude-libs,ALL", "-lm", "-Xcompiler", "-fPIC"]
+           "-Xlinker", "--exclude-libs,ALL", "-lm", "-ldl", "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

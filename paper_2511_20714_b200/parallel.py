@@ -384,6 +384,71 @@ class UlyssesComm:
         return self._unpack(recv, out, 1, self.world, chunk)
 
 
+class NativeComm:
+    """The C-ABI's NCCL communicator (include/ifx_abi.h ifx_comm_*) — what a host without
+    torch.distributed binds (SURVEY §8(b) `ifx_comm_init`): the reference's WorkerGroup +
+    all_to_all (parallel.py:63-111) as a real collective on the current CUDA device.
+    `NativeComm.unique_id()` on rank 0, shipped to every rank out of band, then
+    `NativeComm(uid, world, rank)` on each. `all_to_all` has UlyssesComm.a2a_var's meaning
+    (per-peer element counts, contiguous per-peer chunks); `all_gather` concatenates every
+    rank's buffer in rank order."""
+
+    def __init__(self, uid: bytes, world: int, rank: int):
+        import ctypes
+        if len(uid) != 128:
+            raise DimensionError("an NCCL unique id is 128 bytes")
+        self._h = ctypes.c_void_p()
+        _abi.check(_abi.lib().ifx_comm_init(uid, world, rank, ctypes.byref(self._h)), "comm_init")
+        self.world, self.rank = world, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+        buf = ctypes.create_string_buffer(128)
+        _abi.check(_abi.lib().ifx_comm_unique_id(buf), "comm_unique_id")
+        return buf.raw
+
+    def all_to_all(self, send: torch.Tensor, send_sizes, recv: torch.Tensor, recv_sizes,
+                   stream=None) -> torch.Tensor:
+        import ctypes
+        from ._device import stream_ptr
+        if len(send_sizes) != self.world or len(recv_sizes) != self.world:
+            raise DimensionError("one send and one receive size per rank")
+        if sum(send_sizes) > send.numel() or sum(recv_sizes) > recv.numel() or \
+                send.dtype != recv.dtype or not send.is_contiguous() or not recv.is_contiguous():
+            raise DimensionError("all_to_all sizes exceed the contiguous buffers")
+        es = send.element_size()
+        arr = lambda v: (ctypes.c_int64 * self.world)(*v)  # noqa: E731
+        so = np.concatenate([[0], np.cumsum(send_sizes)[:-1]]) * es
+        ro = np.concatenate([[0], np.cumsum(recv_sizes)[:-1]]) * es
+        _abi.check(_abi.lib().ifx_comm_all_to_all(
+            self._h, send.data_ptr(), arr(so.tolist()), arr([n * es for n in send_sizes]),
+            recv.data_ptr(), arr(ro.tolist()), arr([n * es for n in recv_sizes]),
+            stream_ptr(stream)), "comm_all_to_all")
+        return recv
+
+    def all_gather(self, send: torch.Tensor, recv: torch.Tensor, stream=None) -> torch.Tensor:
+        from ._device import stream_ptr
+        nb = send.numel() * send.element_size()
+        if recv.numel() * recv.element_size() < nb * self.world or not send.is_contiguous() or \
+                not recv.is_contiguous():
+            raise DimensionError("all_gather needs world x the send bytes, contiguous")
+        _abi.check(_abi.lib().ifx_comm_all_gather(self._h, send.data_ptr(), nb, recv.data_ptr(),
+                                                  stream_ptr(stream)), "comm_all_gather")
+        return recv
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            _abi.check(_abi.lib().ifx_comm_destroy(self._h), "comm_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class BalancedPlan:
     """Ulysses re-shard for heads that do not divide the ranks, without dummy heads.
 

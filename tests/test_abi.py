@@ -3,6 +3,8 @@
 import os
 import re
 
+import pytest
+
 from conftest import ROOT
 
 from paper_2511_20714_b200 import _abi
@@ -126,3 +128,20 @@ def test_one_cublaslt_per_process():
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     paths = eval(out.stdout.strip().splitlines()[-1])
     assert len(paths) == 1, paths
+
+
+def test_native_comm_unique_id_and_validation():
+    """ifx_comm_* (the C-ABI NCCL communicator, SURVEY §8(b) ifx_comm_init): unique ids
+    are 128 fresh bytes; bad ranks / ids fail with the reference's error classes before any
+    collective (no GPU needed for these paths)."""
+    from paper_2511_20714_b200.errors import DimensionError
+    from paper_2511_20714_b200.parallel import NativeComm
+
+    a, b = NativeComm.unique_id(), NativeComm.unique_id()
+    assert len(a) == 128 and a != b
+    with pytest.raises(DimensionError):
+        NativeComm(a, 2, 2)  # rank outside [0, world)
+    with pytest.raises(DimensionError):
+        NativeComm(a, 0, 0)
+    with pytest.raises(DimensionError):
+        NativeComm(a[:64], 2, 0)

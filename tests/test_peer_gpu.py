@@ -152,3 +152,36 @@ def test_attn_combine_matches_torch(splits, hd):
     want = (o * w.permute(0, 2, 1)[..., None]).sum(0) / den.t()[..., None]
     assert torch.allclose(out.double().view(n, H, hd), want, atol=2e-2, rtol=1e-2)
     assert torch.allclose(rsum.double(), den, rtol=1e-4) and torch.allclose(rmax.double(), M)
+
+
+def test_native_comm_world1_all_to_all_and_all_gather():
+    """ifx_comm_* on one GPU (NCCL allows one rank per device, so world 1 here; the
+    multi-rank exchange is the same NCCL group call UlyssesComm.a2a_var makes): the
+    variable-size byte all-to-all and the all-gather, also inside a CUDA graph."""
+    from paper_2511_20714_b200.parallel import NativeComm
+
+    comm = NativeComm(NativeComm.unique_id(), 1, 0)
+    try:
+        send = torch.arange(1000, device="cuda", dtype=torch.float32)
+        recv = torch.zeros(1200, device="cuda")
+        comm.all_to_all(send, [1000], recv, [1000])
+        torch.cuda.synchronize()
+        assert torch.equal(recv[:1000], send) and not recv[1000:].any()
+        g = torch.zeros(64, device="cuda", dtype=torch.uint8)
+        h = torch.randint(0, 255, (64,), device="cuda", dtype=torch.uint8)  # e.g. an IPC handle
+        comm.all_gather(h, g)
+        torch.cuda.synchronize()
+        assert torch.equal(g, h)
+        s = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            graph.capture_begin()
+            comm.all_to_all(send, [1000], recv, [1000], stream=s)
+            graph.capture_end()
+        send.mul_(3)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(recv[:1000], send)
+        del graph
+    finally:
+        comm.close()
