@@ -18,8 +18,11 @@ Like make_golden.py this imports the unmodified reference from /root/reference/p
                    47th), full-tensor float64 moments, and the final cache state (zlib JSON)
   c3_deep.npz      configs[2] length: 21 blocks (20 cached, context 93,600 tokens) at
                    2 layers, 1 denoise step: per-block row subsets + moments + final state
+  c4_deep.npz      configs[3] width: the 14B shape (40 heads x 128, D = 5,120, T = 4,680) at
+                   3 layers, 2 blocks x 2 denoise steps (1.0 / 0.5): row subsets + moments
+                   + final state
 
-Timing on the 8-core build container: acceptance ~2 min, c2 ~80 min, c3 ~75 min.
+Timing on the 8-core build container: acceptance ~2 min, c2 ~80 min, c3 ~75 min, c4 8.5 min.
 """
 
 from __future__ import annotations
@@ -87,15 +90,15 @@ def gen_acceptance():
     print(f"acceptance done: {time.time() - t0:.1f}s", flush=True)
 
 
-def gen_deep(name, layers, blocks, steps, edge, stride):
+def gen_deep(name, layers, blocks, steps, edge, stride, heads=12):
     t0 = time.time()
-    mc = RE.ModelConfig(layers=layers, heads=12, head_dim=128, block_len=4680, frame_shape=(16, 16),
+    mc = RE.ModelConfig(layers=layers, heads=heads, head_dim=128, block_len=4680, frame_shape=(16, 16),
                         prompt_dim=16, weight_seed=0)
     model = RE.build_model(mc)
     eng = RE.Engine(model, RE.default_kv_config(mc, capacity_pages_device=10**8, capacity_pages_host=4096))
     rows = sample_rows(mc.block_len, edge, stride)
     out = {"rows": rows, "meta": np.frombuffer(json.dumps(dict(
-        layers=layers, heads=12, head_dim=128, block_len=4680, blocks=blocks, steps=steps,
+        layers=layers, heads=heads, head_dim=128, block_len=4680, blocks=blocks, steps=steps,
         frame_shape=[16, 16], prompt_dim=16, weight_seed=0, seed=0,
         prompt="a quiet scene", capacity_pages_device=10**8, capacity_pages_host=4096)).encode(), np.uint8)}
 
@@ -120,10 +123,12 @@ def gen_deep(name, layers, blocks, steps, edge, stride):
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["acceptance", "c2", "c3"]
+    what = sys.argv[1:] or ["acceptance", "c2", "c3", "c4"]
     if "acceptance" in what:
         gen_acceptance()
     if "c2" in what:
         gen_deep("c2_deep", layers=30, blocks=3, steps=STEPS, edge=32, stride=47)
     if "c3" in what:
         gen_deep("c3_deep", layers=2, blocks=21, steps=[1.0], edge=16, stride=293)
+    if "c4" in what:
+        gen_deep("c4_deep", layers=3, blocks=2, steps=[1.0, 0.5], edge=16, stride=97, heads=40)

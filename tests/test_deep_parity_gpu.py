@@ -11,6 +11,9 @@
 * c3_deep: configs[2]'s context length — 21 blocks (20 cached: 93,600 context tokens at the
   last block) at the 1.3B width, 2 layers, 1 denoise step — row subsets per block and the
   bit-exact page table after all 21 appends.
+* c4_deep: configs[3]'s width — the 14B shape (40 heads x 128, D = 5,120, T = 4,680) at 3
+  layers, 2 blocks x 2 denoise steps: K1 with 40 heads and the 5,120-wide projections
+  against the reference's fp32 numpy.
 
 Tolerance (north_star): max-abs <= 2e-2 and cosine > 0.999 on final latents.
 """
@@ -101,3 +104,8 @@ def test_c2_full_depth_vs_reference():
 def test_c3_context_length_vs_reference():
     """21 blocks (20 cached, 93,600 context tokens) at the 1.3B width vs the live reference."""
     _check("c3_deep")
+
+
+def test_c4_width_vs_reference():
+    """The 14B shape (40 heads, D = 5,120) at 3 layers x 2 blocks vs the live reference."""
+    _check("c4_deep")
