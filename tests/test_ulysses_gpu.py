@@ -358,3 +358,72 @@ def test_ulysses_p2p_c2_shape_vs_oracle(world):
         assert np.abs(got - want).max() <= 2e-2 and cos > 0.999, (rank, float(np.abs(got - want).max()))
         assert state == ocache.state()
         assert plan == ("whole" if world == 2 else "grouped")
+
+
+def _rank_c4(rank, world, port, q, meta, rows):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_20714_b200 import engine as E
+        from paper_2511_20714_b200.parallel import UlyssesComm, UlyssesEngine
+
+        mc = E.ModelConfig(layers=meta["layers"], heads=meta["heads"], head_dim=meta["head_dim"],
+                           block_len=meta["block_len"], frame_shape=tuple(meta["frame_shape"]),
+                           prompt_dim=meta["prompt_dim"], weight_seed=meta["weight_seed"])
+        kvc = E.default_kv_config(mc, capacity_pages_device=meta["capacity_pages_device"],
+                                  capacity_pages_host=meta["capacity_pages_host"])
+        eng = UlyssesEngine(E.build_model(mc), UlyssesComm(), kvc, p2p=True)
+        lats = eng.generate(E.GenerationRequest(meta["blocks"], E.DenoiseSchedule(meta["steps"]),
+                                                seed=meta["seed"], prompt_schedule=[(0, meta["prompt"])]))
+        out = [x.cpu().numpy()[rows] for x in lats]
+        eng.runner.release_graphs()
+        torch.cuda.synchronize()
+        q.put((rank, out, eng.cache.state(), eng.runner.xch is not None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_ulysses_p2p_c4_width_vs_reference(world):
+    """The 14B width the scaling configs name (c4: 40 heads x 128, D = 5,120, T = 4,680;
+    3 layers x 2 blocks x 2 steps) on `world` rank processes sharing cuda:0 through the
+    peer-exchange engine (10 / 5 whole heads per rank) vs the LIVE reference's latents
+    (tests/golden/c4_deep.npz): max-abs <= 2e-2, cosine > 0.999 on every block, and every
+    rank's page table equal to the reference's, bit for bit."""
+    import json
+    import zlib
+
+    import kv_differential as KD
+
+    path = os.path.join(GOLDEN, "c4_deep.npz")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/c4_deep.npz not generated")
+    g = np.load(path)
+    meta = json.loads(bytes(g["meta"]).decode())
+    rows = g["rows"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_c4, args=(r, world, port, q, meta, rows)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want_state = json.loads(zlib.decompress(bytes(g["state_z"])).decode())
+    worst = (0.0, 1.0)
+    for rank, lats, state, p2p in res:
+        assert p2p
+        for c, got in enumerate(lats):
+            want = g[f"b{c}_rows"]
+            a, b = got.ravel().astype(np.float64), want.ravel().astype(np.float64)
+            cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+            err = float(np.abs(got - want).max())
+            assert err <= 2e-2 and cos > 0.999, (rank, c, err, cos)
+            worst = (max(worst[0], err), min(worst[1], cos))
+        assert KD.canon(state) == want_state
+    print(f"c4 width, {world} ranks: worst max-abs {worst[0]:.3e}, cosine {worst[1]:.7f}; "
+          "page table bit-exact on every rank")
