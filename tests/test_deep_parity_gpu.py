@@ -46,10 +46,10 @@ def _cos(a, b):
     return float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
 
 
-def _run(g):
+def _run(g, **override):
     from paper_2511_20714_b200 import engine as E
 
-    meta = json.loads(bytes(g["meta"]).decode())
+    meta = dict(json.loads(bytes(g["meta"]).decode()), **override)
     mc = E.ModelConfig(layers=meta["layers"], heads=meta["heads"], head_dim=meta["head_dim"],
                        block_len=meta["block_len"], frame_shape=tuple(meta["frame_shape"]),
                        prompt_dim=meta["prompt_dim"], weight_seed=meta["weight_seed"])
@@ -109,3 +109,20 @@ def test_c3_context_length_vs_reference():
 def test_c4_width_vs_reference():
     """The 14B shape (40 heads, D = 5,120) at 3 layers x 2 blocks vs the live reference."""
     _check("c4_deep")
+
+
+def test_c4_width_host_tier_vs_reference():
+    """The same 14B-width run with the device tier capped at 600 pages, so most of block 1's
+    context lives on the pinned host tier (staged by the copy engines every pass, as c5 on
+    one GPU): the tiers are bookkeeping in the reference, so its latents must still match
+    (the page table differs from the fixture's by construction and is checked elsewhere
+    against the oracle)."""
+    g = _load("c4_deep")
+    meta, eng, blocks = _run(g, capacity_pages_device=600)
+    assert eng.cache.memory_stats().host_pages_used > 0
+    rows = g["rows"]
+    for b in blocks:
+        got, want = b.latent[rows], g[f"b{b.chunk_index}_rows"]
+        err, cos = float(np.abs(got - want).max()), _cos(got, want)
+        print(f"c4 host tier block {b.chunk_index}: max-abs {err:.3e} cosine {cos:.7f}")
+        assert err <= ATOL_LATENT and cos > COS_MIN
