@@ -443,6 +443,9 @@ class NativeComm:
             self._h = None
 
     def __del__(self):
+        import sys
+        if sys.is_finalizing():  # CUDA / NCCL may already be torn down at interpreter exit
+            return
         try:
             self.close()
         except Exception:
