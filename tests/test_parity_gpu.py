@@ -473,16 +473,20 @@ def test_graph_replayed_passes_equal_eager():
     assert out[True][1] == out[False][1]
 
 
-def test_engine_full_c2_shape_vs_oracle():
+@pytest.mark.parametrize("rope_grid", [None, (3, 30, 52)], ids=["plain", "rope3d"])
+def test_engine_full_c2_shape_vs_oracle(rope_grid):
     """BASELINE configs[1] at full width and block length (12 heads x 128, T = 4680 tokens =
     3 latent frames x 1560), 2 layers, 2 blocks, 2 denoise steps, the reference's PCG64
     weights and seeded noise: final latents vs the numpy oracle (fp32) within the stated
-    tolerance, page table bit-exact (about a minute of numpy on the host)."""
+    tolerance, page table bit-exact (about a minute of numpy on the host). rope3d: with
+    north_star (1)'s 3D RoPE on the (3 frames x 30 x 52) token grid — rotated in G1's QKV
+    epilogue on the GPU, by oracle/rope.py in the oracle (unpinned by the reference, which has
+    no positional encoding)."""
     from oracle import engine as OE
     from paper_2511_20714_b200 import engine as E
 
     kw = dict(layers=2, heads=12, head_dim=128, block_len=4680, frame_shape=(4, 4), prompt_dim=16,
-              weight_seed=0)
+              weight_seed=0, rope_grid=rope_grid)
     req = dict(num_blocks=2, seed=0, prompt_schedule=[(0, "a quiet scene")])
     eng = E.Engine(E.build_model(E.ModelConfig(**kw)))
     got = np.stack([b.latent for b in eng.generate(E.GenerationRequest(
@@ -491,7 +495,8 @@ def test_engine_full_c2_shape_vs_oracle():
         schedule=OE.DenoiseSchedule([1.0, 0.5]), **req))
     want = np.stack(want)
     err, cos = float(np.abs(got - want).max()), _cos(got, want)
-    print(f"c2 shape, 2 layers x 2 blocks: max-abs {err:.3e} cosine {cos:.7f}")
+    print(f"c2 shape ({'3D RoPE' if rope_grid else 'plain'}), 2 layers x 2 blocks: max-abs {err:.3e} "
+          f"cosine {cos:.7f}")
     assert err <= ATOL_LATENT and cos > 0.999
     assert eng.cache.state() == ocache.state()
 
