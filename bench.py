@@ -570,7 +570,11 @@ def run_ulysses_bench(args, c, cfgname, world, rank, local):
     # algorithmic FLOPs of this rank's share (one rollout)
     flops_rank = attn_flops_per_rollout(c) / world
     achieved = flops_rank / (attn_ms / 1e3) / 1e12 if attn_ms > 0 else None
-    # e2e: host noise (reference seeding) in, gathered latents out
+    # e2e: host noise (reference seeding) in, gathered latents out; one untimed rollout
+    # first (pinned host buffers are allocated on first use, then cached)
+    eng.generate(req, to_host=True)
+    torch.cuda.synchronize()
+    dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         host = eng.generate(req, to_host=True)  # gathered latents in pinned host memory
